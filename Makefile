@@ -1,0 +1,51 @@
+# B200 build of the Hydra shard-execution path.
+#   make            -> paper_2110_08633_b200/libhydra.so (host C++ + sm_100a kernels + C-ABI)
+#                      build/plan_dump_b200 (parity driver compiled against this build)
+#                      oracle/liboracle_gpt.so (CPU numeric oracle — test infrastructure)
+#   make ref        -> oracle/_ref/* (reference compiled from /root/reference; needs the tree)
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+NLOHMANN ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
+CUDA_INC := /usr/local/cuda/include
+PKG      := paper_2110_08633_b200
+CSRC     := $(PKG)/csrc
+B        := build
+
+CXXFLAGS  := -std=c++20 -O2 -fPIC -g -Wall -Wextra -Wno-dangling-reference -Iinclude -I$(NLOHMANN) -I$(CUDA_INC) -pthread
+NVFLAGS   := -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -gencode arch=compute_100a,code=sm_100a \
+             -Iinclude -I$(CSRC)/kernels --expt-relaxed-constexpr -Xptxas -v
+
+HOST_SRCS := $(wildcard $(CSRC)/host/*.cpp)
+EXEC_SRCS := $(wildcard $(CSRC)/exec/*.cpp)
+CAPI_SRCS := $(wildcard $(CSRC)/capi/*.cpp)
+CU_SRCS   := $(wildcard $(CSRC)/kernels/*.cu)
+HOST_OBJS := $(patsubst $(CSRC)/%.cpp,$(B)/%.o,$(HOST_SRCS) $(EXEC_SRCS) $(CAPI_SRCS))
+CU_OBJS   := $(patsubst $(CSRC)/%.cu,$(B)/%.o,$(CU_SRCS))
+HDRS      := $(wildcard include/*.h include/spillsim/*.hpp $(CSRC)/kernels/*.cuh $(CSRC)/exec/*.hpp)
+
+all: $(PKG)/libhydra.so $(B)/plan_dump_b200 oracle/liboracle_gpt.so
+
+$(B)/%.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(B)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
+
+$(PKG)/libhydra.so: $(HOST_OBJS) $(CU_OBJS)
+	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -pthread $^ -o $@ -lcuda -lcudart
+
+$(B)/plan_dump_b200: oracle/plan_dump.cpp $(PKG)/libhydra.so
+	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lhydra -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+oracle/liboracle_gpt.so: oracle/gpt_oracle.c oracle/gpt_oracle.h
+	gcc -std=c11 -O2 -fPIC -fopenmp -shared $< -o $@ -lm
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf $(B) $(PKG)/libhydra.so oracle/liboracle_gpt.so
+
+.PHONY: all ref clean
