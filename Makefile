@@ -34,7 +34,7 @@ $(B)/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 $(PKG)/libhydra.so: $(HOST_OBJS) $(CU_OBJS)
-	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -pthread $^ -o $@ -lcuda -lcudart
+	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -pthread $^ -o $@ -cudart static
 
 $(B)/plan_dump_b200: oracle/plan_dump.cpp $(PKG)/libhydra.so
 	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lhydra -Wl,-rpath,'$$ORIGIN/../$(PKG)'

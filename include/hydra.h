@@ -1,0 +1,100 @@
+/* hydra.h — C-ABI of the B200 shard-execution library (paper_2110_08633_b200/libhydra.so).
+ *
+ * The reference (spillsim, /root/reference/proj) is a C++ library with no FFI; its drop-in
+ * boundary is the C++ API re-declared under include/spillsim/*.hpp. This header is the
+ * flat C boundary beneath it, for bindings (ctypes / cgo / JNI) and for kernel-level parity
+ * tests. Plain pointers and sizes only; no torch / C++ types cross it.
+ *
+ * Conventions
+ *  - Every function returns int status: HY_OK (0) or a negative HY_E* code; the message
+ *    for the calling thread is available from hy_last_error(). Codes map 1:1 onto the
+ *    reference exception classes (proj/core/include/spillsim/errors.hpp:23-114).
+ *  - Device pointers are raw CUDA device addresses; `stream` is a cudaStream_t (NULL =
+ *    legacy default stream). The caller owns every buffer; the library never frees caller
+ *    memory. JSON results are written into caller buffers (hy_*_json take out/out_len and
+ *    return HY_E_BUFFER_SMALL with *needed set when the buffer is too small).
+ *  - Thread-compatible: distinct executors / streams may be driven from distinct threads.
+ */
+#ifndef HYDRA_H_
+#define HYDRA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  HY_OK = 0,
+  HY_E_INVALID = -1,        /* spillsim::InvalidArgument */
+  HY_E_CONFIG = -2,         /* spillsim::ConfigError */
+  HY_E_CAPACITY = -3,       /* spillsim::CapacityExhausted */
+  HY_E_BUFFER_OVERFLOW = -4,/* spillsim::BufferOverflow */
+  HY_E_INFEASIBLE = -5,     /* InfeasibleOOM / SingleLayerTooLarge / HostOOM */
+  HY_E_DEADLOCK = -6,       /* spillsim::DeadlockError */
+  HY_E_BYTE_OVERFLOW = -7,  /* spillsim::ByteOverflow */
+  HY_E_CUDA = -8,           /* CUDA runtime / driver failure (spillsim::DeviceError) */
+  HY_E_BUFFER_SMALL = -9,   /* output buffer too small; *needed holds the size */
+  HY_E_INTERNAL = -10
+};
+
+const char* hy_last_error(void);
+const char* hy_version(void);
+
+/* ---------------------------------------------------------------------------------
+ * Planning (host only). Replaces the reference entry points
+ *   parse_workload_config   config.hpp:70      materialize_jobs  config.hpp:79
+ *   build_strategy          strategies.hpp:90  run_simulation    sim.hpp:131
+ *   summarize               metrics.hpp:53     to_chrome_trace_json trace_export.hpp:28
+ * request_json: {"config": {...workload v1...}, "strategy": "sharp", "gpus": G,
+ *                "double_buffering": bool?, "trace": bool?}
+ * result: {"partitions":[...], "tasks":[...], "dispatch":[[task,device,prefetch],...],
+ *          "dispatch_hash":"...", "makespan_s":x, "report":{...}, "chrome_trace":"..."?}
+ * --------------------------------------------------------------------------------- */
+int hy_plan_json(const char* request_json, char* out, size_t out_len, size_t* needed);
+
+/* ---------------------------------------------------------------------------------
+ * Execution (real B200 run of a workload; replaces the simulated Engine, sim.cpp:146-587).
+ * request_json: {"config": {...}, "strategy": "sharp", "gpus": G, "device_ids": [..]?,
+ *                "passes": P?, "warmup_passes": W?, "mode": "plan"}
+ * result: measured trace summary, per-step losses, timings.
+ * --------------------------------------------------------------------------------- */
+int hy_execute_json(const char* request_json, char* out, size_t out_len, size_t* needed);
+
+/* ---------------------------------------------------------------------------------
+ * Kernel entry points (fp32 tensors in HBM, row-major). Used by the executor and by the
+ * GPU parity tests; each maps to one hand-written sm_100a kernel (csrc/kernels/).
+ * --------------------------------------------------------------------------------- */
+
+/* C[M,N] = beta*C + op(A) op(B)^T (+bias[N]) (+R[M,N]) with tcgen05 kind::tf32.
+ * a_mn=0: A is [M][lda] (K contiguous); a_mn=1: A is [K][lda] (M contiguous). Same for B
+ * with N. mode 0 store, 1 GELU (Hout = pre-activation), 2 GELU-backward (C = acc*gelu'(Hin)). */
+int hy_gemm(void* stream, int M, int N, int K, const float* A, long lda, int a_mn, const float* B, long ldb,
+            int b_mn, float* C, long ldc, const float* bias, const float* R, long ldr, float beta, int mode,
+            float* Hout, const float* Hin, long ldh);
+
+int hy_layernorm_fwd(void* stream, int rows, int d, const float* x, const float* g, const float* b, float* y,
+                     float* mean, float* rstd);
+int hy_layernorm_bwd(void* stream, int rows, int d, const float* x, const float* g, const float* mean,
+                     const float* rstd, const float* dy, float* dx, int accumulate_dx, float* dg, float* db,
+                     float* ws);
+int hy_attention_fwd(void* stream, int B, int T, int H, int hd, const float* qkv, float* out, float* lse);
+int hy_attention_bwd(void* stream, int B, int T, int H, int hd, const float* qkv, const float* out,
+                     const float* dout, const float* lse, float* dqkv, float* ws);
+int hy_embed_fwd(void* stream, int rows, int T, int d, const int32_t* tokens, const float* wte, const float* wpe,
+                 float* h);
+int hy_embed_bwd(void* stream, int rows, int T, int d, int V, const int32_t* tokens, const float* dh, float* dwte,
+                 float* dwpe);
+/* Softmax cross-entropy over a [rows, V] logits chunk (row stride ldl); overwrites the
+ * chunk with dlogits * grad_scale and writes row_loss[r] = logsumexp - logit[target]. */
+int hy_softmax_xent(void* stream, int rows, int V, float* logits, long ldl, const int32_t* targets,
+                    float grad_scale, float* row_loss);
+int hy_bias_grad(void* stream, int M, int N, const float* dy, long ldy, float* db, int accumulate, float* ws);
+int hy_adam(void* stream, long n, float* p, const float* g, float* m, float* v, float lr, float beta1, float beta2,
+            float eps, float weight_decay, int step);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYDRA_H_ */

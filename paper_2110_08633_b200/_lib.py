@@ -1,0 +1,83 @@
+"""ctypes binding of the C-ABI in include/hydra.h (libhydra.so, built in-tree by `make`).
+
+The library is the product: there is no Python or CPU fallback. If it is missing or fails
+to load, every entry point raises.
+"""
+import ctypes
+import json
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhydra.so")
+
+c_float_p = ctypes.POINTER(ctypes.c_float)
+
+# name -> (restype, argtypes); mirrors include/hydra.h
+_SIGS = {
+    "hy_last_error": (ctypes.c_char_p, []),
+    "hy_version": (ctypes.c_char_p, []),
+    "hy_plan_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "hy_execute_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+    "hy_gemm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,
+                               ctypes.c_int, ctypes.c_void_p, ctypes.c_long, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long, ctypes.c_float, ctypes.c_int,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_long]),
+    "hy_layernorm_fwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 6),
+    "hy_layernorm_bwd": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int] + [ctypes.c_void_p] * 6
+                         + [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "hy_attention_fwd": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int] * 4 + [ctypes.c_void_p] * 3),
+    "hy_attention_bwd": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int] * 4 + [ctypes.c_void_p] * 6),
+    "hy_embed_fwd": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p] * 4),
+    "hy_embed_bwd": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int] * 4 + [ctypes.c_void_p] * 4),
+    "hy_softmax_xent": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,
+                                       ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p]),
+    "hy_bias_grad": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,
+                                    ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "hy_adam": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_void_p] * 4
+                + [ctypes.c_float] * 5 + [ctypes.c_int]),
+}
+
+EXPORTED = sorted(_SIGS)
+
+_lib = None
+
+
+class HydraError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"hydra status {code}: {msg}")
+        self.code = code
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `make` (or __graft_entry__.build())")
+        l = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def check(code):
+    if code != 0:
+        raise HydraError(code, lib().hy_last_error().decode())
+    return code
+
+
+def call_json(fn_name, request: dict) -> dict:
+    fn = getattr(lib(), fn_name)
+    payload = json.dumps(request).encode()
+    needed = ctypes.c_size_t(0)
+    size = 1 << 20
+    while True:
+        buf = ctypes.create_string_buffer(size)
+        rc = fn(payload, buf, size, ctypes.byref(needed))
+        if rc == -9:  # HY_E_BUFFER_SMALL
+            size = needed.value + 1
+            continue
+        check(rc)
+        return json.loads(buf.value.decode())

@@ -1,0 +1,15 @@
+// Internal glue between the C-ABI and the C++ layers.
+#pragma once
+
+#include <string>
+
+namespace hy {
+
+int set_error(int code, const std::string& msg);
+int status_from_current_exception();
+
+// JSON request -> JSON result; throw spillsim exceptions on failure.
+std::string plan_json(const std::string& request);
+std::string execute_json(const std::string& request);
+
+}  // namespace hy

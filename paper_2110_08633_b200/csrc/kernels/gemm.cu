@@ -1,0 +1,308 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a (kind::tf32, fp32 in HBM).
+//
+//   warp 0      TMA producer (one elected lane): A/B tiles -> 4-stage smem ring (128B swizzle)
+//   warp 1      MMA issuer  (one elected lane): tcgen05.mma 128xBNx8 into TMEM, commit -> mbarriers
+//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> bias / residual / GELU / GELU' -> st.global
+//
+// Operands may be K-major or MN-major in global memory (the UMMA descriptor major bit),
+// so forward (X W^T), data-grad (dY W) and weight-grad (dY^T X) GEMMs all read their
+// inputs in place with no transposes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace hy {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 32;  // one 128-byte swizzle atom of fp32
+constexpr int kStages = 4;
+constexpr int kThreads = 256;
+
+template <int BN>
+struct Smem {
+  static constexpr int kABytes = BM * BK * 4;
+  static constexpr int kBBytes = BN * BK * 4;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kRing = kStages * kStageBytes;
+  static constexpr int kTotal = kRing + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+  const float u = k0 * (x + k1 * x * x * x);
+  const float t = tanhf(u);
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
+                 int N, int K, GemmEpilogue epi) {
+  using L = Smem<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kRing);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id();
+  const int tiles_m = (M + BM - 1) / BM;
+  const int tiles_n = (N + BN - 1) / BN;
+  const int n_tiles = tiles_m * tiles_n;
+  const int k_blocks = (K + BK - 1) / BK;
+
+  if (warp == 0 && elect_one()) {
+    tma_prefetch_desc(&map_a);
+    tma_prefetch_desc(&map_b);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        const int m0 = (tile % tiles_m) * BM;
+        const int n0 = (tile / tiles_m) * BN;
+        for (int kb = 0; kb < k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * L::kStageBytes;
+          uint8_t* sb = sa + L::kABytes;
+          mbar_expect_tx(&full[stage], L::kStageBytes);
+          const int k0 = kb * BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * (32 * BK * 4), &map_a, &full[stage], m0 + 32 * j, k0);
+          } else {
+            tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * (32 * BK * 4), &map_b, &full[stage], n0 + 32 * j, k0);
+          } else {
+            tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int local = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (local >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < k_blocks; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
+          const uint32_t sb = sa + L::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            // K-major: advance 8 fp32 = 32 B inside the swizzled row; SBO = 8 rows * 128 B.
+            // MN-major: advance 8 k-rows = 1024 B; LBO = one 32-element MN atom (BK rows * 128 B).
+            const uint64_t da = A_MN ? smem_desc_sw128(sa + kk * 1024, BK * 128, 1024)
+                                     : smem_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t db = B_MN ? smem_desc_sw128(sb + kk * 1024, BK * 128, 1024)
+                                     : smem_desc_sw128(sb + kk * 32, 16, 1024);
+            mma_tf32(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          mma_commit(&empty[stage]);
+          if (kb == k_blocks - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp - 4;  // TMEM lane quarter this warp may access
+    int local = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
+      const int m0 = (tile % tiles_m) * BM;
+      const int n0 = (tile / tiles_m) * BN;
+      const int acc = local & 1;
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      tc_fence_after();
+      const int row = m0 + static_cast<int>(q * 32 + lane_id());
+      const bool row_ok = row < M;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, v);
+        const int col0 = n0 + c * 32;
+        if (!row_ok || col0 >= N) continue;
+        const bool full_chunk = col0 + 32 <= N;
+        float* crow = epi.C + static_cast<long>(row) * epi.ldc + col0;
+        if (epi.mode == kEpiGeluBwd) {
+          const float* hrow = epi.Hin + static_cast<long>(row) * epi.ldhi + col0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            if (full_chunk || col0 + i < N) v[i] *= gelu_tanh_grad(hrow[i]);
+          }
+        } else {
+          if (epi.bias) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (full_chunk || col0 + i < N) v[i] += epi.bias[col0 + i];
+            }
+          }
+          if (epi.mode == kEpiGelu) {
+            float* hrow = epi.Hout + static_cast<long>(row) * epi.ldho + col0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              if (full_chunk || col0 + i < N) {
+                hrow[i] = v[i];
+                v[i] = gelu_tanh(v[i]);
+              }
+            }
+          } else {
+            if (epi.R) {
+              const float* rrow = epi.R + static_cast<long>(row) * epi.ldr + col0;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                if (full_chunk || col0 + i < N) v[i] += rrow[i];
+              }
+            }
+            if (epi.beta != 0.f) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                if (full_chunk || col0 + i < N) v[i] += epi.beta * crow[i];
+              }
+            }
+          }
+        }
+        if (full_chunk) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            *reinterpret_cast<float4*>(crow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          }
+        } else {
+          for (int i = 0; i < 32 && col0 + i < N; ++i) crow[i] = v[i];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<2 * BN>(tmem_base);
+  }
+}
+
+// ---- host side -------------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess) {
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+  });
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer`, row stride ld.
+bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long ld, int box_inner, int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
+                   const GemmEpilogue& epi) {
+  CUtensorMap ma, mb;
+  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK) : make_map(&ma, A, K, M, lda, BK, BM);
+  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK) : make_map(&mb, B, K, N, ldb, BK, BN);
+  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < sm_count() ? tiles : sm_count();
+  kern<<<grid, kThreads, Smem<BN>::kTotal, stream>>>(ma, mb, M, N, K, epi);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
+                      const float* B, long ldb, bool b_mn, const GemmEpilogue& epi) {
+  if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
+  if ((lda & 3) || (ldb & 3) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
+    return cudaErrorInvalidValue;
+  }
+  if (!a_mn && !b_mn) return launch<128, false, false>(stream, M, N, K, A, lda, B, ldb, epi);
+  if (!a_mn && b_mn) return launch<128, false, true>(stream, M, N, K, A, lda, B, ldb, epi);
+  if (a_mn && !b_mn) return launch<128, true, false>(stream, M, N, K, A, lda, B, ldb, epi);
+  return launch<128, true, true>(stream, M, N, K, A, lda, B, ldb, epi);
+}
+
+}  // namespace hy

@@ -1,0 +1,409 @@
+// HBM-bound kernels: one warp per row for row reductions (128-bit loads, warp shuffles),
+// grid-stride float4 loops for elementwise work, two-stage deterministic column sums.
+#include <cfloat>
+
+#include "ops.cuh"
+
+namespace hy {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+int sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+// ---- LayerNorm -----------------------------------------------------------------
+// One warp per row; the row lives in registers (d <= 32 * 4 * kMaxVec).
+constexpr int kMaxVecAll = 32;  // d <= 4096
+
+template <int kMaxVec>
+__global__ void ln_fwd_kernel(int rows, int d, const float* __restrict__ x, const float* __restrict__ g,
+                              const float* __restrict__ b, float* __restrict__ y, float* __restrict__ mean_out,
+                              float* __restrict__ rstd_out) {
+  const int row = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int nv = d >> 2;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long>(row) * d);
+  float4 buf[kMaxVec];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = lane + 32 * k;
+    if (i < nv) {
+      buf[k] = xr[i];
+      s += (buf[k].x + buf[k].y) + (buf[k].z + buf[k].w);
+    }
+  }
+  const float mu = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = lane + 32 * k;
+    if (i < nv) {
+      const float a = buf[k].x - mu, bb = buf[k].y - mu, c = buf[k].z - mu, e = buf[k].w - mu;
+      q += (a * a + bb * bb) + (c * c + e * e);
+    }
+  }
+  const float rs = rsqrtf(warp_sum(q) / d + 1e-5f);
+  float4* yr = reinterpret_cast<float4*>(y + static_cast<long>(row) * d);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll
+  for (int k = 0; k < kMaxVec; ++k) {
+    const int i = lane + 32 * k;
+    if (i < nv) {
+      const float4 gg = g4[i], bb = b4[i];
+      yr[i] = make_float4((buf[k].x - mu) * rs * gg.x + bb.x, (buf[k].y - mu) * rs * gg.y + bb.y,
+                          (buf[k].z - mu) * rs * gg.z + bb.z, (buf[k].w - mu) * rs * gg.w + bb.w);
+    }
+  }
+  if (lane == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = rs;
+  }
+}
+
+// dx = rstd * (dy*g - mean(dy*g) - xhat * mean(dy*g*xhat)); per-block partial dg/db.
+template <int kMaxVec>
+__global__ void ln_bwd_kernel(int rows, int d, const float* __restrict__ x, const float* __restrict__ g,
+                              const float* __restrict__ mean, const float* __restrict__ rstd,
+                              const float* __restrict__ dy, float* __restrict__ dx, int accumulate,
+                              float* __restrict__ ws_dg, float* __restrict__ ws_db, int rows_per_block) {
+  extern __shared__ float sh[];  // [warps][2][d]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_warps = blockDim.x >> 5;
+  const int nv = d >> 2;
+  float* my_dg = sh + warp * 2 * d;
+  float* my_db = my_dg + d;
+  for (int i = lane; i < d; i += 32) {
+    my_dg[i] = 0.f;
+    my_db[i] = 0.f;
+  }
+  __syncwarp();
+  const int r0 = blockIdx.x * rows_per_block;
+  const int r1 = min(rows, r0 + rows_per_block);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int row = r0 + warp; row < r1; row += n_warps) {
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long>(row) * d);
+    const float4* dyr = reinterpret_cast<const float4*>(dy + static_cast<long>(row) * d);
+    const float mu = mean[row], rs = rstd[row];
+    float4 xh[kMaxVec], gy[kMaxVec];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nv) {
+        const float4 xv = xr[i], dv = dyr[i], gv = g4[i];
+        xh[k] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        gy[k] = make_float4(dv.x * gv.x, dv.y * gv.y, dv.z * gv.z, dv.w * gv.w);
+        s1 += (gy[k].x + gy[k].y) + (gy[k].z + gy[k].w);
+        s2 += (gy[k].x * xh[k].x + gy[k].y * xh[k].y) + (gy[k].z * xh[k].z + gy[k].w * xh[k].w);
+        float* dgp = my_dg + 4 * i;
+        float* dbp = my_db + 4 * i;
+        dgp[0] += dv.x * xh[k].x;
+        dgp[1] += dv.y * xh[k].y;
+        dgp[2] += dv.z * xh[k].z;
+        dgp[3] += dv.w * xh[k].w;
+        dbp[0] += dv.x;
+        dbp[1] += dv.y;
+        dbp[2] += dv.z;
+        dbp[3] += dv.w;
+      }
+    }
+    const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) / d;
+    float4* dxr = reinterpret_cast<float4*>(dx + static_cast<long>(row) * d);
+#pragma unroll
+    for (int k = 0; k < kMaxVec; ++k) {
+      const int i = lane + 32 * k;
+      if (i < nv) {
+        float4 o = make_float4(rs * (gy[k].x - m1 - xh[k].x * m2), rs * (gy[k].y - m1 - xh[k].y * m2),
+                               rs * (gy[k].z - m1 - xh[k].z * m2), rs * (gy[k].w - m1 - xh[k].w * m2));
+        if (accumulate) {
+          const float4 p = dxr[i];
+          o.x += p.x;
+          o.y += p.y;
+          o.z += p.z;
+          o.w += p.w;
+        }
+        dxr[i] = o;
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float a = 0.f, c = 0.f;
+    for (int w = 0; w < n_warps; ++w) {
+      a += sh[w * 2 * d + i];
+      c += sh[w * 2 * d + d + i];
+    }
+    ws_dg[static_cast<long>(blockIdx.x) * d + i] = a;
+    ws_db[static_cast<long>(blockIdx.x) * d + i] = c;
+  }
+}
+
+// out[n] (+)= sum_b part[b][n], fixed order => deterministic.
+__global__ void reduce_parts_kernel(int parts, int N, const float* __restrict__ part, float* __restrict__ out,
+                                    int accumulate) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  float s = 0.f;
+  for (int b = 0; b < parts; ++b) s += part[static_cast<long>(b) * N + n];
+  out[n] = accumulate ? out[n] + s : s;
+}
+
+// Partial column sums over a row range per block; 256 threads stride the columns.
+__global__ void colsum_part_kernel(int M, int N, const float* __restrict__ X, long ldx, float* __restrict__ part,
+                                   int rows_per_block) {
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(M, r0 + rows_per_block);
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int r = r0; r < r1; ++r) s += X[static_cast<long>(r) * ldx + n];
+    part[static_cast<long>(blockIdx.y) * N + n] = s;
+  }
+}
+
+// ---- embedding -----------------------------------------------------------------
+__global__ void embed_fwd_kernel(int rows, int T, int d, const int32_t* __restrict__ tok,
+                                 const float* __restrict__ wte, const float* __restrict__ wpe, float* __restrict__ h) {
+  const int nv = d >> 2;
+  const long total = static_cast<long>(rows) * nv;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / nv), c = static_cast<int>(i % nv);
+    const float4 a = reinterpret_cast<const float4*>(wte + static_cast<long>(tok[r]) * d)[c];
+    const float4 p = reinterpret_cast<const float4*>(wpe + static_cast<long>(r % T) * d)[c];
+    reinterpret_cast<float4*>(h)[i] = make_float4(a.x + p.x, a.y + p.y, a.z + p.z, a.w + p.w);
+  }
+}
+
+__global__ void embed_scatter_kernel(int rows, int d, const int32_t* __restrict__ tok, const float* __restrict__ dh,
+                                     float* __restrict__ dwte) {
+  const long total = static_cast<long>(rows) * d;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / d), c = static_cast<int>(i % d);
+    atomicAdd(dwte + static_cast<long>(tok[r]) * d + c, dh[i]);
+  }
+}
+
+// dwpe[t][c] = sum_b dh[b*T + t][c]
+__global__ void embed_pos_kernel(int B, int T, int d, const float* __restrict__ dh, float* __restrict__ dwpe) {
+  const long total = static_cast<long>(T) * d;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int b = 0; b < B; ++b) s += dh[static_cast<long>(b) * T * d + i];
+    dwpe[i] = s;
+  }
+}
+
+// ---- softmax cross-entropy ------------------------------------------------------
+__global__ void xent_kernel(int V, float* __restrict__ logits, long ldl, const int32_t* __restrict__ targets,
+                            float grad_scale, float* __restrict__ row_loss) {
+  __shared__ float red_m[32], red_s[32];
+  const int row = blockIdx.x;
+  float* lr = logits + static_cast<long>(row) * ldl;
+  const int tid = threadIdx.x, nw = blockDim.x >> 5, warp = tid >> 5, lane = tid & 31;
+  float m = -FLT_MAX, s = 0.f;
+  for (int i = tid; i < V; i += blockDim.x) {
+    const float z = lr[i];
+    if (z > m) {
+      s = s * __expf(m - z) + 1.f;
+      m = z;
+    } else {
+      s += __expf(z - m);
+    }
+  }
+  // combine (m, s) across the block
+  float wm = warp_max(m);
+  float ws = s * __expf(m - wm);
+  ws = warp_sum(ws);
+  if (lane == 0) {
+    red_m[warp] = wm;
+    red_s[warp] = ws;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float mm = lane < nw ? red_m[lane] : -FLT_MAX;
+    float ss = lane < nw ? red_s[lane] : 0.f;
+    const float gm = warp_max(mm);
+    ss = warp_sum(lane < nw ? ss * __expf(mm - gm) : 0.f);
+    if (lane == 0) {
+      red_m[0] = gm;
+      red_s[0] = ss;
+    }
+  }
+  __syncthreads();
+  const float gm = red_m[0], gs = red_s[0];
+  const float inv = 1.f / gs;
+  const int tgt = targets[row];
+  const float zt = lr[tgt];
+  __syncthreads();
+  for (int i = tid; i < V; i += blockDim.x) {
+    const float p = __expf(lr[i] - gm) * inv;
+    lr[i] = (p - (i == tgt ? 1.f : 0.f)) * grad_scale;
+  }
+  if (tid == 0) row_loss[row] = logf(gs) + gm - zt;
+}
+
+__global__ void sum_double_kernel(int n, const float* __restrict__ x, double* __restrict__ out, int accumulate) {
+  __shared__ double sh[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] += sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = accumulate ? out[0] + sh[0] : sh[0];
+}
+
+// ---- Adam ------------------------------------------------------------------------
+__global__ void adam_kernel(long n4, float4* __restrict__ p, const float4* __restrict__ g, float4* __restrict__ m,
+                            float4* __restrict__ v, AdamHyper h) {
+  const float c1 = 1.f - h.beta1, c2 = 1.f - h.beta2;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    float4 pp = p[i], gg = g[i], mm = m[i], vv = v[i];
+    float* pe = &pp.x;
+    const float* ge = &gg.x;
+    float* me = &mm.x;
+    float* ve = &vv.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      me[k] = h.beta1 * me[k] + c1 * ge[k];
+      ve[k] = h.beta2 * ve[k] + c2 * ge[k] * ge[k];
+      const float upd = (me[k] / h.bc1) / (sqrtf(ve[k] / h.bc2) + h.eps);
+      pe[k] = pe[k] - h.lr * (upd + h.weight_decay * pe[k]);
+    }
+    p[i] = pp;
+    m[i] = mm;
+    v[i] = vv;
+  }
+}
+
+int grid_for(long n, int block) {
+  long g = (n + block - 1) / block;
+  const long cap = static_cast<long>(sms()) * 8;
+  if (g > cap) g = cap;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace
+
+int colsum_blocks(int rows) {
+  const int target = sms() * 2;
+  return rows < target ? (rows > 0 ? rows : 1) : target;
+}
+
+cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b, float* y,
+                          float* mean, float* rstd) {
+  if (d % 4 || d > 4 * 32 * kMaxVecAll) return cudaErrorInvalidValue;
+  const int grid = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock, block = 32 * kWarpsPerBlock;
+  if (d <= 1024) {
+    ln_fwd_kernel<8><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
+  } else if (d <= 2048) {
+    ln_fwd_kernel<16><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
+  } else {
+    ln_fwd_kernel<32><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* mean,
+                          const float* rstd, const float* dy, float* dx, bool accumulate_dx, float* dg, float* db,
+                          float* ws) {
+  if (d % 4 || d > 4 * 32 * kMaxVecAll) return cudaErrorInvalidValue;
+  const int nb = colsum_blocks(rows);
+  const int rpb = (rows + nb - 1) / nb;
+  const int n_warps = d <= 3072 ? kWarpsPerBlock : 4;
+  const size_t smem = static_cast<size_t>(n_warps) * 2 * d * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(ln_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(ln_bwd_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(ln_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  float* ws_dg = ws;
+  float* ws_db = ws + static_cast<long>(nb) * d;
+  const int acc = accumulate_dx ? 1 : 0;
+  if (d <= 1024) {
+    ln_bwd_kernel<8><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
+  } else if (d <= 2048) {
+    ln_bwd_kernel<16><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
+  } else {
+    ln_bwd_kernel<32><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
+  }
+  reduce_parts_kernel<<<(d + 255) / 256, 256, 0, s>>>(nb, d, ws_dg, dg, 1);
+  reduce_parts_kernel<<<(d + 255) / 256, 256, 0, s>>>(nb, d, ws_db, db, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float* out, bool accumulate, float* ws) {
+  const int nb = colsum_blocks(M);
+  const int rpb = (M + nb - 1) / nb;
+  dim3 grid((N + 255) / 256, nb);
+  colsum_part_kernel<<<grid, 256, 0, s>>>(M, N, X, ldx, ws, rpb);
+  reduce_parts_kernel<<<(N + 255) / 256, 256, 0, s>>>(nb, N, ws, out, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t embed_fwd(cudaStream_t s, int rows, int T, int d, const int32_t* tok, const float* wte, const float* wpe,
+                      float* h) {
+  if (d % 4) return cudaErrorInvalidValue;
+  const long n = static_cast<long>(rows) * (d / 4);
+  embed_fwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(rows, T, d, tok, wte, wpe, h);
+  return cudaGetLastError();
+}
+
+cudaError_t embed_bwd(cudaStream_t s, int rows, int T, int d, const int32_t* tok, const float* dh, float* dwte,
+                      float* dwpe, float* /*ws*/) {
+  const long n = static_cast<long>(rows) * d;
+  embed_scatter_kernel<<<grid_for(n, 256), 256, 0, s>>>(rows, d, tok, dh, dwte);
+  embed_pos_kernel<<<grid_for(static_cast<long>(T) * d, 256), 256, 0, s>>>(rows / T, T, d, dh, dwpe);
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_xent(cudaStream_t s, int rows, int V, float* logits, long ldl, const int32_t* targets,
+                         float grad_scale, float* row_loss) {
+  if (rows <= 0) return cudaSuccess;
+  xent_kernel<<<rows, 512, 0, s>>>(V, logits, ldl, targets, grad_scale, row_loss);
+  return cudaGetLastError();
+}
+
+cudaError_t sum_to_double(cudaStream_t s, int n, const float* x, double* out, bool accumulate) {
+  sum_double_kernel<<<1, 256, 0, s>>>(n, x, out, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t adam_update(cudaStream_t s, long n, float* p, const float* g, float* m, float* v, const AdamHyper& h) {
+  if (n % 4) return cudaErrorInvalidValue;
+  const long n4 = n / 4;
+  adam_kernel<<<grid_for(n4, 256), 256, 0, s>>>(n4, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+                                                reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), h);
+  return cudaGetLastError();
+}
+
+}  // namespace hy

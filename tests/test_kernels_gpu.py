@@ -1,0 +1,178 @@
+"""GPU parity of each sm_100a kernel against a plain PyTorch fp32 reference of the op.
+
+Tolerances: the GEMM runs tcgen05 kind::tf32 (10-bit mantissa inputs, fp32 accumulate),
+so GEMM-derived outputs are checked with relative Frobenius error <= 3e-3 against fp32;
+everything else is fp32 CUDA-core math checked at <= 1e-4 relative (1e-5 absolute).
+"""
+import math
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2110_08633_b200 import kernels as K  # noqa: E402
+
+dev = torch.device("cuda:0")
+torch.backends.cuda.matmul.allow_tf32 = False
+
+
+def rel(a, b):
+    return ((a - b).norm() / (b.norm() + 1e-30)).item()
+
+
+SHAPES = [(128, 128, 32), (256, 384, 768), (300, 200, 96), (1024, 2304, 768), (4096, 768, 3072), (64, 1000, 64),
+          (96, 520, 40)]
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_majors(shape, a_mn, b_mn):
+    M, N, Kd = shape
+    torch.manual_seed(M + N + Kd)
+    A = torch.randn(M, Kd, device=dev)
+    B = torch.randn(N, Kd, device=dev)
+    ref = A @ B.T
+    Ain = A.T.contiguous() if a_mn else A
+    Bin = B.T.contiguous() if b_mn else B
+    C = K.gemm(Ain, Bin, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=Kd)
+    torch.cuda.synchronize()
+    assert rel(C, ref) < 3e-3, (shape, a_mn, b_mn, rel(C, ref))
+
+
+def test_gemm_epilogues():
+    M, N, Kd = 512, 640, 256
+    A = torch.randn(M, Kd, device=dev)
+    B = torch.randn(N, Kd, device=dev) * 0.05
+    bias = torch.randn(N, device=dev)
+    R = torch.randn(M, N, device=dev)
+    C0 = torch.randn(M, N, device=dev)
+    base = A @ B.T
+    C = K.gemm(A, B, bias=bias, R=R)
+    assert rel(C, base + bias + R) < 3e-3
+    C2 = C0.clone()
+    K.gemm(A, B, C=C2, beta=1.0)
+    assert rel(C2, C0 + base) < 3e-3
+    H = torch.empty(M, N, device=dev)
+    G = K.gemm(A, B, bias=bias, mode=1, H=H)
+    pre = base + bias
+    assert rel(H, pre) < 3e-3
+    assert rel(G, torch.nn.functional.gelu(pre, approximate="tanh")) < 3e-3
+    Hin = torch.randn(M, N, device=dev)
+    D = K.gemm(A, B, mode=2, H=Hin)
+    x = Hin.clone().requires_grad_(True)
+    torch.nn.functional.gelu(x, approximate="tanh").backward(torch.ones_like(x))
+    assert rel(D, base * x.grad) < 3e-3
+
+
+def test_gemm_vocab_head_shapes():
+    rows, d, V, Vp = 256, 128, 50257, 50304
+    z = torch.randn(rows, d, device=dev)
+    wte = torch.randn(V, d, device=dev) * 0.02
+    logits = torch.zeros(rows, Vp, device=dev)
+    K.gemm(z, wte, C=logits, M=rows, N=V, K=d, ldc=Vp)
+    assert rel(logits[:, :V], z @ wte.T) < 3e-3
+    assert logits[:, V:].abs().max().item() == 0
+    # dz = dlogits @ wte (A K-major with K = V ragged; B MN-major)
+    dl = torch.randn(rows, Vp, device=dev)
+    dl[:, V:] = 0
+    dz = K.gemm(dl, wte, a_mn=False, b_mn=True, M=rows, N=d, K=V, lda=Vp)
+    assert rel(dz, dl[:, :V] @ wte) < 3e-3
+    # dwte = dlogits^T @ z (both MN-major), M = V ragged
+    dwte = torch.zeros(V, d, device=dev)
+    K.gemm(dl, z, a_mn=True, b_mn=True, M=V, N=d, K=rows, lda=Vp, C=dwte)
+    assert rel(dwte, dl[:, :V].T @ z) < 3e-3
+
+
+@pytest.mark.parametrize("d", [64, 768, 1600, 4096])
+def test_layernorm(d):
+    rows = 333
+    x = torch.randn(rows, d, device=dev) * 3 + 1
+    g = torch.randn(d, device=dev)
+    b = torch.randn(d, device=dev)
+    y, mean, rstd = K.layernorm_fwd(x, g, b)
+    ref = torch.nn.functional.layer_norm(x, (d,), g, b, 1e-5)
+    assert rel(y, ref) < 1e-5
+    xr = x.clone().requires_grad_(True)
+    gr = g.clone().requires_grad_(True)
+    br = b.clone().requires_grad_(True)
+    dy = torch.randn(rows, d, device=dev)
+    torch.nn.functional.layer_norm(xr, (d,), gr, br, 1e-5).backward(dy)
+    prior = torch.randn(rows, d, device=dev)
+    dx, dg, db = K.layernorm_bwd(x, g, mean, rstd, dy, dx=prior.clone(), accumulate=True)
+    assert rel(dx, xr.grad + prior) < 1e-5
+    assert rel(dg, gr.grad) < 1e-5
+    assert rel(db, br.grad) < 1e-5
+
+
+def ref_attention(qkv, B, T, H):
+    D = H * 64
+    q, k, v = qkv.view(B, T, 3, H, 64).permute(2, 0, 3, 1, 4)
+    att = (q @ k.transpose(-1, -2)) / 8.0
+    mask = torch.ones(T, T, device=qkv.device, dtype=torch.bool).tril()
+    att = att.masked_fill(~mask, float("-inf")).softmax(-1)
+    return (att @ v).permute(0, 2, 1, 3).reshape(B * T, D)
+
+
+@pytest.mark.parametrize("B,T,H", [(2, 32, 1), (2, 100, 3), (1, 512, 2), (4, 128, 12)])
+def test_attention(B, T, H):
+    torch.manual_seed(T)
+    qkv = torch.randn(B * T, 3 * H * 64, device=dev)
+    out, lse = K.attention_fwd(qkv, B, T, H)
+    qr = qkv.clone().requires_grad_(True)
+    ref = ref_attention(qr, B, T, H)
+    assert rel(out, ref) < 1e-4
+    dout = torch.randn_like(out)
+    ref.backward(dout)
+    dqkv = K.attention_bwd(qkv, out, dout, lse, B, T, H)
+    assert rel(dqkv, qr.grad) < 1e-4
+
+
+def test_embedding():
+    V, d, B, T = 1000, 128, 3, 40
+    tok = torch.randint(0, V, (B * T,), device=dev, dtype=torch.int32)
+    tok[:10] = 5  # collisions
+    wte = torch.randn(V, d, device=dev)
+    wpe = torch.randn(T, d, device=dev)
+    h = K.embed_fwd(tok, wte, wpe, T)
+    pos = torch.arange(B * T, device=dev) % T
+    assert rel(h, wte[tok.long()] + wpe[pos]) < 1e-6
+    dh = torch.randn(B * T, d, device=dev)
+    dwte, dwpe = K.embed_bwd(tok, dh, V, T)
+    ref_wte = torch.zeros(V, d, device=dev).index_add_(0, tok.long(), dh)
+    assert rel(dwte, ref_wte) < 1e-5
+    assert rel(dwpe, dh.view(B, T, d).sum(0)) < 1e-5
+
+
+def test_softmax_xent():
+    rows, V, Vp = 77, 50257, 50304
+    logits = torch.randn(rows, Vp, device=dev) * 3
+    tgt = torch.randint(0, V, (rows,), device=dev, dtype=torch.int32)
+    lr = logits[:, :V].clone().requires_grad_(True)
+    loss = torch.nn.functional.cross_entropy(lr, tgt.long(), reduction="none")
+    loss.sum().backward()
+    scale = 1.0 / 300
+    row_loss = K.softmax_xent(logits, tgt, V, scale)
+    assert rel(row_loss, loss.detach()) < 1e-5
+    assert rel(logits[:, :V], lr.grad * scale) < 1e-4
+
+
+def test_bias_grad_and_adam():
+    dy = torch.randn(3000, 700, device=dev)
+    assert rel(K.bias_grad(dy), dy.sum(0)) < 1e-5
+    n = 1 << 16
+    p = torch.randn(n, device=dev)
+    g = torch.randn(n, device=dev)
+    m = torch.zeros(n, device=dev)
+    v = torch.zeros(n, device=dev)
+    pr = p.clone().requires_grad_(True)
+    opt = torch.optim.Adam([pr], lr=1e-3, betas=(0.9, 0.999), eps=1e-8)
+    for step in range(1, 4):
+        K.adam(p, g, m, v, 1e-3, step)
+        pr.grad = g.clone()
+        opt.step()
+    assert rel(p, pr.detach()) < 1e-6
