@@ -135,10 +135,11 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
             // K-major: advance 8 fp32 = 32 B inside the swizzled row; SBO = 8 rows * 128 B.
-            // MN-major: advance 8 k-rows = 1024 B; LBO = one 32-element MN atom (BK rows * 128 B).
-            const uint64_t da = A_MN ? smem_desc_sw128(sa + kk * 1024, BK * 128, 1024)
+            // MN-major: advance 8 k-rows = 1024 B; LBO = one 32-element MN column (BK rows * 128 B),
+            // SBO = 4 k-rows (512 B) of the 32-byte-atom swizzle.
+            const uint64_t da = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
                                      : smem_desc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t db = B_MN ? smem_desc_sw128(sb + kk * 1024, BK * 128, 1024)
+            const uint64_t db = B_MN ? smem_desc_sw128_b32(sb + kk * 1024, BK * 128, 512)
                                      : smem_desc_sw128(sb + kk * 32, 16, 1024);
             mma_tf32(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
@@ -248,7 +249,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer`, row stride ld.
-bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long ld, int box_inner, int box_outer) {
+bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long ld, int box_inner, int box_outer,
+              bool mn_major) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
@@ -256,7 +258,9 @@ bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long l
   cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -275,8 +279,8 @@ template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
                    const GemmEpilogue& epi) {
   CUtensorMap ma, mb;
-  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK) : make_map(&ma, A, K, M, lda, BK, BM);
-  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK) : make_map(&mb, B, K, N, ldb, BK, BN);
+  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true) : make_map(&ma, A, K, M, lda, BK, BM, false);
+  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true) : make_map(&mb, B, K, N, ldb, BK, BN, false);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
   auto kern = gemm_tf32_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;  // per instantiation

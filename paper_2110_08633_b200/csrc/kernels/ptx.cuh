@@ -121,6 +121,14 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr, uint32_t lbo
   return d;
 }
 
+// MN-major fp32/tf32 operands need "128B swizzle with 32-byte atoms" (layout type 1,
+// cute Layout_MN_SW128_32B_Atom; TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): atoms of
+// 32 MN elements x 4 k-rows (512 B). LBO = MN-atom stride, SBO = 4-row k-group stride.
+__device__ __forceinline__ uint64_t smem_desc_sw128_b32(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = smem_desc_sw128(saddr, lbo_bytes, sbo_bytes);
+  return (d & ~(7ull << 61)) | (1ull << 61);
+}
+
 // Instruction descriptor for kind::tf32, fp32 accumulate.
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4)                          // D format F32
