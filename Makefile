@@ -4,14 +4,14 @@
 #                      oracle/liboracle_gpt.so (CPU numeric oracle — test infrastructure)
 #   make ref        -> oracle/_ref/* (reference compiled from /root/reference; needs the tree)
 NVCC     ?= /usr/local/cuda/bin/nvcc
-CXX      ?= g++
+CXX      := /usr/bin/g++
 NLOHMANN ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty
 CUDA_INC := /usr/local/cuda/include
 PKG      := paper_2110_08633_b200
 CSRC     := $(PKG)/csrc
 B        := build
 
-CXXFLAGS  := -std=c++20 -O2 -fPIC -g -Wall -Wextra -Wno-dangling-reference -Iinclude -I$(NLOHMANN) -I$(CUDA_INC) -pthread
+CXXFLAGS  := -std=c++20 -O2 -fPIC -g -Wall -Wextra -Wno-dangling-reference -Wno-unused-parameter -Iinclude -I$(NLOHMANN) -I$(CUDA_INC) -pthread -fopenmp
 NVFLAGS   := -std=c++17 -O3 -lineinfo -Xcompiler -fPIC -gencode arch=compute_100a,code=sm_100a \
              -Iinclude -I$(CSRC)/kernels --expt-relaxed-constexpr -Xptxas -v
 
@@ -34,7 +34,7 @@ $(B)/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 $(PKG)/libhydra.so: $(HOST_OBJS) $(CU_OBJS)
-	$(NVCC) -shared -gencode arch=compute_100a,code=sm_100a -Xcompiler -pthread $^ -o $@ -cudart static
+	$(CXX) -shared $^ -o $@ -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -pthread -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp
 
 $(B)/plan_dump_b200: oracle/plan_dump.cpp $(PKG)/libhydra.so
 	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lhydra -Wl,-rpath,'$$ORIGIN/../$(PKG)'

@@ -1,7 +1,7 @@
 /* hydra.h — C-ABI of the B200 shard-execution library (paper_2110_08633_b200/libhydra.so).
  *
  * The reference (spillsim, /root/reference/proj) is a C++ library with no FFI; its drop-in
- * boundary is the C++ API re-declared under include/spillsim/*.hpp. This header is the
+ * boundary is the C++ API re-declared under include/spillsim/ (*.hpp). This header is the
  * flat C boundary beneath it, for bindings (ctypes / cgo / JNI) and for kernel-level parity
  * tests. Plain pointers and sizes only; no torch / C++ types cross it.
  *

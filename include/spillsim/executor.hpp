@@ -1,0 +1,59 @@
+// Real B200 execution of a compiled strategy — the B200 build's replacement for the
+// reference's simulated Engine (proj/core/src/sim.cpp:146-587). Same inputs as
+// run_simulation (cluster, tasks, scheduler via its dispatch plan, options) plus the real
+// model of every job; returns the same SimTrace type with CUDA-event timestamps, so
+// summarize() and to_chrome_trace_json() apply unchanged.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "hydra_gpt.h"
+#include "spillsim/sim.hpp"
+
+namespace spillsim {
+
+struct ExecJob {
+  hy_dims dims{};              // the real GPT-2 (include/hydra_gpt.h)
+  uint64_t model_key = 0;      // init stream (jobs of one model share it)
+  float lr = 1e-4f;
+  float beta1 = 0.9f, beta2 = 0.999f, eps = 1e-8f, weight_decay = 0.f;
+  std::vector<int> shard_starts;  // from the partitioner (layer indices)
+};
+
+struct ExecOptions {
+  std::vector<ExecJob> jobs;       // indexed like ShardTask::job
+  std::vector<int> device_ids;     // plan device -> CUDA ordinal (default: identity)
+  std::vector<int> run_devices;    // plan devices executed by this process (default: all)
+  uint64_t seed = 0;               // synthetic tokens
+  int passes = 1;                  // times the whole plan is replayed (minibatch index continues)
+  int warmup_passes = 0;           // replays before the timed ones (not in the trace)
+  long opt_chunk_floats = 4L << 20;  // Adam m/v streaming chunk
+  std::string params_out_dir;      // if set: final params of every executed job as job<j>.f32
+};
+
+struct ExecStats {
+  double makespan_s = 0;           // timed passes, max over executed devices
+  double h2d_bytes = 0, d2h_bytes = 0;            // physical, timed passes
+  double model_h2d_bytes = 0, model_d2h_bytes = 0;  // cost-model bytes of the executed tasks
+  double param_h2d_bytes = 0, opt_h2d_bytes = 0, opt_d2h_bytes = 0, act_h2d_bytes = 0, act_d2h_bytes = 0;
+  double elided_param_bytes = 0, elided_act_bytes = 0;
+  std::vector<double> arena_bytes;  // per executed device: HBM reserved (<= mem_bytes)
+  std::vector<double> device_busy_s;
+  std::vector<double> pinned_bytes;
+  int kernel_launches = 0;
+  double setup_s = 0;
+};
+
+struct ExecResult {
+  SimTrace trace;                              // measured, last timed pass
+  std::vector<std::vector<double>> losses;     // [job][global minibatch] (executed jobs)
+  std::vector<double> pass_seconds;            // per timed pass (max over devices)
+  ExecStats stats;
+};
+
+ExecResult run_execution(const ClusterSpec& cluster, const std::vector<SimTask>& tasks, const DispatchPlan& plan,
+                         const SimOptions& options, const ExecOptions& exec);
+
+}  // namespace spillsim

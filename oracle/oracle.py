@@ -120,3 +120,46 @@ def sharded_step(m, params, mom, var, starts, step, lr, tok, tgt):
         g = shard_bwd(m, params, grads, bounds[s], bounds[s + 1], tok, tgt, ckpt, g)
     adam(params, grads, mom, var, lr, step)
     return loss
+
+
+M64 = (1 << 64) - 1
+
+
+def mix64(x):
+    """splitmix64 finalizer (include/hydra_gpt.h hy_mix64)."""
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M64
+    return x ^ (x >> 31)
+
+
+def model_key(config_seed, model_index):
+    """Init stream of config.models[model_index] (csrc/capi/execute.cpp exec_job_for)."""
+    return mix64((config_seed * 0x100000001B3 + model_index) & M64)
+
+
+def run_workload_cpu(config, shard_starts, max_minibatches=None, jobs=None):
+    """Execute every job of a workload config on the CPU oracle in the SHARP chain order
+    (per job: minibatches in order, each F(0..k-1), B(k-1..0), Adam). Returns
+    (losses[job][mb], params[job])."""
+    names = [m["name"] for m in config["models"]]
+    seed = int(config.get("seed", 0))
+    losses, params_out = {}, {}
+    for j, job in enumerate(config["jobs"]):
+        if jobs is not None and j not in jobs:
+            continue
+        mi = names.index(job["model"])
+        g = config["models"][mi]["generator"]
+        m = make_dims(d=g["d_model"], L=g["n_blocks"], T=g["seq_len"], B=g["batch_size"])
+        p = init_params(m, model_key(seed, mi))
+        mom, var = np.zeros_like(p), np.zeros_like(p)
+        lr = float(job.get("hyperparams", {}).get("lr", "0.0001"))
+        n_mb = job.get("epochs", 1) * job.get("minibatches_per_epoch", 1)
+        if max_minibatches is not None:
+            n_mb = min(n_mb, max_minibatches)
+        ls = []
+        for mb in range(n_mb):
+            tok, tgt = tokens(m, seed, j, mb)
+            ls.append(sharded_step(m, p, mom, var, shard_starts[j], mb + 1, lr, tok, tgt))
+        losses[j], params_out[j] = ls, p
+    return losses, params_out

@@ -1,0 +1,938 @@
+// Plan-mode B200 executor: replays the virtual engine's dispatch plan on real GPUs.
+//
+// One host worker thread per GPU enqueues its task list asynchronously on four streams:
+//   down    ParamLoad + ActPromote  (H2D, pinned host -> HBM; the reference's down channel)
+//   comp    shard forward / recompute+backward / fused Adam (sm_100a kernels)
+//   up      ActDemote + GradOffload (D2H; updated params + optimizer state write-back)
+//   opt     optimizer-state promote (Adam m,v chunks, H2D) — kept off the down FIFO so the
+//           next shard's prefetch is never queued behind it
+// Double buffering falls out of the stream structure: task t+1's ParamLoad is enqueued right
+// after task t's compute and runs on the copy engine while t computes (slot t+1 only waits
+// for slot t-1's last reader). Every buffer shared between streams carries a hazard tracker
+// (last-writer / last-reader-per-stream CUDA events), so no host-side synchronisation is
+// needed inside a pass. Physical optimisations that keep the plan unchanged: a ParamLoad is
+// skipped when the slot already holds that shard at the current version (B(k-1) after
+// F(k-1) — the reference's elision, sim.cpp:356-365 — and F(0) of the next minibatch after
+// B(0)); an ActPromote is skipped when the producer's output is still resident on this GPU.
+#include "spillsim/executor.hpp"
+
+#include <cuda_runtime.h>
+#include <omp.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+
+#include "../kernels/ops.cuh"
+#include "gpt_runner.hpp"
+#include "spillsim/errors.hpp"
+
+namespace spillsim {
+namespace {
+
+using hy::check_cuda;
+using hy::ShardGeom;
+
+constexpr int kStaging = 2;
+
+cudaEvent_t new_event(bool timing) {
+  cudaEvent_t e;
+  check_cuda(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming), "event create");
+  return e;
+}
+
+int device_of_stream(cudaStream_t s) {
+  int dev = 0;
+  check_cuda(cudaStreamGetDevice(s, &dev), "stream device");
+  return dev;
+}
+
+// Hazard tracker for one buffer accessed from several streams (possibly several GPUs).
+struct Tracked {
+  std::mutex mu;
+  cudaStream_t writer = nullptr;
+  std::map<cudaStream_t, cudaEvent_t> write_ev, read_ev;
+  std::map<cudaStream_t, bool> read_live;
+
+  cudaEvent_t ev(std::map<cudaStream_t, cudaEvent_t>& m, cudaStream_t s) {
+    auto it = m.find(s);
+    if (it != m.end()) return it->second;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    const int dev = device_of_stream(s);
+    if (dev != cur) cudaSetDevice(dev);
+    cudaEvent_t e = new_event(false);
+    if (dev != cur) cudaSetDevice(cur);
+    m[s] = e;
+    return e;
+  }
+  void before_write(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& kv : read_live) {
+      if (kv.second && kv.first != s) check_cuda(cudaStreamWaitEvent(s, read_ev[kv.first], 0), "wait read");
+    }
+    if (writer && writer != s) check_cuda(cudaStreamWaitEvent(s, write_ev[writer], 0), "wait write");
+  }
+  void after_write(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    check_cuda(cudaEventRecord(ev(write_ev, s), s), "record write");
+    writer = s;
+    for (auto& kv : read_live) kv.second = false;
+  }
+  void before_read(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    if (writer && writer != s) check_cuda(cudaStreamWaitEvent(s, write_ev[writer], 0), "wait write");
+  }
+  void after_read(cudaStream_t s) {
+    std::lock_guard<std::mutex> g(mu);
+    check_cuda(cudaEventRecord(ev(read_ev, s), s), "record read");
+    read_live[s] = true;
+  }
+  void destroy() {
+    for (auto& kv : write_ev) cudaEventDestroy(kv.second);
+    for (auto& kv : read_ev) cudaEventDestroy(kv.second);
+    write_ev.clear();
+    read_ev.clear();
+  }
+};
+
+struct Tag {
+  int job = -1, gmb = -1, idx = -1, ver = -1;
+  bool operator==(const Tag& o) const { return job == o.job && gmb == o.gmb && idx == o.idx && ver == o.ver; }
+};
+
+struct HostJob {
+  const ExecJob* spec = nullptr;
+  hy_dims m{};
+  long M = 0, n_act = 0, total = 0;
+  std::vector<ShardGeom> geom;
+  float *params = nullptr, *mom = nullptr, *var = nullptr, *z = nullptr;
+  std::vector<float*> ckpt, grad;  // per boundary 0..k-2
+  int32_t *tokens = nullptr, *targets = nullptr;  // [n_gmb][M]
+  int n_gmb = 0;
+  std::vector<std::unique_ptr<Tracked>> params_tr, mv_tr, ckpt_tr, grad_tr;
+  std::unique_ptr<Tracked> z_tr;
+  std::vector<int> version;  // per shard: Adam updates applied
+};
+
+struct TaskTiming {
+  cudaEvent_t pl0 = nullptr, pl1 = nullptr, pr0 = nullptr, pr1 = nullptr, c0 = nullptr, c1 = nullptr,
+              d0 = nullptr, d1 = nullptr;
+  bool loaded = false, promoted = false, demoted = false;
+};
+
+
+}  // namespace
+
+struct ExecutorImpl;
+
+namespace {
+
+struct Worker {
+  ExecutorImpl* ex = nullptr;
+  int plan_dev = 0, cuda_dev = 0;
+  std::vector<int> tasks;  // plan order
+  cudaStream_t comp{}, down{}, up{}, opt{};
+  char* arena = nullptr;
+  long arena_bytes = 0;
+  float* slot[2] = {nullptr, nullptr};
+  Tag slot_tag[2];
+  Tracked slot_tr[2];
+  float* gbuf = nullptr;
+  Tracked gbuf_tr;
+  float* abuf[2] = {nullptr, nullptr};
+  Tag abuf_tag[2];
+  Tracked abuf_tr[2];
+  float* gbd[2] = {nullptr, nullptr};
+  Tag gbd_tag[2];
+  Tracked gbd_tr[2];
+  float* zbuf = nullptr;
+  Tag z_tag;
+  Tracked z_tr;
+  int32_t* tok[2] = {nullptr, nullptr};
+  Tag tok_tag[2];
+  Tracked tok_tr[2];
+  float* stg[kStaging] = {nullptr, nullptr};
+  Tracked stg_tr[kStaging];
+  float* scratch = nullptr;
+  double* loss_dev = nullptr;  // per task slot
+  int last_slot = -1;
+  int last_tok = 1;
+  bool stg_alias = false;
+  long stg_chunk = 0;
+  std::vector<TaskTiming> timing;  // per local task index
+  cudaEvent_t t0 = nullptr, t_end = nullptr;
+  cudaEvent_t join[3] = {nullptr, nullptr, nullptr};
+  ExecStats st;  // per pass accumulation (bytes)
+};
+
+}  // namespace
+
+struct ExecutorImpl {
+  const ClusterSpec& cluster;
+  const std::vector<SimTask>& tasks;
+  const DispatchPlan& plan;
+  const SimOptions& options;
+  const ExecOptions& exec;
+  std::map<int, HostJob> jobs;  // executed jobs
+  std::vector<std::unique_ptr<Worker>> workers;
+  std::vector<int> task_local;    // task -> local index on its worker
+  std::vector<int> task_device;   // task -> plan device
+  int mb_per_job_max = 0;
+  std::vector<int> job_mb;        // minibatches per job per pass
+  double* host_loss = nullptr;    // [task] per pass (pinned)
+  // cross-device ordering: task enqueued flags
+  std::mutex flag_mu;
+  std::condition_variable flag_cv;
+  std::vector<int> enqueued_pass;  // per task: last pass enqueued
+
+  ExecutorImpl(const ClusterSpec& c, const std::vector<SimTask>& t, const DispatchPlan& p, const SimOptions& o,
+               const ExecOptions& e)
+      : cluster(c), tasks(t), plan(p), options(o), exec(e) {}
+  ~ExecutorImpl();
+
+  void setup(ExecResult& res);
+  void setup_host_job(int j);
+  void setup_worker(Worker& w);
+  void run_pass(int pass, bool timed, ExecResult& res);
+  void enqueue_task(Worker& w, int t, int pass);
+  void adam_writeback(Worker& w, HostJob& hj, int s, int slot, int step, int local);
+  void collect(int pass, ExecResult& res);
+};
+
+ExecutorImpl::~ExecutorImpl() {
+  for (auto& wp : workers) {
+    Worker& w = *wp;
+    cudaSetDevice(w.cuda_dev);
+    cudaDeviceSynchronize();
+    for (auto& tm : w.timing) {
+      for (cudaEvent_t e : {tm.pl0, tm.pl1, tm.pr0, tm.pr1, tm.c0, tm.c1, tm.d0, tm.d1}) {
+        if (e) cudaEventDestroy(e);
+      }
+    }
+    for (int i = 0; i < 2; ++i) {
+      w.slot_tr[i].destroy();
+      w.abuf_tr[i].destroy();
+      w.gbd_tr[i].destroy();
+      w.tok_tr[i].destroy();
+    }
+    for (int i = 0; i < kStaging; ++i) w.stg_tr[i].destroy();
+    w.gbuf_tr.destroy();
+    w.z_tr.destroy();
+    for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2]}) {
+      if (e) cudaEventDestroy(e);
+    }
+    if (w.arena) cudaFree(w.arena);
+    for (cudaStream_t s : {w.comp, w.down, w.up, w.opt}) {
+      if (s) cudaStreamDestroy(s);
+    }
+  }
+  for (auto& kv : jobs) {
+    HostJob& hj = kv.second;
+    for (auto& t : hj.params_tr) t->destroy();
+    for (auto& t : hj.mv_tr) t->destroy();
+    for (auto& t : hj.ckpt_tr) t->destroy();
+    for (auto& t : hj.grad_tr) t->destroy();
+    if (hj.z_tr) hj.z_tr->destroy();
+    for (void* p : {static_cast<void*>(hj.params), static_cast<void*>(hj.mom), static_cast<void*>(hj.var),
+                    static_cast<void*>(hj.z), static_cast<void*>(hj.tokens), static_cast<void*>(hj.targets)}) {
+      if (p) cudaFreeHost(p);
+    }
+    for (float* p : hj.ckpt) cudaFreeHost(p);
+    for (float* p : hj.grad) cudaFreeHost(p);
+  }
+  if (host_loss) cudaFreeHost(host_loss);
+}
+
+namespace {
+
+void* pinned(size_t bytes) {
+  void* p = nullptr;
+  check_cuda(cudaHostAlloc(&p, bytes ? bytes : 4, cudaHostAllocPortable), "cudaHostAlloc");
+  return p;
+}
+
+}  // namespace
+
+void ExecutorImpl::setup_host_job(int j) {
+  HostJob& hj = jobs[j];
+  const ExecJob& spec = exec.jobs.at(static_cast<size_t>(j));
+  hj.spec = &spec;
+  hj.m = spec.dims;
+  hj.M = static_cast<long>(hj.m.B) * hj.m.T;
+  hj.n_act = hj.M * hj.m.d;
+  hj.total = hy_total_floats(&hj.m);
+  const int n_layers = hj.m.L + 2;
+  const std::vector<int>& starts = spec.shard_starts;
+  const int k = static_cast<int>(starts.size());
+  for (int s = 0; s < k; ++s) {
+    hj.geom.push_back(hy::shard_geom(hj.m, starts[static_cast<size_t>(s)],
+                                     s + 1 < k ? starts[static_cast<size_t>(s) + 1] : n_layers));
+  }
+  hj.params = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.total)));
+  hj.mom = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.total)));
+  hj.var = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.total)));
+  // GPT-2 init, layers in parallel (each layer's stream is independent of the others).
+#pragma omp parallel for schedule(dynamic)
+  for (int l = 0; l < n_layers; ++l) hy_init_layer(&hj.m, spec.model_key, l, hj.params + hy_layer_offset(&hj.m, l));
+  std::memset(hj.mom, 0, sizeof(float) * static_cast<size_t>(hj.total));
+  std::memset(hj.var, 0, sizeof(float) * static_cast<size_t>(hj.total));
+  for (int b = 0; b + 1 < k; ++b) {
+    hj.ckpt.push_back(static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.n_act))));
+    hj.grad.push_back(static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.n_act))));
+    hj.ckpt_tr.emplace_back(new Tracked);
+    hj.grad_tr.emplace_back(new Tracked);
+  }
+  hj.z = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.n_act)));
+  hj.z_tr.reset(new Tracked);
+  for (int s = 0; s < k; ++s) {
+    hj.params_tr.emplace_back(new Tracked);
+    hj.mv_tr.emplace_back(new Tracked);
+  }
+  hj.version.assign(static_cast<size_t>(k), 0);
+  hj.n_gmb = job_mb[static_cast<size_t>(j)] * (exec.passes + exec.warmup_passes);
+  hj.tokens = static_cast<int32_t*>(pinned(sizeof(int32_t) * static_cast<size_t>(hj.M * hj.n_gmb)));
+  hj.targets = static_cast<int32_t*>(pinned(sizeof(int32_t) * static_cast<size_t>(hj.M * hj.n_gmb)));
+#pragma omp parallel for schedule(static)
+  for (int g = 0; g < hj.n_gmb; ++g) {
+    for (int r = 0; r < hj.m.B; ++r) {
+      for (int t = 0; t < hj.m.T; ++t) {
+        const long i = static_cast<long>(g) * hj.M + static_cast<long>(r) * hj.m.T + t;
+        hj.tokens[i] = hy_token(exec.seed, j, g, r, t);
+        hj.targets[i] = hy_token(exec.seed, j, g, r, t + 1);
+      }
+    }
+  }
+}
+
+void ExecutorImpl::setup_worker(Worker& w) {
+  check_cuda(cudaSetDevice(w.cuda_dev), "set device");
+  check_cuda(cudaStreamCreateWithFlags(&w.comp, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithFlags(&w.down, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithFlags(&w.up, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithFlags(&w.opt, cudaStreamNonBlocking), "stream");
+  // Size the arena from the tasks this GPU will run.
+  long slot_f = 0, grad_f = 0, act_f = 0, scratch_f = 0, tok_n = 0;
+  for (int t : w.tasks) {
+    const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
+    const ShardGeom& g = hj.geom[static_cast<size_t>(tasks[static_cast<size_t>(t)].t.shard)];
+    slot_f = std::max(slot_f, g.slot_floats);
+    grad_f = std::max(grad_f, g.param_floats);
+    act_f = std::max(act_f, hj.n_act);
+    tok_n = std::max(tok_n, hj.M);
+    int max_blocks = 0;
+    for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
+    scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, max_blocks));
+  }
+  const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(grad_f) + 5 * hy_pad32(act_f) +
+                           2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
+                           hy_pad32(2 * static_cast<long>(w.tasks.size()) + 2);
+  const DeviceSpec& dev = cluster.devices[static_cast<size_t>(w.plan_dev)];
+  // Adam m/v staging: a dedicated ring when the HBM cap leaves room, otherwise it aliases
+  // the dead MLP activations of the scratch (then compute waits for the m/v write-back).
+  const long budget_floats = static_cast<long>(dev.mem_bytes / 4) - base_floats - 2048;
+  long chunk = std::min(exec.opt_chunk_floats, budget_floats / (2 * kStaging));
+  chunk = chunk / 1024 * 1024;
+  w.stg_alias = chunk < (1L << 20);
+  if (w.stg_alias) chunk = 0;
+  const long floats = base_floats + kStaging * 2 * hy_pad32(chunk);
+  w.arena_bytes = floats * 4 + 4096;
+  if (static_cast<double>(w.arena_bytes) > dev.mem_bytes) {
+    throw CapacityExhausted(dev.device_id, static_cast<double>(w.arena_bytes), dev.mem_bytes);
+  }
+  check_cuda(cudaMalloc(&w.arena, static_cast<size_t>(w.arena_bytes)), "arena cudaMalloc");
+  float* p = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(w.arena) + 1023) & ~uintptr_t(1023));
+  auto take = [&](long n) {
+    float* r = p;
+    p += hy_pad32(n);
+    return r;
+  };
+  w.slot[0] = take(slot_f);
+  w.slot[1] = take(slot_f);
+  w.gbuf = take(grad_f);
+  w.abuf[0] = take(act_f);
+  w.abuf[1] = take(act_f);
+  w.gbd[0] = take(act_f);
+  w.gbd[1] = take(act_f);
+  w.zbuf = take(act_f);
+  w.tok[0] = reinterpret_cast<int32_t*>(take(2 * tok_n));
+  w.tok[1] = reinterpret_cast<int32_t*>(take(2 * tok_n));
+  if (!w.stg_alias) {
+    for (int i = 0; i < kStaging; ++i) w.stg[i] = take(2 * chunk);
+  }
+  w.scratch = take(scratch_f);
+  if (w.stg_alias) {
+    // staging inside the scratch fc/act block of the largest job on this GPU
+    long best = 0;
+    for (int t : w.tasks) {
+      const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
+      int mb = 0;
+      for (const ShardGeom& sg : hj.geom) mb = std::max(mb, sg.n_blocks);
+      hy::Scratch sc;
+      hy::carve_scratch(hj.m, mb, w.scratch, &sc);
+      const long avail = 8L * hj.M * hj.m.d;  // fc + act
+      if (avail > best) {
+        best = avail;
+        chunk = avail / (2 * kStaging) / 1024 * 1024;
+        for (int i = 0; i < kStaging; ++i) w.stg[i] = sc.fc + static_cast<long>(i) * 2 * chunk;
+      }
+    }
+  }
+  w.stg_chunk = chunk;
+  w.loss_dev = reinterpret_cast<double*>(take(2 * static_cast<long>(w.tasks.size()) + 2));
+  check_cuda(cudaMemset(w.arena, 0, static_cast<size_t>(w.arena_bytes)), "arena memset");
+  w.timing.resize(w.tasks.size());
+  for (TaskTiming& tm : w.timing) {
+    for (cudaEvent_t* e : {&tm.pl0, &tm.pl1, &tm.pr0, &tm.pr1, &tm.c0, &tm.c1, &tm.d0, &tm.d1}) *e = new_event(true);
+  }
+  w.t0 = new_event(true);
+  w.t_end = new_event(true);
+  for (auto& e : w.join) e = new_event(false);
+  w.st.arena_bytes.push_back(static_cast<double>(w.arena_bytes));
+}
+
+void ExecutorImpl::setup(ExecResult& res) {
+  const auto t_start = std::chrono::steady_clock::now();
+  const int G = static_cast<int>(cluster.devices.size());
+  std::vector<int> run = exec.run_devices;
+  if (run.empty()) {
+    for (int d = 0; d < G; ++d) run.push_back(d);
+  }
+  const auto per_dev = plan.per_device(G);
+  task_local.assign(tasks.size(), -1);
+  task_device.assign(tasks.size(), -1);
+  for (int d = 0; d < G; ++d) {
+    for (size_t i = 0; i < per_dev[static_cast<size_t>(d)].size(); ++i) {
+      task_device[static_cast<size_t>(per_dev[static_cast<size_t>(d)][i])] = d;
+      task_local[static_cast<size_t>(per_dev[static_cast<size_t>(d)][i])] = static_cast<int>(i);
+    }
+  }
+  // minibatches per job per pass
+  job_mb.assign(exec.jobs.size(), 0);
+  for (const SimTask& t : tasks) {
+    job_mb[static_cast<size_t>(t.t.job)] = std::max(job_mb[static_cast<size_t>(t.t.job)], t.t.minibatch + 1);
+  }
+  for (int d : run) {
+    auto w = std::make_unique<Worker>();
+    w->ex = this;
+    w->plan_dev = d;
+    w->cuda_dev = exec.device_ids.empty() ? d : exec.device_ids.at(static_cast<size_t>(d));
+    w->tasks = per_dev[static_cast<size_t>(d)];
+    for (int t : w->tasks) {
+      const int j = tasks[static_cast<size_t>(t)].t.job;
+      if (!jobs.count(j)) {
+        check_cuda(cudaSetDevice(w->cuda_dev), "set device");
+        setup_host_job(j);
+      }
+    }
+    workers.push_back(std::move(w));
+  }
+  for (auto& w : workers) setup_worker(*w);
+  host_loss = static_cast<double*>(pinned(sizeof(double) * tasks.size()));
+  enqueued_pass.assign(tasks.size(), -1);
+  res.losses.assign(exec.jobs.size(), {});
+  double pinned_total = 0;
+  for (auto& kv : jobs) {
+    const HostJob& hj = kv.second;
+    pinned_total += 3.0 * 4 * hj.total + 4.0 * hj.n_act * (2 * hj.ckpt.size() + 1) + 8.0 * hj.M * hj.n_gmb;
+  }
+  res.stats.pinned_bytes.push_back(pinned_total);
+  res.stats.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+}
+
+namespace {
+
+float lr_of(const ExecJob& j) { return j.lr; }
+
+}  // namespace
+
+void ExecutorImpl::adam_writeback(Worker& w, HostJob& hj, int s, int slot, int step, int local) {
+  const ShardGeom& g = hj.geom[static_cast<size_t>(s)];
+  const long base = hy_layer_offset(&hj.m, g.l0);
+  const long chunk = w.stg_chunk;
+  const ExecJob& spec = *hj.spec;
+  hy::AdamHyper h{lr_of(spec), spec.beta1, spec.beta2, spec.eps, spec.weight_decay, 0.f, 0.f};
+  h.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta1), step));
+  h.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta2), step));
+  Tracked& ptr = *hj.params_tr[static_cast<size_t>(s)];
+  Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
+  // host regions: m/v read by opt (H2D), written by up (D2H); params written by up
+  mvt.before_read(w.opt);
+  ptr.before_write(w.up);
+  mvt.before_write(w.up);
+  int c = 0;
+  for (long off = 0; off < g.param_floats; off += chunk, ++c) {
+    const long n = std::min(chunk, g.param_floats - off);
+    const size_t bytes = sizeof(float) * static_cast<size_t>(n);
+    const int si = c % kStaging;
+    float* sm = w.stg[si];
+    float* sv = w.stg[si] + chunk;
+    Tracked& stg = w.stg_tr[si];
+    // opt stream: m, v chunk -> staging
+    stg.before_write(w.opt);
+    check_cuda(cudaMemcpyAsync(sm, hj.mom + base + off, bytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
+    check_cuda(cudaMemcpyAsync(sv, hj.var + base + off, bytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
+    stg.after_write(w.opt);
+    w.st.opt_h2d_bytes += 2.0 * bytes;
+    w.st.h2d_bytes += 2.0 * bytes;
+    // compute: fused Adam on (slot params, grads, m, v)
+    stg.before_read(w.comp);
+    stg.before_write(w.comp);
+    check_cuda(hy::adam_update(w.comp, n, w.slot[slot] + off, w.gbuf + off, sm, sv, h), "adam");
+    ++w.st.kernel_launches;
+    stg.after_write(w.comp);
+    // up: updated params + m, v -> host
+    stg.before_read(w.up);
+    check_cuda(cudaMemcpyAsync(hj.params + base + off, w.slot[slot] + off, bytes, cudaMemcpyDeviceToHost, w.up),
+               "p d2h");
+    check_cuda(cudaMemcpyAsync(hj.mom + base + off, sm, bytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
+    check_cuda(cudaMemcpyAsync(hj.var + base + off, sv, bytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
+    stg.after_read(w.up);
+    w.st.opt_d2h_bytes += 2.0 * bytes;
+    w.st.d2h_bytes += 3.0 * bytes;
+  }
+  mvt.after_read(w.opt);
+  // the slot was written by Adam (compute) and read by the write-back (up)
+  w.slot_tr[slot].after_write(w.comp);
+  w.slot_tr[slot].after_read(w.up);
+  w.gbuf_tr.after_read(w.comp);
+  check_cuda(cudaEventRecord(w.timing[static_cast<size_t>(local)].d1, w.up), "d1");
+  ptr.after_write(w.up);
+  mvt.after_write(w.up);
+}
+
+void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
+  const SimTask& task = tasks[static_cast<size_t>(t)];
+  const int j = task.t.job;
+  const int s = task.t.shard;
+  HostJob& hj = jobs.at(j);
+  const ShardGeom& g = hj.geom[static_cast<size_t>(s)];
+  const int k = static_cast<int>(hj.geom.size());
+  const int gmb = pass * job_mb[static_cast<size_t>(j)] + task.t.minibatch;
+  const bool fwd = task.t.direction == Direction::kForward;
+  const int local = task_local[static_cast<size_t>(t)];
+  TaskTiming& tm = w.timing[static_cast<size_t>(local)];
+  const size_t act_bytes = sizeof(float) * static_cast<size_t>(hj.n_act);
+
+  // Cross-device predecessors (only with jobs migrating, e.g. double_buffering=false):
+  // wait until their producer has been enqueued so its events exist.
+  for (int p : task.preds) {
+    if (task_device[static_cast<size_t>(p)] != w.plan_dev) {
+      std::unique_lock<std::mutex> lk(flag_mu);
+      flag_cv.wait(lk, [&] { return enqueued_pass[static_cast<size_t>(p)] >= pass; });
+    }
+  }
+
+  w.st.model_h2d_bytes += task.t.param_load_bytes + task.t.activation_in_bytes;
+  w.st.model_d2h_bytes += task.t.activation_out_bytes + task.t.grad_offload_bytes;
+
+  // ---- ParamLoad (down) -----------------------------------------------------------
+  const Tag want{j, -1, s, hj.version[static_cast<size_t>(s)]};
+  int slot = -1;
+  for (int i = 0; i < 2; ++i) {
+    if (w.slot_tag[i] == want) slot = i;
+  }
+  check_cuda(cudaEventRecord(tm.pl0, w.down), "pl0");
+  if (slot < 0) {
+    slot = w.last_slot < 0 ? 0 : 1 - w.last_slot;
+    const long base = hy_layer_offset(&hj.m, g.l0);
+    w.slot_tr[slot].before_write(w.down);
+    hj.params_tr[static_cast<size_t>(s)]->before_read(w.down);
+    check_cuda(cudaMemcpyAsync(w.slot[slot], hj.params + base, sizeof(float) * static_cast<size_t>(g.param_floats),
+                               cudaMemcpyHostToDevice, w.down),
+               "param h2d");
+    double bytes = 4.0 * g.param_floats;
+    if (g.wte_offset >= 0) {  // tied wte for a head shard without the embedding
+      hj.params_tr[0]->before_read(w.down);
+      const size_t wb = sizeof(float) * static_cast<size_t>(hj.m.V) * static_cast<size_t>(hj.m.d);
+      check_cuda(cudaMemcpyAsync(w.slot[slot] + g.wte_offset, hj.params, wb, cudaMemcpyHostToDevice, w.down),
+                 "wte h2d");
+      hj.params_tr[0]->after_read(w.down);
+      bytes += static_cast<double>(wb);
+    }
+    hj.params_tr[static_cast<size_t>(s)]->after_read(w.down);
+    w.slot_tr[slot].after_write(w.down);
+    w.slot_tag[slot] = want;
+    w.st.param_h2d_bytes += bytes;
+    w.st.h2d_bytes += bytes;
+  } else {
+    w.st.elided_param_bytes += task.t.param_load_bytes;
+  }
+  check_cuda(cudaEventRecord(tm.pl1, w.down), "pl1");
+  w.last_slot = slot;
+
+  // ---- ActPromote (down): tokens, boundary activation / checkpoint, grad_in, z --------
+  check_cuda(cudaEventRecord(tm.pr0, w.down), "pr0");
+  hy::TaskIO io;
+  const bool need_tokens = g.has_embed || g.has_head;
+  int tok_i = -1;
+  if (need_tokens) {
+    const Tag tt{j, gmb, 0, 0};
+    for (int i = 0; i < 2; ++i) {
+      if (w.tok_tag[i] == tt) tok_i = i;
+    }
+    if (tok_i < 0) {
+      tok_i = 1 - w.last_tok;  // alternate: the other buffer may still feed a resident task
+      w.last_tok = tok_i;
+      w.tok_tr[tok_i].before_write(w.down);
+      const size_t tb = sizeof(int32_t) * static_cast<size_t>(hj.M);
+      check_cuda(cudaMemcpyAsync(w.tok[tok_i], hj.tokens + static_cast<long>(gmb) * hj.M, tb, cudaMemcpyHostToDevice,
+                                 w.down),
+                 "tok h2d");
+      check_cuda(cudaMemcpyAsync(w.tok[tok_i] + hj.M, hj.targets + static_cast<long>(gmb) * hj.M, tb,
+                                 cudaMemcpyHostToDevice, w.down),
+                 "tgt h2d");
+      w.tok_tr[tok_i].after_write(w.down);
+      w.tok_tag[tok_i] = tt;
+      w.st.h2d_bytes += 2.0 * static_cast<double>(tb);
+    }
+  }
+  // act buffers: find resident or load
+  auto find_tag = [](const Tag* tags, int n, const Tag& want_tag) {
+    for (int i = 0; i < n; ++i) {
+      if (tags[i] == want_tag) return i;
+    }
+    return -1;
+  };
+  int ain = -1;  // abuf holding the shard's input activation (boundary s-1)
+  if (s > 0) {
+    const Tag at{j, gmb, s - 1, 0};
+    ain = find_tag(w.abuf_tag, 2, at);
+    if (ain < 0) {
+      ain = 0;
+      // don't clobber a resident buffer that the forward output will need: pick the older
+      if (w.abuf_tag[0].job >= 0 && w.abuf_tag[1].job < 0) ain = 1;
+      w.abuf_tr[ain].before_write(w.down);
+      hj.ckpt_tr[static_cast<size_t>(s - 1)]->before_read(w.down);
+      check_cuda(cudaMemcpyAsync(w.abuf[ain], hj.ckpt[static_cast<size_t>(s - 1)], act_bytes, cudaMemcpyHostToDevice,
+                                 w.down),
+                 "act h2d");
+      hj.ckpt_tr[static_cast<size_t>(s - 1)]->after_read(w.down);
+      w.abuf_tr[ain].after_write(w.down);
+      w.abuf_tag[ain] = at;
+      w.st.act_h2d_bytes += static_cast<double>(act_bytes);
+      w.st.h2d_bytes += static_cast<double>(act_bytes);
+    } else {
+      w.st.elided_act_bytes += static_cast<double>(act_bytes);
+    }
+  }
+  int gin = -1;  // gbd holding dL/d(boundary s) for a backward task
+  if (!fwd && s < k - 1) {
+    const Tag gt{j, gmb, s, 1};
+    gin = find_tag(w.gbd_tag, 2, gt);
+    if (gin < 0) {
+      gin = 0;
+      w.gbd_tr[gin].before_write(w.down);
+      hj.grad_tr[static_cast<size_t>(s)]->before_read(w.down);
+      check_cuda(cudaMemcpyAsync(w.gbd[gin], hj.grad[static_cast<size_t>(s)], act_bytes, cudaMemcpyHostToDevice,
+                                 w.down),
+                 "grad h2d");
+      hj.grad_tr[static_cast<size_t>(s)]->after_read(w.down);
+      w.gbd_tr[gin].after_write(w.down);
+      w.gbd_tag[gin] = gt;
+      w.st.act_h2d_bytes += static_cast<double>(act_bytes);
+      w.st.h2d_bytes += static_cast<double>(act_bytes);
+    } else {
+      w.st.elided_act_bytes += static_cast<double>(act_bytes);
+    }
+  }
+  const bool needs_z = !fwd && g.has_embed && !g.has_head;
+  if (needs_z) {
+    const Tag zt{j, gmb, 0, 2};
+    if (!(w.z_tag == zt)) {
+      w.z_tr.before_write(w.down);
+      hj.z_tr->before_read(w.down);
+      check_cuda(cudaMemcpyAsync(w.zbuf, hj.z, act_bytes, cudaMemcpyHostToDevice, w.down), "z h2d");
+      hj.z_tr->after_read(w.down);
+      w.z_tr.after_write(w.down);
+      w.z_tag = zt;
+      w.st.h2d_bytes += static_cast<double>(act_bytes);
+    }
+  }
+  check_cuda(cudaEventRecord(tm.pr1, w.down), "pr1");
+
+  // ---- Compute (comp) ---------------------------------------------------------------
+  hy::Scratch sc;
+  int max_blocks = 0;
+  for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
+  hy::carve_scratch(hj.m, max_blocks, w.scratch, &sc);
+  if (w.stg_alias) {
+    for (int i = 0; i < kStaging; ++i) w.stg_tr[i].before_write(w.comp);  // scratch reused as staging
+  }
+  w.slot_tr[slot].before_read(w.comp);
+  if (need_tokens) w.tok_tr[tok_i].before_read(w.comp);
+  if (ain >= 0) w.abuf_tr[ain].before_read(w.comp);
+  if (gin >= 0) w.gbd_tr[gin].before_read(w.comp);
+  if (needs_z) w.z_tr.before_read(w.comp);
+  check_cuda(cudaEventRecord(tm.c0, w.comp), "c0");
+  int aout = -1, gout = -1;
+  if (fwd) {
+    io.tokens = need_tokens ? w.tok[tok_i] : nullptr;
+    io.act_in = ain >= 0 ? w.abuf[ain] : nullptr;
+    if (!g.has_head) {
+      aout = ain >= 0 ? 1 - ain : (w.abuf_tag[0].job < 0 ? 0 : (w.abuf_tag[1].job < 0 ? 1 : 0));
+      w.abuf_tr[aout].before_write(w.comp);
+      io.act_out = w.abuf[aout];
+    }
+  } else {
+    io.tokens = need_tokens ? w.tok[tok_i] : nullptr;
+    io.act_in = ain >= 0 ? w.abuf[ain] : nullptr;
+    io.grad_in = gin >= 0 ? w.gbd[gin] : nullptr;
+    if (s > 0) {
+      gout = gin >= 0 ? 1 - gin : 0;
+      w.gbd_tr[gout].before_write(w.comp);
+      io.grad_out = w.gbd[gout];
+    }
+    if (needs_z) io.z_in = w.zbuf;
+    w.gbuf_tr.before_write(w.comp);
+    check_cuda(cudaMemsetAsync(w.gbuf, 0, sizeof(float) * static_cast<size_t>(g.param_floats), w.comp), "zero grads");
+  }
+  // targets live in the second half of the token buffer ([tokens | targets], 2*M ints)
+  io.targets = need_tokens ? w.tok[tok_i] + hj.M : nullptr;
+  if (fwd) {
+    hy::run_forward(w.comp, hj.m, g, w.slot[slot], io, sc);
+    if (g.has_head) {
+      check_cuda(cudaMemcpyAsync(w.loss_dev + local, sc.loss, sizeof(double), cudaMemcpyDeviceToDevice, w.comp),
+                 "loss copy");
+    }
+  } else {
+    hy::run_backward(w.comp, hj.m, g, w.slot[slot], w.gbuf, io, sc);
+    if (w.stg_alias) {
+      for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // m/v loads wait for the backward
+    }
+    if (g.has_head && !g.has_embed) {
+      w.z_tr.before_write(w.comp);
+      check_cuda(cudaMemcpyAsync(w.zbuf, sc.z, act_bytes, cudaMemcpyDeviceToDevice, w.comp), "z save");
+      w.z_tr.after_write(w.comp);
+      w.z_tag = Tag{j, gmb, 0, 2};
+    }
+    w.gbuf_tr.after_write(w.comp);
+  }
+  check_cuda(cudaEventRecord(tm.c1, w.comp), "c1");
+  w.slot_tr[slot].after_read(w.comp);
+  if (need_tokens) w.tok_tr[tok_i].after_read(w.comp);
+  if (ain >= 0) w.abuf_tr[ain].after_read(w.comp);
+  if (gin >= 0) w.gbd_tr[gin].after_read(w.comp);
+  if (needs_z) w.z_tr.after_read(w.comp);
+  if (aout >= 0) {
+    w.abuf_tr[aout].after_write(w.comp);
+    w.abuf_tag[aout] = Tag{j, gmb, s, 0};
+  }
+  if (gout >= 0) {
+    w.gbd_tr[gout].after_write(w.comp);
+    w.gbd_tag[gout] = Tag{j, gmb, s - 1, 1};
+  }
+
+  // ---- ActDemote + GradOffload (up) ---------------------------------------------------
+  check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
+  if (aout >= 0) {  // forward boundary activation -> checkpoint store
+    Tracked& host = *hj.ckpt_tr[static_cast<size_t>(s)];
+    w.abuf_tr[aout].before_read(w.up);
+    host.before_write(w.up);
+    check_cuda(cudaMemcpyAsync(hj.ckpt[static_cast<size_t>(s)], w.abuf[aout], act_bytes, cudaMemcpyDeviceToHost, w.up),
+               "act d2h");
+    host.after_write(w.up);
+    w.abuf_tr[aout].after_read(w.up);
+    w.st.act_d2h_bytes += static_cast<double>(act_bytes);
+    w.st.d2h_bytes += static_cast<double>(act_bytes);
+  }
+  if (gout >= 0) {  // dL/d(input boundary) -> host
+    Tracked& host = *hj.grad_tr[static_cast<size_t>(s - 1)];
+    w.gbd_tr[gout].before_read(w.up);
+    host.before_write(w.up);
+    check_cuda(cudaMemcpyAsync(hj.grad[static_cast<size_t>(s - 1)], w.gbd[gout], act_bytes, cudaMemcpyDeviceToHost,
+                               w.up),
+               "grad d2h");
+    host.after_write(w.up);
+    w.gbd_tr[gout].after_read(w.up);
+    w.st.act_d2h_bytes += static_cast<double>(act_bytes);
+    w.st.d2h_bytes += static_cast<double>(act_bytes);
+  }
+  if (!fwd && g.has_head && !g.has_embed) {  // saved ln_f output for shard 0's tied-wte grad
+    w.z_tr.before_read(w.up);
+    hj.z_tr->before_write(w.up);
+    check_cuda(cudaMemcpyAsync(hj.z, w.zbuf, act_bytes, cudaMemcpyDeviceToHost, w.up), "z d2h");
+    hj.z_tr->after_write(w.up);
+    w.z_tr.after_read(w.up);
+    w.st.d2h_bytes += static_cast<double>(act_bytes);
+  }
+  if (!fwd) {
+    const int step = gmb + 1;
+    adam_writeback(w, hj, s, slot, step, local);
+    hj.version[static_cast<size_t>(s)] += 1;
+    w.slot_tag[slot] = Tag{j, -1, s, hj.version[static_cast<size_t>(s)]};
+  } else {
+    check_cuda(cudaEventRecord(tm.d1, w.up), "d1");
+  }
+  {
+    std::lock_guard<std::mutex> lk(flag_mu);
+    enqueued_pass[static_cast<size_t>(t)] = pass;
+  }
+  flag_cv.notify_all();
+}
+
+void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
+  std::vector<std::thread> threads;
+  std::vector<std::exception_ptr> errs(workers.size());
+  for (size_t i = 0; i < workers.size(); ++i) {
+    threads.emplace_back([&, i] {
+      Worker& w = *workers[i];
+      try {
+        check_cuda(cudaSetDevice(w.cuda_dev), "set device");
+        check_cuda(cudaDeviceSynchronize(), "pre-pass sync");
+        check_cuda(cudaEventRecord(w.t0, w.comp), "t0");
+        for (cudaStream_t s : {w.down, w.up, w.opt}) check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");
+        for (int t : w.tasks) enqueue_task(w, t, pass);
+        // join all streams into comp, then record the end
+        cudaStream_t others[3] = {w.down, w.up, w.opt};
+        for (int k = 0; k < 3; ++k) {
+          check_cuda(cudaEventRecord(w.join[k], others[k]), "join");
+          check_cuda(cudaStreamWaitEvent(w.comp, w.join[k], 0), "join wait");
+        }
+        check_cuda(cudaEventRecord(w.t_end, w.comp), "t_end");
+        check_cuda(cudaEventSynchronize(w.t_end), "pass sync");
+        check_cuda(cudaGetLastError(), "pass");
+      } catch (...) {
+        errs[i] = std::current_exception();
+        std::lock_guard<std::mutex> lk(flag_mu);
+        for (auto& e : enqueued_pass) e = std::max(e, pass);  // unblock peers
+        flag_cv.notify_all();
+      }
+    });
+  }
+  for (auto& th : threads) th.join();
+  for (auto& e : errs) {
+    if (e) std::rethrow_exception(e);
+  }
+  if (timed) collect(pass, res);
+}
+
+void ExecutorImpl::collect(int pass, ExecResult& res) {
+  // losses
+  double pass_max = 0;
+  SimTrace tr;
+  const int G = static_cast<int>(cluster.devices.size());
+  tr.device_resource.assign(static_cast<size_t>(G), -1);
+  std::vector<int> down_res(static_cast<size_t>(G), -1), up_res(static_cast<size_t>(G), -1);
+  for (int d = 0; d < G; ++d) {
+    const std::string& id = cluster.devices[static_cast<size_t>(d)].device_id;
+    tr.device_resource[static_cast<size_t>(d)] = static_cast<int>(tr.resource_names.size());
+    tr.resource_names.push_back(id);
+    tr.resource_device.push_back(d);
+    down_res[static_cast<size_t>(d)] = static_cast<int>(tr.resource_names.size());
+    tr.resource_names.push_back("h2d." + id + ".down");
+    tr.resource_device.push_back(d);
+    up_res[static_cast<size_t>(d)] = static_cast<int>(tr.resource_names.size());
+    tr.resource_names.push_back("h2d." + id + ".up");
+    tr.resource_device.push_back(d);
+  }
+  for (size_t i = 0; i < tasks.size(); ++i) {
+    const SimTask& t = tasks[i];
+    tr.task_labels.push_back("j" + std::to_string(t.t.job) + ".mb" + std::to_string(t.t.minibatch) + ".s" +
+                             std::to_string(t.t.shard) + (t.t.direction == Direction::kForward ? ".F" : ".B"));
+  }
+  for (auto& wp : workers) {
+    Worker& w = *wp;
+    check_cuda(cudaSetDevice(w.cuda_dev), "set device");
+    float ms = 0;
+    check_cuda(cudaEventElapsedTime(&ms, w.t0, w.t_end), "elapsed");
+    pass_max = std::max(pass_max, ms * 1e-3);
+    auto rel = [&](cudaEvent_t e) {
+      float v = 0;
+      check_cuda(cudaEventElapsedTime(&v, w.t0, e), "elapsed");
+      return static_cast<double>(v) * 1e-3;
+    };
+    // losses of forward head tasks
+    std::vector<double> lbuf(w.tasks.size() + 1, 0.0);
+    check_cuda(cudaMemcpy(lbuf.data(), w.loss_dev, sizeof(double) * w.tasks.size(), cudaMemcpyDeviceToHost),
+               "loss d2h");
+    double busy = 0;
+    for (size_t li = 0; li < w.tasks.size(); ++li) {
+      const int t = w.tasks[li];
+      const SimTask& task = tasks[static_cast<size_t>(t)];
+      const HostJob& hj = jobs.at(task.t.job);
+      const ShardGeom& g = hj.geom[static_cast<size_t>(task.t.shard)];
+      TaskTiming& tm = w.timing[li];
+      const double pl0 = rel(tm.pl0), pl1 = rel(tm.pl1), pr0 = rel(tm.pr0), pr1 = rel(tm.pr1);
+      const double c0 = rel(tm.c0), c1 = rel(tm.c1), d0 = rel(tm.d0), d1 = rel(tm.d1);
+      if (pl1 > pl0) tr.events.push_back(SimEvent{down_res[static_cast<size_t>(w.plan_dev)], EventKind::kParamLoad, t, pl0, pl1});
+      if (pr1 > pr0) tr.events.push_back(SimEvent{down_res[static_cast<size_t>(w.plan_dev)], EventKind::kActPromote, t, pr0, pr1});
+      tr.events.push_back(SimEvent{tr.device_resource[static_cast<size_t>(w.plan_dev)], EventKind::kCompute, t, c0, c1});
+      busy += c1 - c0;
+      if (d1 > d0) {
+        const EventKind k = task.t.direction == Direction::kForward ? EventKind::kActDemote : EventKind::kGradOffload;
+        tr.events.push_back(SimEvent{up_res[static_cast<size_t>(w.plan_dev)], k, t, d0, d1});
+      }
+      tr.makespan_s = std::max(tr.makespan_s, std::max(c1, d1));
+      if (task.t.direction == Direction::kForward && g.has_head) {
+        const int gmb = pass * job_mb[static_cast<size_t>(task.t.job)] + task.t.minibatch;
+        auto& L = res.losses[static_cast<size_t>(task.t.job)];
+        if (static_cast<int>(L.size()) <= gmb) L.resize(static_cast<size_t>(gmb) + 1, 0.0);
+        L[static_cast<size_t>(gmb)] = lbuf[li] / static_cast<double>(hj.M);
+      }
+    }
+    res.stats.device_busy_s.push_back(busy);
+  }
+  std::sort(tr.events.begin(), tr.events.end(), [](const SimEvent& a, const SimEvent& b) {
+    return std::tie(a.resource, a.start_s, a.end_s) < std::tie(b.resource, b.start_s, b.end_s);
+  });
+  res.trace = std::move(tr);
+  res.pass_seconds.push_back(pass_max);
+}
+
+ExecResult run_execution(const ClusterSpec& cluster, const std::vector<SimTask>& tasks, const DispatchPlan& plan,
+                         const SimOptions& options, const ExecOptions& exec) {
+  ExecResult res;
+  ExecutorImpl ex(cluster, tasks, plan, options, exec);
+  ex.setup(res);
+  const int total = exec.warmup_passes + exec.passes;
+  for (int p = 0; p < total; ++p) {
+    const bool timed = p >= exec.warmup_passes;
+    if (timed) {
+      for (auto& w : ex.workers) w->st = ExecStats{};
+    }
+    ex.run_pass(p, timed, res);
+    if (timed) {
+      for (auto& w : ex.workers) {
+        ExecStats& a = res.stats;
+        const ExecStats& b = w->st;
+        a.h2d_bytes += b.h2d_bytes;
+        a.d2h_bytes += b.d2h_bytes;
+        a.model_h2d_bytes += b.model_h2d_bytes;
+        a.model_d2h_bytes += b.model_d2h_bytes;
+        a.param_h2d_bytes += b.param_h2d_bytes;
+        a.opt_h2d_bytes += b.opt_h2d_bytes;
+        a.opt_d2h_bytes += b.opt_d2h_bytes;
+        a.act_h2d_bytes += b.act_h2d_bytes;
+        a.act_d2h_bytes += b.act_d2h_bytes;
+        a.elided_param_bytes += b.elided_param_bytes;
+        a.elided_act_bytes += b.elided_act_bytes;
+        a.kernel_launches += b.kernel_launches;
+      }
+    }
+  }
+  for (auto& w : ex.workers) res.stats.arena_bytes.push_back(static_cast<double>(w->arena_bytes));
+  double ms = 0;
+  for (double s : res.pass_seconds) ms += s;
+  res.stats.makespan_s = res.pass_seconds.empty() ? 0 : ms / static_cast<double>(res.pass_seconds.size());
+  if (!exec.params_out_dir.empty()) {
+    for (auto& kv : ex.jobs) {
+      const std::string path = exec.params_out_dir + "/job" + std::to_string(kv.first) + ".f32";
+      FILE* f = std::fopen(path.c_str(), "wb");
+      if (!f) throw InvalidArgument("cannot write " + path);
+      std::fwrite(kv.second.params, sizeof(float), static_cast<size_t>(kv.second.total), f);
+      std::fclose(f);
+    }
+  }
+  return res;
+}
+
+}  // namespace spillsim

@@ -1,0 +1,262 @@
+// GPT-2 shard compute on sm_100a kernels. Forward: embed -> blocks -> (head loss).
+// Backward: recompute the shard forward from its checkpoint keeping block inputs, then
+// per block recompute intermediates and back-propagate (reference semantics: backward
+// compute = fwd recompute + bwd, strategies.cpp:775). Backward temporaries alias dead
+// forward intermediates, so a block needs ~12 M*d floats of scratch in total.
+#include "gpt_runner.hpp"
+
+#include <algorithm>
+#include <string>
+
+#include "../kernels/gemm.cuh"
+#include "../kernels/ops.cuh"
+#include "spillsim/errors.hpp"
+
+namespace hy {
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw spillsim::DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+ShardGeom shard_geom(const hy_dims& m, int l0, int l1) {
+  ShardGeom g;
+  g.l0 = l0;
+  g.l1 = l1;
+  g.has_embed = l0 == 0;
+  g.has_head = l1 == m.L + 2;
+  g.n_blocks = std::min(l1, m.L + 1) - std::max(l0, 1);
+  if (g.n_blocks < 0) g.n_blocks = 0;
+  g.param_floats = hy_layer_offset(&m, l1) - hy_layer_offset(&m, l0);
+  g.slot_floats = g.param_floats;
+  if (g.has_head && !g.has_embed) {
+    g.wte_offset = hy_pad32(g.param_floats);
+    g.slot_floats = g.wte_offset + static_cast<long>(m.V) * m.d;
+  }
+  return g;
+}
+
+namespace {
+
+inline long lo(const hy_dims& m, int layer, int l0) { return hy_layer_offset(&m, layer) - hy_layer_offset(&m, l0); }
+inline const float* bt(const float* w, int d, int t) { return w + hy_block_tensor_offset(d, t); }
+inline float* btw(float* w, int d, int t) { return w + hy_block_tensor_offset(d, t); }
+
+void gemm(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool amn, const float* B, long ldb,
+          bool bmn, float* C, long ldc, const float* bias = nullptr, const float* R = nullptr, long ldr = 0,
+          float beta = 0.f, int mode = kEpiStore, float* hout = nullptr, const float* hin = nullptr, long ldh = 0) {
+  GemmEpilogue e;
+  e.C = C;
+  e.ldc = ldc;
+  e.bias = bias;
+  e.R = R;
+  e.ldr = ldr;
+  e.beta = beta;
+  e.mode = mode;
+  e.Hout = hout;
+  e.ldho = ldh;
+  e.Hin = hin;
+  e.ldhi = ldh;
+  check_cuda(gemm_tf32(st, M, N, K, A, lda, amn, B, ldb, bmn, e), "gemm");
+}
+
+void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const float* h_in, float* h_out, Scratch& s) {
+  const int M = s.M, d = m.d;
+  check_cuda(layernorm_fwd(st, M, d, h_in, bt(w, d, HY_LN1_G), bt(w, d, HY_LN1_B), s.ln1, s.mean1, s.rstd1), "ln1");
+  gemm(st, M, 3 * d, d, s.ln1, d, false, bt(w, d, HY_WQKV), d, false, s.qkv, 3 * d, bt(w, d, HY_BQKV));
+  check_cuda(attention_fwd(st, m.B, m.T, m.H, s.qkv, s.att, s.lse), "attn_fwd");
+  gemm(st, M, d, d, s.att, d, false, bt(w, d, HY_WO), d, false, s.hmid, d, bt(w, d, HY_BO), h_in, d);
+  check_cuda(layernorm_fwd(st, M, d, s.hmid, bt(w, d, HY_LN2_G), bt(w, d, HY_LN2_B), s.ln2, s.mean2, s.rstd2), "ln2");
+  gemm(st, M, 4 * d, d, s.ln2, d, false, bt(w, d, HY_WFC), d, false, s.act, 4 * d, bt(w, d, HY_BFC), nullptr, 0, 0.f,
+       kEpiGelu, s.fc, nullptr, 4 * d);
+  gemm(st, M, d, 4 * d, s.act, 4 * d, false, bt(w, d, HY_WPR), 4 * d, false, h_out, d, bt(w, d, HY_BPR), s.hmid, d);
+}
+
+// dh: in dL/dh_out, out dL/dh_in. Requires the intermediates of block_forward(h_in).
+void block_backward(cudaStream_t st, const hy_dims& m, const float* w, float* gw, const float* h_in, float* dh,
+                    Scratch& s) {
+  const int M = s.M, d = m.d;
+  // MLP out: h_out = hmid + act Wpr^T + bpr
+  gemm(st, d, 4 * d, M, dh, d, true, s.act, 4 * d, true, btw(gw, d, HY_WPR), 4 * d, nullptr, nullptr, 0, 1.f);
+  check_cuda(colsum(st, M, d, dh, d, btw(gw, d, HY_BPR), true, s.ws), "colsum bpr");
+  float* dact = s.act;  // act is dead after dWpr
+  gemm(st, M, 4 * d, d, dh, d, false, bt(w, d, HY_WPR), 4 * d, true, dact, 4 * d, nullptr, nullptr, 0, 0.f, kEpiGeluBwd,
+       nullptr, s.fc, 4 * d);
+  gemm(st, 4 * d, d, M, dact, 4 * d, true, s.ln2, d, true, btw(gw, d, HY_WFC), d, nullptr, nullptr, 0, 1.f);
+  check_cuda(colsum(st, M, 4 * d, dact, 4 * d, btw(gw, d, HY_BFC), true, s.ws), "colsum bfc");
+  float* dln2 = s.fc;  // fc dead after dact
+  gemm(st, M, d, 4 * d, dact, 4 * d, false, bt(w, d, HY_WFC), d, true, dln2, d);
+  check_cuda(layernorm_bwd(st, M, d, s.hmid, bt(w, d, HY_LN2_G), s.mean2, s.rstd2, dln2, dh, true,
+                           btw(gw, d, HY_LN2_G), btw(gw, d, HY_LN2_B), s.ws),
+             "ln2 bwd");
+  // attention out: hmid = h_in + att Wo^T + bo   (dh now holds dL/dhmid)
+  gemm(st, d, d, M, dh, d, true, s.att, d, true, btw(gw, d, HY_WO), d, nullptr, nullptr, 0, 1.f);
+  check_cuda(colsum(st, M, d, dh, d, btw(gw, d, HY_BO), true, s.ws), "colsum bo");
+  float* datt = s.ln2;  // ln2 dead after dWfc
+  gemm(st, M, d, d, dh, d, false, bt(w, d, HY_WO), d, true, datt, d);
+  float* dqkv = s.act;  // dact dead after dln2 / dWfc
+  check_cuda(attention_bwd(st, m.B, m.T, m.H, s.qkv, s.att, datt, s.lse, dqkv, s.attn_ws), "attn bwd");
+  gemm(st, 3 * d, d, M, dqkv, 3 * d, true, s.ln1, d, true, btw(gw, d, HY_WQKV), d, nullptr, nullptr, 0, 1.f);
+  check_cuda(colsum(st, M, 3 * d, dqkv, 3 * d, btw(gw, d, HY_BQKV), true, s.ws), "colsum bqkv");
+  float* dln1 = s.hmid;  // hmid dead after ln2 bwd
+  gemm(st, M, d, 3 * d, dqkv, 3 * d, false, bt(w, d, HY_WQKV), d, true, dln1, d);
+  check_cuda(layernorm_bwd(st, M, d, h_in, bt(w, d, HY_LN1_G), s.mean1, s.rstd1, dln1, dh, true,
+                           btw(gw, d, HY_LN1_G), btw(gw, d, HY_LN1_B), s.ws),
+             "ln1 bwd");
+}
+
+// z = ln_f(h); logits chunks -> xent. want_grad: dlogits scaled by 1/M; dz, dwte (if given).
+void head_pass(cudaStream_t st, const hy_dims& m, const float* lnf, const float* wte, const float* h,
+               const int32_t* targets, Scratch& s, bool want_grad, float* dwte, bool z_ready = false) {
+  const int M = s.M, d = m.d, V = m.V;
+  if (!z_ready) {
+    check_cuda(layernorm_fwd(st, M, d, h, lnf, lnf + hy_pad32(d), s.z, s.zmean, s.zrstd), "ln_f");
+  }
+  check_cuda(cudaMemsetAsync(s.loss, 0, sizeof(double), st), "memset loss");
+  for (int r0 = 0; r0 < M; r0 += s.logits_rows) {
+    const int rows = std::min(s.logits_rows, M - r0);
+    gemm(st, rows, V, d, s.z + static_cast<long>(r0) * d, d, false, wte, d, false, s.logits, HY_VOCAB_PAD);
+    check_cuda(softmax_xent(st, rows, V, s.logits, HY_VOCAB_PAD, targets + r0, 1.f / M, s.row_loss + r0), "xent");
+    if (want_grad && s.dz) {
+      gemm(st, rows, d, V, s.logits, HY_VOCAB_PAD, false, wte, d, true, s.dz + static_cast<long>(r0) * d, d);
+    }
+    if (want_grad && dwte) {
+      gemm(st, V, d, rows, s.logits, HY_VOCAB_PAD, true, s.z + static_cast<long>(r0) * d, d, true, dwte, d, nullptr,
+           nullptr, 0, 1.f);
+    }
+  }
+  check_cuda(sum_to_double(st, M, s.row_loss, s.loss, false), "loss sum");
+}
+
+}  // namespace
+
+long scratch_floats(const hy_dims& m, int max_blocks) {
+  Scratch s;
+  carve_scratch(m, max_blocks, nullptr, &s);
+  return reinterpret_cast<long>(s.attn_ws) / static_cast<long>(sizeof(float)) +
+         hy_pad32(static_cast<long>(m.B) * m.H * m.T);
+}
+
+void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s) {
+  const long M = static_cast<long>(m.B) * m.T, d = m.d;
+  float* p = base;
+  auto take = [&](long n) {
+    float* r = p;
+    p += hy_pad32(n);
+    return r;
+  };
+  s->M = static_cast<int>(M);
+  s->d = m.d;
+  s->stash_slots = max_blocks + 1;
+  s->stash = take(M * d * s->stash_slots);
+  s->ln1 = take(M * d);
+  s->mean1 = take(M);
+  s->rstd1 = take(M);
+  s->qkv = take(3 * M * d);
+  s->att = take(M * d);
+  s->lse = take(static_cast<long>(m.B) * m.H * m.T);
+  s->hmid = take(M * d);
+  s->ln2 = take(M * d);
+  s->mean2 = take(M);
+  s->rstd2 = take(M);
+  // fc and act are adjacent: the head's logits chunk aliases both.
+  s->fc = take(4 * M * d);
+  s->act = take(4 * M * d);
+  s->logits = s->fc;
+  const long logit_floats = 8 * M * d;
+  s->logits_rows = static_cast<int>(std::min<long>(M, logit_floats / HY_VOCAB_PAD));
+  s->tmp_h = take(M * d);
+  s->ws = take(512L * 4 * d);  // >= colsum_blocks(M) * max(4d, 2d)
+  s->z = take(M * d);
+  s->zmean = take(M);
+  s->zrstd = take(M);
+  s->dz = take(M * d);
+  s->row_loss = take(M);
+  s->loss = reinterpret_cast<double*>(take(2));
+  s->attn_ws = take(static_cast<long>(m.B) * m.H * m.T);
+}
+
+void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, const TaskIO& io,
+                 Scratch& s) {
+  const long n = static_cast<long>(s.M) * m.d;
+  const int b0 = std::max(g.l0, 1);
+  const int b1 = std::min(g.l1, m.L + 1);
+  const bool write_out = !g.has_head && io.act_out != nullptr;
+  const float* cur = io.act_in;
+  if (g.has_embed) {
+    float* dst = (write_out && g.n_blocks == 0) ? io.act_out : s.tmp_h;
+    check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), dst),
+               "embed");
+    cur = dst;
+  }
+  for (int l = b0; l < b1; ++l) {
+    float* dst = (cur == s.tmp_h) ? s.stash : s.tmp_h;
+    if (write_out && l == b1 - 1) dst = io.act_out;
+    block_forward(st, m, slot + lo(m, l, g.l0), cur, dst, s);
+    cur = dst;
+  }
+  if (g.has_head) {
+    const float* wte = g.has_embed ? slot : slot + g.wte_offset;
+    head_pass(st, m, slot + lo(m, m.L + 1, g.l0), wte, cur, io.targets, s, false, nullptr);
+  } else if (write_out && cur != io.act_out) {
+    check_cuda(cudaMemcpyAsync(io.act_out, cur, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "act copy");
+  }
+}
+
+void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, float* grads,
+                  const TaskIO& io, Scratch& s) {
+  const long n = static_cast<long>(s.M) * m.d;
+  const int b0 = std::max(g.l0, 1);
+  const int nb = g.n_blocks;
+  // 1) recompute: stash[i] = input of block b0+i; stash[nb] = shard output.
+  if (g.has_embed) {
+    check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), s.stash),
+               "embed");
+  } else {
+    check_cuda(cudaMemcpyAsync(s.stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
+  }
+  for (int i = 0; i < nb; ++i) {
+    block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, s.stash + (i + 1) * n, s);
+  }
+  // 2) gradient wrt the shard output
+  float* dh = s.tmp_h;
+  if (g.has_head) {
+    const float* lnf = slot + lo(m, m.L + 1, g.l0);
+    float* glnf = grads + lo(m, m.L + 1, g.l0);
+    const float* wte = g.has_embed ? slot : slot + g.wte_offset;
+    float* dwte = g.has_embed ? grads : nullptr;  // otherwise deferred to shard 0 via z
+    const float* hfin = s.stash + nb * n;
+    head_pass(st, m, lnf, wte, hfin, io.targets, s, true, dwte);
+    check_cuda(layernorm_bwd(st, s.M, m.d, hfin, lnf, s.zmean, s.zrstd, s.dz, dh, false, glnf, glnf + hy_pad32(m.d),
+                             s.ws),
+               "ln_f bwd");
+  } else {
+    check_cuda(cudaMemcpyAsync(dh, io.grad_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad in");
+  }
+  // 3) blocks, last to first: recompute intermediates, back-propagate
+  for (int i = nb - 1; i >= 0; --i) {
+    const float* w = slot + lo(m, b0 + i, g.l0);
+    float* gw = grads + lo(m, b0 + i, g.l0);
+    float* scratch_out = s.stash + (i + 1) * n;  // block output no longer needed
+    block_forward(st, m, w, s.stash + i * n, scratch_out, s);
+    block_backward(st, m, w, gw, s.stash + i * n, dh, s);
+  }
+  // 4) embedding (+ deferred tied-wte gradient from the head's saved z)
+  if (g.has_embed) {
+    if (!g.has_head && io.z_in) {
+      if (io.z_in != s.z) {
+        check_cuda(cudaMemcpyAsync(s.z, io.z_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "z in");
+      }
+      float* saved_dz = s.dz;
+      s.dz = nullptr;  // only dwte is wanted
+      head_pass(st, m, nullptr, slot, nullptr, io.targets, s, true, grads, /*z_ready=*/true);
+      s.dz = saved_dz;
+    }
+    check_cuda(embed_bwd(st, s.M, m.T, m.d, io.tokens, dh, grads, grads + hy_pad32(static_cast<long>(m.V) * m.d),
+                         nullptr),
+               "embed bwd");
+  } else if (io.grad_out) {
+    check_cuda(cudaMemcpyAsync(io.grad_out, dh, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad out");
+  }
+}
+
+}  // namespace hy

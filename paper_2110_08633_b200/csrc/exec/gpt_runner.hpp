@@ -1,0 +1,66 @@
+// Device compute of one ShardTask of the GPT-2 model in include/hydra_gpt.h, as a
+// sequence of sm_100a kernel launches on one stream. Transfers are the executor's job.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hydra_gpt.h"
+
+namespace hy {
+
+struct ShardGeom {
+  int l0 = 0, l1 = 0;       // layer range [l0, l1)
+  long param_floats = 0;    // contiguous layers l0..l1-1
+  long wte_offset = -1;     // offset of a tied-wte copy inside the slot (head shard w/o embed), else -1
+  long slot_floats = 0;     // param_floats (+ pad + V*d when wte_offset >= 0)
+  bool has_embed = false, has_head = false;
+  int n_blocks = 0;         // transformer blocks in the shard
+};
+
+ShardGeom shard_geom(const hy_dims& m, int l0, int l1);
+
+// Device scratch for one worker (carved from the capped arena).
+struct Scratch {
+  int M = 0, d = 0;
+  float* stash = nullptr;  // [max_blocks + 1][M*d] block inputs for recompute
+  int stash_slots = 0;
+  float *ln1, *mean1, *rstd1, *qkv, *att, *lse, *hmid, *ln2, *mean2, *rstd2, *fc, *act;
+  float* tmp_h;                  // [M*d]
+  float* ws;                     // colsum / LN partials
+  float *z, *zmean, *zrstd, *dz;  // head
+  float* row_loss;               // [M]
+  double* loss;                  // [1]
+  float* logits;                 // aliases fc..act, logits_rows x HY_VOCAB_PAD
+  int logits_rows = 0;
+  float* attn_ws;                // [B*H*T]
+};
+
+// Bytes of scratch a worker needs for these dims with `max_blocks` blocks per shard.
+long scratch_floats(const hy_dims& m, int max_blocks);
+void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s);
+
+struct TaskIO {
+  const int32_t* tokens = nullptr;   // [M] device
+  const int32_t* targets = nullptr;  // [M] device
+  const float* act_in = nullptr;     // boundary activation in (l0 > 0)
+  float* act_out = nullptr;          // boundary activation out (forward, no head)
+  const float* grad_in = nullptr;    // dL/d act_out (backward, no head)
+  float* grad_out = nullptr;         // dL/d act_in (backward, l0 > 0)
+  const float* z_in = nullptr;       // saved ln_f output for the deferred tied-wte grad (B of shard 0)
+};
+
+// Forward task: leaves the loss (when the shard has the head) in s.loss[0].
+void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, const TaskIO& io,
+                 Scratch& s);
+// Backward task (recompute + backward): grads (shard layout, pre-zeroed by the caller) +=.
+// When the shard has the head but not the embed, the ln_f output z is left in s.z for the
+// caller to demote; when it has the embed but not the head, io.z_in drives the deferred
+// tied-wte gradient.
+void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, float* grads,
+                  const TaskIO& io, Scratch& s);
+
+void check_cuda(cudaError_t e, const char* what);
+
+}  // namespace hy
