@@ -31,6 +31,8 @@ struct ExecOptions {
   int warmup_passes = 0;           // replays before the timed ones (not in the trace)
   long opt_chunk_floats = 4L << 20;  // Adam m/v streaming chunk
   std::string params_out_dir;      // if set: final params of every executed job as job<j>.f32
+  double hbm_slack_bytes = 0;      // physical arena may exceed mem_bytes by this much (toy configs
+                                   // whose cost model leaves no room for real activations)
 };
 
 struct ExecStats {

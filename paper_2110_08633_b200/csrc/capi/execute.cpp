@@ -71,6 +71,7 @@ std::string execute_json(const std::string& request) {
   ex.passes = req.value("passes", 1);
   ex.warmup_passes = req.value("warmup_passes", 0);
   ex.params_out_dir = req.value("params_out_dir", std::string());
+  ex.hbm_slack_bytes = req.value("hbm_slack_bytes", 0.0);
   if (req.contains("device_ids")) ex.device_ids = req["device_ids"].get<std::vector<int>>();
   if (req.contains("run_devices")) ex.run_devices = req["run_devices"].get<std::vector<int>>();
   if (req.contains("opt_chunk_floats")) ex.opt_chunk_floats = req["opt_chunk_floats"].get<long>();

@@ -338,15 +338,17 @@ void ExecutorImpl::setup_worker(Worker& w) {
   const DeviceSpec& dev = cluster.devices[static_cast<size_t>(w.plan_dev)];
   // Adam m/v staging: a dedicated ring when the HBM cap leaves room, otherwise it aliases
   // the dead MLP activations of the scratch (then compute waits for the m/v write-back).
-  const long budget_floats = static_cast<long>(dev.mem_bytes / 4) - base_floats - 2048;
+  const double cap = dev.mem_bytes + exec.hbm_slack_bytes;
+  const long budget_floats = static_cast<long>(cap / 4) - base_floats - 2048;
   long chunk = std::min(exec.opt_chunk_floats, budget_floats / (2 * kStaging));
   chunk = chunk / 1024 * 1024;
   w.stg_alias = chunk < (1L << 20);
   if (w.stg_alias) chunk = 0;
   const long floats = base_floats + kStaging * 2 * hy_pad32(chunk);
   w.arena_bytes = floats * 4 + 4096;
-  if (static_cast<double>(w.arena_bytes) > dev.mem_bytes) {
-    throw CapacityExhausted(dev.device_id, static_cast<double>(w.arena_bytes), dev.mem_bytes);
+  if (static_cast<double>(w.arena_bytes) > cap) {
+    throw InfeasibleOOM("sharp-executor", "(all jobs on this device)", dev.device_id,
+                        static_cast<double>(w.arena_bytes), cap);
   }
   check_cuda(cudaMalloc(&w.arena, static_cast<size_t>(w.arena_bytes)), "arena cudaMalloc");
   float* p = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(w.arena) + 1023) & ~uintptr_t(1023));

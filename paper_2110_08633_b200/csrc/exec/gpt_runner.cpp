@@ -161,9 +161,16 @@ void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s) {
   // fc and act are adjacent: the head's logits chunk aliases both.
   s->fc = take(4 * M * d);
   s->act = take(4 * M * d);
-  s->logits = s->fc;
-  const long logit_floats = 8 * M * d;
-  s->logits_rows = static_cast<int>(std::min<long>(M, logit_floats / HY_VOCAB_PAD));
+  // Head logits chunk: aliases fc+act when at least 16 rows fit there, else its own region.
+  const long alias_rows = std::min<long>(M, 8 * M * d / HY_VOCAB_PAD);
+  const bool alias_logits = alias_rows >= std::min<long>(M, 16);
+  if (alias_logits) {
+    s->logits = s->fc;
+    s->logits_rows = static_cast<int>(alias_rows);
+  } else {
+    s->logits_rows = static_cast<int>(std::min<long>(M, 16));
+    s->logits = take(static_cast<long>(s->logits_rows) * HY_VOCAB_PAD);
+  }
   s->tmp_h = take(M * d);
   s->ws = take(512L * 4 * d);  // >= colsum_blocks(M) * max(4d, 2d)
   s->z = take(M * d);
