@@ -62,6 +62,19 @@ int hy_plan_json(const char* request_json, char* out, size_t out_len, size_t* ne
  * --------------------------------------------------------------------------------- */
 int hy_execute_json(const char* request_json, char* out, size_t out_len, size_t* needed);
 
+/* Stateful form (what bench.py and long runs use): setup once — pinned host state,
+ * capped HBM arenas, streams, GPT-2 init — then replay the plan pass by pass.
+ * request_json as for hy_execute_json ("passes" + "warmup_passes" bound the total). */
+int hy_executor_create(const char* request_json, void** handle);
+/* Replays the plan `passes` times; timed passes are measured with CUDA events and
+ * accumulate into the result JSON (pass_seconds, losses, byte counters, report). */
+int hy_executor_run(void* handle, int passes, int timed, int with_trace, char* out, size_t out_len,
+                    size_t* needed);
+int hy_executor_dump_params(void* handle, const char* dir);
+void hy_executor_destroy(void* handle);
+/* Kernel launches issued by this library since load (for the bench's gpu_launches). */
+long hy_kernel_launches(void);
+
 /* ---------------------------------------------------------------------------------
  * Kernel entry points (fp32 tensors in HBM, row-major). Used by the executor and by the
  * GPU parity tests; each maps to one hand-written sm_100a kernel (csrc/kernels/).

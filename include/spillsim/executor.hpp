@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -53,6 +54,31 @@ struct ExecResult {
   std::vector<std::vector<double>> losses;     // [job][global minibatch] (executed jobs)
   std::vector<double> pass_seconds;            // per timed pass (max over devices)
   ExecStats stats;
+};
+
+struct ExecutorImpl;
+
+/// Stateful form: setup (pinned host state, HBM arenas, streams, init) once, then replay
+/// the plan pass by pass. Inputs are borrowed and must outlive the executor. At most
+/// exec.warmup_passes + exec.passes passes may be run in total (tokens are pre-drawn).
+class Executor {
+ public:
+  Executor(const ClusterSpec& cluster, const std::vector<SimTask>& tasks, const DispatchPlan& plan,
+           const SimOptions& options, const ExecOptions& exec);
+  ~Executor();
+  Executor(const Executor&) = delete;
+  Executor& operator=(const Executor&) = delete;
+
+  /// Replays the plan `passes` times. Timed passes append to result(): pass_seconds (CUDA
+  /// events on each GPU, max over this process's GPUs), losses, byte counters, trace.
+  void run(int passes, bool timed);
+  ExecResult& result() { return res_; }
+  void dump_params(const std::string& dir) const;
+
+ private:
+  std::unique_ptr<ExecutorImpl> impl_;
+  ExecResult res_;
+  int next_pass_ = 0;
 };
 
 ExecResult run_execution(const ClusterSpec& cluster, const std::vector<SimTask>& tasks, const DispatchPlan& plan,

@@ -19,3 +19,53 @@ def execute(config: dict, **kw) -> dict:
     req = {"config": config}
     req.update(kw)
     return call_json("hy_execute_json", req)
+
+
+class Executor:
+    """Stateful B200 executor over the C-ABI (hy_executor_*): setup once, run passes."""
+
+    def __init__(self, config: dict, **kw):
+        import ctypes
+        import json as _json
+
+        from ._lib import check
+
+        req = {"config": config}
+        req.update(kw)
+        h = ctypes.c_void_p()
+        check(lib().hy_executor_create(_json.dumps(req).encode(), ctypes.byref(h)))
+        self._h = h
+
+    def run(self, passes: int, timed: bool = True, trace: bool = False) -> dict:
+        import ctypes
+        import json as _json
+
+        from ._lib import check
+
+        size = 1 << 22
+        needed = ctypes.c_size_t(0)
+        while True:
+            buf = ctypes.create_string_buffer(size)
+            rc = lib().hy_executor_run(self._h, int(passes), int(timed), int(trace), buf, size, ctypes.byref(needed))
+            if rc == -9:
+                size = needed.value + 1
+                continue
+            check(rc)
+            return _json.loads(buf.value.decode())
+
+    def dump_params(self, directory: str):
+        from ._lib import check
+
+        check(lib().hy_executor_dump_params(self._h, directory.encode()))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hy_executor_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def kernel_launches() -> int:
+    return int(lib().hy_kernel_launches())

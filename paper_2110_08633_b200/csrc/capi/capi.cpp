@@ -9,6 +9,7 @@
 #include <string>
 
 #include "../kernels/gemm.cuh"
+#include "../kernels/launch_count.cuh"
 #include "../kernels/ops.cuh"
 #include "capi_internal.hpp"
 #include "spillsim/errors.hpp"
@@ -88,6 +89,44 @@ int hy_execute_json(const char* request_json, char* out, size_t out_len, size_t*
     return hy::status_from_current_exception();
   }
 }
+
+int hy_executor_create(const char* request_json, void** handle) {
+  try {
+    *handle = hy::session_create(request_json);
+    return HY_OK;
+  } catch (...) {
+    *handle = nullptr;
+    return hy::status_from_current_exception();
+  }
+}
+
+int hy_executor_run(void* handle, int passes, int timed, int with_trace, char* out, size_t out_len,
+                    size_t* needed) {
+  try {
+    if (!handle) return hy::set_error(HY_E_INVALID, "null executor handle");
+    return hy::write_out(hy::session_run(handle, passes, timed != 0, with_trace != 0), out, out_len, needed);
+  } catch (...) {
+    return hy::status_from_current_exception();
+  }
+}
+
+int hy_executor_dump_params(void* handle, const char* dir) {
+  try {
+    hy::session_dump_params(handle, dir);
+    return HY_OK;
+  } catch (...) {
+    return hy::status_from_current_exception();
+  }
+}
+
+void hy_executor_destroy(void* handle) {
+  try {
+    hy::session_destroy(handle);
+  } catch (...) {
+  }
+}
+
+long hy_kernel_launches(void) { return hy::g_kernel_launches.load(); }
 
 int hy_gemm(void* stream, int M, int N, int K, const float* A, long lda, int a_mn, const float* B, long ldb, int b_mn,
             float* C, long ldc, const float* bias, const float* R, long ldr, float beta, int mode, float* Hout,

@@ -11,5 +11,9 @@ int status_from_current_exception();
 // JSON request -> JSON result; throw spillsim exceptions on failure.
 std::string plan_json(const std::string& request);
 std::string execute_json(const std::string& request);
+void* session_create(const std::string& request);
+std::string session_run(void* handle, int passes, bool timed, bool with_trace);
+void session_dump_params(void* handle, const std::string& dir);
+void session_destroy(void* handle);
 
 }  // namespace hy

@@ -2,6 +2,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <memory>
 
 #include "capi_internal.hpp"
 #include "nlohmann/json.hpp"
@@ -50,24 +51,37 @@ ExecJob exec_job_for(const WorkloadConfig& cfg, const JobConfig& jc, const std::
 
 }  // namespace
 
-std::string execute_json(const std::string& request) {
-  const auto t_call = std::chrono::steady_clock::now();
-  const json req = json::parse(request);
-  WorkloadConfig cfg = parse_workload_config(req.at("config").dump());
-  const int gpus = req.value("gpus", 0);
-  if (gpus > 0) replicate_devices(cfg.cluster, gpus);
-  const std::string strategy = req.value("strategy", std::string("sharp"));
-  const bool db = req.value("double_buffering", cfg.options.double_buffering);
-  const std::vector<ModelJob> jobs = materialize_jobs(cfg);
-  CompiledStrategy cs = build_strategy(strategy_for(cfg, strategy_kind_from_string(strategy)), jobs, cfg.cluster,
-                                       cfg.options.buffer_policy);
-  cs.options.double_buffering = db;
-  const auto t_plan0 = std::chrono::steady_clock::now();
-  const DispatchPlan plan = plan_simulation(cfg.cluster, cs.tasks, *cs.scheduler, cs.options);
-  const double plan_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_plan0).count();
-
+// Everything one execution needs, owned together (the Executor borrows from it).
+struct Session {
+  WorkloadConfig cfg;
+  std::string strategy;
+  std::vector<ModelJob> jobs;
+  CompiledStrategy cs;
+  DispatchPlan plan;
   ExecOptions ex;
-  ex.seed = req.value("seed", static_cast<uint64_t>(cfg.seed));
+  double plan_s = 0;
+  std::unique_ptr<Executor> exec;
+  double samples_per_pass = 0, model_flops_per_pass = 0;
+};
+
+std::unique_ptr<Session> make_session(const std::string& request) {
+  auto S = std::make_unique<Session>();
+  const json req = json::parse(request);
+  S->cfg = parse_workload_config(req.at("config").dump());
+  const int gpus = req.value("gpus", 0);
+  if (gpus > 0) replicate_devices(S->cfg.cluster, gpus);
+  S->strategy = req.value("strategy", std::string("sharp"));
+  const bool db = req.value("double_buffering", S->cfg.options.double_buffering);
+  S->jobs = materialize_jobs(S->cfg);
+  S->cs = build_strategy(strategy_for(S->cfg, strategy_kind_from_string(S->strategy)), S->jobs, S->cfg.cluster,
+                         S->cfg.options.buffer_policy);
+  S->cs.options.double_buffering = db;
+  const auto t0 = std::chrono::steady_clock::now();
+  S->plan = plan_simulation(S->cfg.cluster, S->cs.tasks, *S->cs.scheduler, S->cs.options);
+  S->plan_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+
+  ExecOptions& ex = S->ex;
+  ex.seed = req.value("seed", static_cast<uint64_t>(S->cfg.seed));
   ex.passes = req.value("passes", 1);
   ex.warmup_passes = req.value("warmup_passes", 0);
   ex.params_out_dir = req.value("params_out_dir", std::string());
@@ -75,54 +89,54 @@ std::string execute_json(const std::string& request) {
   if (req.contains("device_ids")) ex.device_ids = req["device_ids"].get<std::vector<int>>();
   if (req.contains("run_devices")) ex.run_devices = req["run_devices"].get<std::vector<int>>();
   if (req.contains("opt_chunk_floats")) ex.opt_chunk_floats = req["opt_chunk_floats"].get<long>();
-  for (size_t j = 0; j < cfg.jobs.size(); ++j) {
+  for (size_t j = 0; j < S->cfg.jobs.size(); ++j) {
     std::vector<int> starts{0};
-    if (j < cs.partitionings.size()) starts = cs.partitionings[j].shard_starts;
-    ex.jobs.push_back(exec_job_for(cfg, cfg.jobs[j], starts));
+    if (j < S->cs.partitionings.size()) starts = S->cs.partitionings[j].shard_starts;
+    ex.jobs.push_back(exec_job_for(S->cfg, S->cfg.jobs[j], starts));
   }
-  ExecResult r = run_execution(cfg.cluster, cs.tasks, plan, cs.options, ex);
-
-  // Work of the executed devices per pass: samples and cost-model roofline terms.
-  const int G = static_cast<int>(cfg.cluster.devices.size());
-  const auto per_dev = plan.per_device(G);
+  // Work of the GPUs this process executes, per pass.
+  const int G = static_cast<int>(S->cfg.cluster.devices.size());
+  const auto per_dev = S->plan.per_device(G);
   std::vector<int> run = ex.run_devices;
   if (run.empty()) {
     for (int d = 0; d < G; ++d) run.push_back(d);
   }
-  double samples = 0, roofline_link_s = 0, model_flops = 0;
   for (int d : run) {
     for (int t : per_dev[static_cast<size_t>(d)]) {
-      const ShardTask& task = cs.tasks[static_cast<size_t>(t)].t;
-      const ModelJob& job = jobs[static_cast<size_t>(task.job)];
-      const auto* spec = &cfg.models[0];
-      for (const auto& m : cfg.models) {
-        if (m.name == cfg.jobs[static_cast<size_t>(task.job)].model) spec = &m;
+      const ShardTask& task = S->cs.tasks[static_cast<size_t>(t)].t;
+      const JobConfig& jc = S->cfg.jobs[static_cast<size_t>(task.job)];
+      double F = 1.0;
+      for (const ModelSpec& m : S->cfg.models) {
+        if (m.name == jc.model && m.transformer) F = m.transformer->device_reference_flops;
       }
-      const double F = spec->transformer ? spec->transformer->device_reference_flops : 1.0;
-      model_flops += task.compute_s * F;
-      if (task.direction == Direction::kBackward && task.shard == 0) samples += job.batch_size;
+      S->model_flops_per_pass += task.compute_s * F;
+      if (task.direction == Direction::kBackward && task.shard == 0) S->samples_per_pass += jc.batch_size;
     }
   }
-  (void)roofline_link_s;
+  S->exec = std::make_unique<Executor>(S->cfg.cluster, S->cs.tasks, S->plan, S->cs.options, ex);
+  return S;
+}
 
+ojson session_result(Session& S, bool with_trace) {
+  const ExecResult& r = S.exec->result();
   ojson out;
   char h[32];
-  std::snprintf(h, sizeof h, "%016llx", plan.hash());
+  std::snprintf(h, sizeof h, "%016llx", S.plan.hash());
   out["dispatch_hash"] = h;
-  out["virtual_makespan_s"] = plan.trace.makespan_s;
-  out["plan_wall_s"] = plan_s;
+  out["virtual_makespan_s"] = S.plan.trace.makespan_s;
+  out["plan_wall_s"] = S.plan_s;
   out["pass_seconds"] = r.pass_seconds;
   out["makespan_s"] = r.stats.makespan_s;
-  out["samples_per_pass"] = samples;
-  out["model_flops_per_pass"] = model_flops;
+  out["samples_per_pass"] = S.samples_per_pass;
+  out["model_flops_per_pass"] = S.model_flops_per_pass;
   ojson losses = ojson::array();
   for (const auto& l : r.losses) losses.push_back(l);
   out["losses"] = losses;
   ojson parts = ojson::array();
-  for (const Partitioning& p : cs.partitionings) parts.push_back(p.shard_starts);
+  for (const Partitioning& p : S.cs.partitionings) parts.push_back(p.shard_starts);
   out["shard_starts"] = parts;
   ojson st;
-  const double np = std::max<size_t>(1, r.pass_seconds.size());
+  const double np = static_cast<double>(std::max<size_t>(1, r.pass_seconds.size()));
   st["h2d_bytes_per_pass"] = r.stats.h2d_bytes / np;
   st["d2h_bytes_per_pass"] = r.stats.d2h_bytes / np;
   st["model_h2d_bytes_per_pass"] = r.stats.model_h2d_bytes / np;
@@ -138,12 +152,39 @@ std::string execute_json(const std::string& request) {
   st["pinned_bytes"] = r.stats.pinned_bytes;
   st["device_busy_s_last_pass"] = r.stats.device_busy_s.empty() ? 0.0 : r.stats.device_busy_s.back();
   st["setup_s"] = r.stats.setup_s;
-  st["adam_launches"] = r.stats.kernel_launches;
   out["stats"] = st;
-  out["report"] = ojson::parse(report_to_json(summarize(r.trace, cfg.cluster, strategy)));
-  if (req.value("trace", false)) out["chrome_trace"] = to_chrome_trace_json(r.trace);
+  if (!r.pass_seconds.empty()) {
+    out["report"] = ojson::parse(report_to_json(summarize(r.trace, S.cfg.cluster, S.strategy)));
+    if (with_trace) out["chrome_trace"] = to_chrome_trace_json(r.trace);
+  }
+  return out;
+}
+
+std::string execute_json(const std::string& request) {
+  const auto t_call = std::chrono::steady_clock::now();
+  const json req = json::parse(request);
+  std::unique_ptr<Session> S = make_session(request);
+  S->exec->run(S->ex.warmup_passes, false);
+  S->exec->run(S->ex.passes, true);
+  if (!S->ex.params_out_dir.empty()) S->exec->dump_params(S->ex.params_out_dir);
+  ojson out = session_result(*S, req.value("trace", false));
   out["wall_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call).count();
   return out.dump();
 }
+
+void* session_create(const std::string& request) { return make_session(request).release(); }
+
+std::string session_run(void* handle, int passes, bool timed, bool with_trace) {
+  Session* S = static_cast<Session*>(handle);
+  const auto t0 = std::chrono::steady_clock::now();
+  S->exec->run(passes, timed);
+  ojson out = session_result(*S, with_trace);
+  out["wall_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return out.dump();
+}
+
+void session_dump_params(void* handle, const std::string& dir) { static_cast<Session*>(handle)->exec->dump_params(dir); }
+
+void session_destroy(void* handle) { delete static_cast<Session*>(handle); }
 
 }  // namespace hy

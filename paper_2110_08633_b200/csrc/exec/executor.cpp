@@ -890,51 +890,62 @@ void ExecutorImpl::collect(int pass, ExecResult& res) {
   res.pass_seconds.push_back(pass_max);
 }
 
+Executor::Executor(const ClusterSpec& cluster, const std::vector<SimTask>& tasks, const DispatchPlan& plan,
+                   const SimOptions& options, const ExecOptions& exec)
+    : impl_(new ExecutorImpl(cluster, tasks, plan, options, exec)) {
+  impl_->setup(res_);
+}
+
+Executor::~Executor() = default;
+
+void Executor::run(int passes, bool timed) {
+  const int limit = impl_->exec.warmup_passes + impl_->exec.passes;
+  for (int i = 0; i < passes; ++i) {
+    if (next_pass_ >= limit) throw InvalidArgument("executor: more passes than ExecOptions allowed");
+    for (auto& w : impl_->workers) w->st = ExecStats{};
+    impl_->run_pass(next_pass_++, timed, res_);
+    if (!timed) continue;
+    ExecStats& a = res_.stats;
+    for (auto& w : impl_->workers) {
+      const ExecStats& b = w->st;
+      a.h2d_bytes += b.h2d_bytes;
+      a.d2h_bytes += b.d2h_bytes;
+      a.model_h2d_bytes += b.model_h2d_bytes;
+      a.model_d2h_bytes += b.model_d2h_bytes;
+      a.param_h2d_bytes += b.param_h2d_bytes;
+      a.opt_h2d_bytes += b.opt_h2d_bytes;
+      a.opt_d2h_bytes += b.opt_d2h_bytes;
+      a.act_h2d_bytes += b.act_h2d_bytes;
+      a.act_d2h_bytes += b.act_d2h_bytes;
+      a.elided_param_bytes += b.elided_param_bytes;
+      a.elided_act_bytes += b.elided_act_bytes;
+      a.kernel_launches += b.kernel_launches;
+    }
+  }
+  double total = 0;
+  for (double x : res_.pass_seconds) total += x;
+  res_.stats.makespan_s = res_.pass_seconds.empty() ? 0 : total / static_cast<double>(res_.pass_seconds.size());
+  res_.stats.arena_bytes.clear();
+  for (auto& w : impl_->workers) res_.stats.arena_bytes.push_back(static_cast<double>(w->arena_bytes));
+}
+
+void Executor::dump_params(const std::string& dir) const {
+  for (auto& kv : impl_->jobs) {
+    const std::string path = dir + "/job" + std::to_string(kv.first) + ".f32";
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw InvalidArgument("cannot write " + path);
+    std::fwrite(kv.second.params, sizeof(float), static_cast<size_t>(kv.second.total), f);
+    std::fclose(f);
+  }
+}
+
 ExecResult run_execution(const ClusterSpec& cluster, const std::vector<SimTask>& tasks, const DispatchPlan& plan,
                          const SimOptions& options, const ExecOptions& exec) {
-  ExecResult res;
-  ExecutorImpl ex(cluster, tasks, plan, options, exec);
-  ex.setup(res);
-  const int total = exec.warmup_passes + exec.passes;
-  for (int p = 0; p < total; ++p) {
-    const bool timed = p >= exec.warmup_passes;
-    if (timed) {
-      for (auto& w : ex.workers) w->st = ExecStats{};
-    }
-    ex.run_pass(p, timed, res);
-    if (timed) {
-      for (auto& w : ex.workers) {
-        ExecStats& a = res.stats;
-        const ExecStats& b = w->st;
-        a.h2d_bytes += b.h2d_bytes;
-        a.d2h_bytes += b.d2h_bytes;
-        a.model_h2d_bytes += b.model_h2d_bytes;
-        a.model_d2h_bytes += b.model_d2h_bytes;
-        a.param_h2d_bytes += b.param_h2d_bytes;
-        a.opt_h2d_bytes += b.opt_h2d_bytes;
-        a.opt_d2h_bytes += b.opt_d2h_bytes;
-        a.act_h2d_bytes += b.act_h2d_bytes;
-        a.act_d2h_bytes += b.act_d2h_bytes;
-        a.elided_param_bytes += b.elided_param_bytes;
-        a.elided_act_bytes += b.elided_act_bytes;
-        a.kernel_launches += b.kernel_launches;
-      }
-    }
-  }
-  for (auto& w : ex.workers) res.stats.arena_bytes.push_back(static_cast<double>(w->arena_bytes));
-  double ms = 0;
-  for (double s : res.pass_seconds) ms += s;
-  res.stats.makespan_s = res.pass_seconds.empty() ? 0 : ms / static_cast<double>(res.pass_seconds.size());
-  if (!exec.params_out_dir.empty()) {
-    for (auto& kv : ex.jobs) {
-      const std::string path = exec.params_out_dir + "/job" + std::to_string(kv.first) + ".f32";
-      FILE* f = std::fopen(path.c_str(), "wb");
-      if (!f) throw InvalidArgument("cannot write " + path);
-      std::fwrite(kv.second.params, sizeof(float), static_cast<size_t>(kv.second.total), f);
-      std::fclose(f);
-    }
-  }
-  return res;
+  Executor ex(cluster, tasks, plan, options, exec);
+  ex.run(exec.warmup_passes, false);
+  ex.run(exec.passes, true);
+  if (!exec.params_out_dir.empty()) ex.dump_params(exec.params_out_dir);
+  return std::move(ex.result());
 }
 
 }  // namespace spillsim

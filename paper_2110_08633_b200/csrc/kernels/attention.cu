@@ -4,6 +4,7 @@
 // Reads the fused QKV projection in place ([B*T, 3*H*64]) and writes dQKV in the same layout.
 #include <cfloat>
 
+#include "launch_count.cuh"
 #include "ops.cuh"
 
 namespace hy {
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(2 * TILE) attn_bwd_q_kernel(int T, int H, cons
 
 cudaError_t attention_fwd(cudaStream_t s, int B, int T, int H, const float* qkv, float* out, float* lse) {
   dim3 grid((T + TILE - 1) / TILE, B * H);
+  count_launch();
   attn_fwd_kernel<<<grid, TILE, 0, s>>>(T, H, qkv, out, lse);
   return cudaGetLastError();
 }
@@ -280,9 +282,12 @@ cudaError_t attention_fwd(cudaStream_t s, int B, int T, int H, const float* qkv,
 cudaError_t attention_bwd(cudaStream_t s, int B, int T, int H, const float* qkv, const float* out, const float* dout,
                           const float* lse, float* dqkv, float* ws) {
   const long n = static_cast<long>(B) * T * H;
+  count_launch();
   attn_delta_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(B * T, H, T, out, dout, ws);
   dim3 grid((T + TILE - 1) / TILE, B * H);
+  count_launch();
   attn_bwd_kv_kernel<<<grid, 2 * TILE, 0, s>>>(T, H, qkv, dout, lse, ws, dqkv);
+  count_launch();
   attn_bwd_q_kernel<<<grid, 2 * TILE, 0, s>>>(T, H, qkv, dout, lse, ws, dqkv);
   return cudaGetLastError();
 }

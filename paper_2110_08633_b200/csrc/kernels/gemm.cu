@@ -15,6 +15,7 @@
 #include <mutex>
 
 #include "gemm.cuh"
+#include "launch_count.cuh"
 #include "ptx.cuh"
 
 namespace hy {
@@ -291,6 +292,7 @@ cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, lon
   }
   const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
   const int grid = tiles < sm_count() ? tiles : sm_count();
+  count_launch();
   kern<<<grid, kThreads, Smem<BN>::kTotal, stream>>>(ma, mb, M, N, K, epi);
   return cudaGetLastError();
 }

@@ -2,6 +2,7 @@
 // grid-stride float4 loops for elementwise work, two-stage deterministic column sums.
 #include <cfloat>
 
+#include "launch_count.cuh"
 #include "ops.cuh"
 
 namespace hy {
@@ -322,10 +323,13 @@ cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const
   if (d % 4 || d > 4 * 32 * kMaxVecAll) return cudaErrorInvalidValue;
   const int grid = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock, block = 32 * kWarpsPerBlock;
   if (d <= 1024) {
+    count_launch();
     ln_fwd_kernel<8><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
   } else if (d <= 2048) {
+    count_launch();
     ln_fwd_kernel<16><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
   } else {
+    count_launch();
     ln_fwd_kernel<32><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
   }
   return cudaGetLastError();
@@ -350,13 +354,18 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
   float* ws_db = ws + static_cast<long>(nb) * d;
   const int acc = accumulate_dx ? 1 : 0;
   if (d <= 1024) {
+    count_launch();
     ln_bwd_kernel<8><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
   } else if (d <= 2048) {
+    count_launch();
     ln_bwd_kernel<16><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
   } else {
+    count_launch();
     ln_bwd_kernel<32><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
   }
+  count_launch();
   reduce_parts_kernel<<<(d + 255) / 256, 256, 0, s>>>(nb, d, ws_dg, dg, 1);
+  count_launch();
   reduce_parts_kernel<<<(d + 255) / 256, 256, 0, s>>>(nb, d, ws_db, db, 1);
   return cudaGetLastError();
 }
@@ -365,7 +374,9 @@ cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float
   const int nb = colsum_blocks(M);
   const int rpb = (M + nb - 1) / nb;
   dim3 grid((N + 255) / 256, nb);
+  count_launch();
   colsum_part_kernel<<<grid, 256, 0, s>>>(M, N, X, ldx, ws, rpb);
+  count_launch();
   reduce_parts_kernel<<<(N + 255) / 256, 256, 0, s>>>(nb, N, ws, out, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
@@ -374,6 +385,7 @@ cudaError_t embed_fwd(cudaStream_t s, int rows, int T, int d, const int32_t* tok
                       float* h) {
   if (d % 4) return cudaErrorInvalidValue;
   const long n = static_cast<long>(rows) * (d / 4);
+  count_launch();
   embed_fwd_kernel<<<grid_for(n, 256), 256, 0, s>>>(rows, T, d, tok, wte, wpe, h);
   return cudaGetLastError();
 }
@@ -381,7 +393,9 @@ cudaError_t embed_fwd(cudaStream_t s, int rows, int T, int d, const int32_t* tok
 cudaError_t embed_bwd(cudaStream_t s, int rows, int T, int d, const int32_t* tok, const float* dh, float* dwte,
                       float* dwpe, float* /*ws*/) {
   const long n = static_cast<long>(rows) * d;
+  count_launch();
   embed_scatter_kernel<<<grid_for(n, 256), 256, 0, s>>>(rows, d, tok, dh, dwte);
+  count_launch();
   embed_pos_kernel<<<grid_for(static_cast<long>(T) * d, 256), 256, 0, s>>>(rows / T, T, d, dh, dwpe);
   return cudaGetLastError();
 }
@@ -389,11 +403,13 @@ cudaError_t embed_bwd(cudaStream_t s, int rows, int T, int d, const int32_t* tok
 cudaError_t softmax_xent(cudaStream_t s, int rows, int V, float* logits, long ldl, const int32_t* targets,
                          float grad_scale, float* row_loss) {
   if (rows <= 0) return cudaSuccess;
+  count_launch();
   xent_kernel<<<rows, 512, 0, s>>>(V, logits, ldl, targets, grad_scale, row_loss);
   return cudaGetLastError();
 }
 
 cudaError_t sum_to_double(cudaStream_t s, int n, const float* x, double* out, bool accumulate) {
+  count_launch();
   sum_double_kernel<<<1, 256, 0, s>>>(n, x, out, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
@@ -401,6 +417,7 @@ cudaError_t sum_to_double(cudaStream_t s, int n, const float* x, double* out, bo
 cudaError_t adam_update(cudaStream_t s, long n, float* p, const float* g, float* m, float* v, const AdamHyper& h) {
   if (n % 4) return cudaErrorInvalidValue;
   const long n4 = n / 4;
+  count_launch();
   adam_kernel<<<grid_for(n4, 256), 256, 0, s>>>(n4, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                                 reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), h);
   return cudaGetLastError();
