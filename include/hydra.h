@@ -92,9 +92,12 @@ int hy_layernorm_fwd(void* stream, int rows, int d, const float* x, const float*
 int hy_layernorm_bwd(void* stream, int rows, int d, const float* x, const float* g, const float* mean,
                      const float* rstd, const float* dy, float* dx, int accumulate_dx, float* dg, float* db,
                      float* ws);
-int hy_attention_fwd(void* stream, int B, int T, int H, int hd, const float* qkv, float* out, float* lse);
-int hy_attention_bwd(void* stream, int B, int T, int H, int hd, const float* qkv, const float* out,
-                     const float* dout, const float* lse, float* dqkv, float* ws);
+/* Causal attention on tcgen05 (head dim 64). qkv [B*T, 3*H*64]; out [B*T, H*64]. `work`
+ * holds score matrices: >= T*T floats (fwd) / 2*T*T (bwd); (batch, head) chunks sized to it. */
+int hy_attention_fwd(void* stream, int B, int T, int H, int hd, const float* qkv, float* out, float* work,
+                     long work_floats);
+int hy_attention_bwd(void* stream, int B, int T, int H, int hd, const float* qkv, const float* dout, float* dqkv,
+                     float* work, long work_floats);
 int hy_embed_fwd(void* stream, int rows, int T, int d, const int32_t* tokens, const float* wte, const float* wpe,
                  float* h);
 int hy_embed_bwd(void* stream, int rows, int T, int d, int V, const int32_t* tokens, const float* dh, float* dwte,

@@ -161,16 +161,19 @@ int hy_layernorm_bwd(void* stream, int rows, int d, const float* x, const float*
                      "hy_layernorm_bwd");
 }
 
-int hy_attention_fwd(void* stream, int B, int T, int H, int hd, const float* qkv, float* out, float* lse) {
+int hy_attention_fwd(void* stream, int B, int T, int H, int hd, const float* qkv, float* out, float* work,
+                     long work_floats) {
   if (hd != 64) return hy::set_error(HY_E_INVALID, "attention: head dim must be 64");
-  return cuda_status(hy::attention_fwd(static_cast<cudaStream_t>(stream), B, T, H, qkv, out, lse), "hy_attention_fwd");
+  return cuda_status(hy::attention_fwd_tc(static_cast<cudaStream_t>(stream), B, T, H, qkv, out, work, work_floats),
+                     "hy_attention_fwd");
 }
 
-int hy_attention_bwd(void* stream, int B, int T, int H, int hd, const float* qkv, const float* out,
-                     const float* dout, const float* lse, float* dqkv, float* ws) {
+int hy_attention_bwd(void* stream, int B, int T, int H, int hd, const float* qkv, const float* dout, float* dqkv,
+                     float* work, long work_floats) {
   if (hd != 64) return hy::set_error(HY_E_INVALID, "attention: head dim must be 64");
-  return cuda_status(hy::attention_bwd(static_cast<cudaStream_t>(stream), B, T, H, qkv, out, dout, lse, dqkv, ws),
-                     "hy_attention_bwd");
+  return cuda_status(
+      hy::attention_bwd_tc(static_cast<cudaStream_t>(stream), B, T, H, qkv, dout, dqkv, work, work_floats),
+      "hy_attention_bwd");
 }
 
 int hy_embed_fwd(void* stream, int rows, int T, int d, const int32_t* tokens, const float* wte, const float* wpe,

@@ -470,6 +470,10 @@ void ExecutorImpl::adam_writeback(Worker& w, HostJob& hj, int s, int slot, int s
   mvt.before_read(w.opt);
   ptr.before_write(w.up);
   mvt.before_write(w.up);
+  // Adam runs on the opt stream (not comp): the next shard's compute overlaps this shard's
+  // optimizer-state streaming. It reads the grads and rewrites the slot's params in place.
+  w.slot_tr[slot].before_write(w.opt);
+  w.gbuf_tr.before_read(w.opt);
   int c = 0;
   for (long off = 0; off < g.param_floats; off += chunk, ++c) {
     const long n = std::min(chunk, g.param_floats - off);
@@ -478,19 +482,15 @@ void ExecutorImpl::adam_writeback(Worker& w, HostJob& hj, int s, int slot, int s
     float* sm = w.stg[si];
     float* sv = w.stg[si] + chunk;
     Tracked& stg = w.stg_tr[si];
-    // opt stream: m, v chunk -> staging
+    // opt stream: m, v chunk -> staging, then fused Adam on (params, grads, m, v)
     stg.before_write(w.opt);
     check_cuda(cudaMemcpyAsync(sm, hj.mom + base + off, bytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
     check_cuda(cudaMemcpyAsync(sv, hj.var + base + off, bytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
-    stg.after_write(w.opt);
     w.st.opt_h2d_bytes += 2.0 * bytes;
     w.st.h2d_bytes += 2.0 * bytes;
-    // compute: fused Adam on (slot params, grads, m, v)
-    stg.before_read(w.comp);
-    stg.before_write(w.comp);
-    check_cuda(hy::adam_update(w.comp, n, w.slot[slot] + off, w.gbuf + off, sm, sv, h), "adam");
+    check_cuda(hy::adam_update(w.opt, n, w.slot[slot] + off, w.gbuf + off, sm, sv, h), "adam");
     ++w.st.kernel_launches;
-    stg.after_write(w.comp);
+    stg.after_write(w.opt);
     // up: updated params + m, v -> host
     stg.before_read(w.up);
     check_cuda(cudaMemcpyAsync(hj.params + base + off, w.slot[slot] + off, bytes, cudaMemcpyDeviceToHost, w.up),
@@ -502,10 +502,9 @@ void ExecutorImpl::adam_writeback(Worker& w, HostJob& hj, int s, int slot, int s
     w.st.d2h_bytes += 3.0 * bytes;
   }
   mvt.after_read(w.opt);
-  // the slot was written by Adam (compute) and read by the write-back (up)
-  w.slot_tr[slot].after_write(w.comp);
+  w.slot_tr[slot].after_write(w.opt);
   w.slot_tr[slot].after_read(w.up);
-  w.gbuf_tr.after_read(w.comp);
+  w.gbuf_tr.after_read(w.opt);
   check_cuda(cudaEventRecord(w.timing[static_cast<size_t>(local)].d1, w.up), "d1");
   ptr.after_write(w.up);
   mvt.after_write(w.up);
@@ -694,8 +693,6 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       io.grad_out = w.gbd[gout];
     }
     if (needs_z) io.z_in = w.zbuf;
-    w.gbuf_tr.before_write(w.comp);
-    check_cuda(cudaMemsetAsync(w.gbuf, 0, sizeof(float) * static_cast<size_t>(g.param_floats), w.comp), "zero grads");
   }
   // targets live in the second half of the token buffer ([tokens | targets], 2*M ints)
   io.targets = need_tokens ? w.tok[tok_i] + hj.M : nullptr;
@@ -706,7 +703,13 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
                  "loss copy");
     }
   } else {
-    hy::run_backward(w.comp, hj.m, g, w.slot[slot], w.gbuf, io, sc);
+    // The previous shard's Adam (opt stream) may still read the grad buffer: wait for it
+    // only after this shard's forward recompute, then zero it.
+    hy::run_backward(w.comp, hj.m, g, w.slot[slot], w.gbuf, io, sc, [&] {
+      w.gbuf_tr.before_write(w.comp);
+      check_cuda(cudaMemsetAsync(w.gbuf, 0, sizeof(float) * static_cast<size_t>(g.param_floats), w.comp),
+                 "zero grads");
+    });
     if (w.stg_alias) {
       for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // m/v loads wait for the backward
     }

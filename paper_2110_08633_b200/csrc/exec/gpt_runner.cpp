@@ -63,7 +63,8 @@ void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const floa
   const int M = s.M, d = m.d;
   check_cuda(layernorm_fwd(st, M, d, h_in, bt(w, d, HY_LN1_G), bt(w, d, HY_LN1_B), s.ln1, s.mean1, s.rstd1), "ln1");
   gemm(st, M, 3 * d, d, s.ln1, d, false, bt(w, d, HY_WQKV), d, false, s.qkv, 3 * d, bt(w, d, HY_BQKV));
-  check_cuda(attention_fwd(st, m.B, m.T, m.H, s.qkv, s.att, s.lse), "attn_fwd");
+  // scores live in the (not yet written) MLP buffers fc+act: 8*M*d floats, contiguous
+  check_cuda(attention_fwd_tc(st, m.B, m.T, m.H, s.qkv, s.att, s.fc, s.act + 4L * M * d - s.fc), "attn_fwd");
   gemm(st, M, d, d, s.att, d, false, bt(w, d, HY_WO), d, false, s.hmid, d, bt(w, d, HY_BO), h_in, d);
   check_cuda(layernorm_fwd(st, M, d, s.hmid, bt(w, d, HY_LN2_G), bt(w, d, HY_LN2_B), s.ln2, s.mean2, s.rstd2), "ln2");
   gemm(st, M, 4 * d, d, s.ln2, d, false, bt(w, d, HY_WFC), d, false, s.act, 4 * d, bt(w, d, HY_BFC), nullptr, 0, 0.f,
@@ -93,8 +94,10 @@ void block_backward(cudaStream_t st, const hy_dims& m, const float* w, float* gw
   check_cuda(colsum(st, M, d, dh, d, btw(gw, d, HY_BO), true, s.ws), "colsum bo");
   float* datt = s.ln2;  // ln2 dead after dWfc
   gemm(st, M, d, d, dh, d, false, bt(w, d, HY_WO), d, true, datt, d);
-  float* dqkv = s.act;  // dact dead after dln2 / dWfc
-  check_cuda(attention_bwd(st, m.B, m.T, m.H, s.qkv, s.att, datt, s.lse, dqkv, s.attn_ws), "attn bwd");
+  // fc (dln2) and act (dact) are dead here: dqkv takes fc[0, 3Md), scores the rest of fc+act
+  float* dqkv = s.fc;
+  float* work = s.fc + 3L * M * d;
+  check_cuda(attention_bwd_tc(st, m.B, m.T, m.H, s.qkv, datt, dqkv, work, s.act + 4L * M * d - work), "attn bwd");
   gemm(st, 3 * d, d, M, dqkv, 3 * d, true, s.ln1, d, true, btw(gw, d, HY_WQKV), d, nullptr, nullptr, 0, 1.f);
   check_cuda(colsum(st, M, 3 * d, dqkv, 3 * d, btw(gw, d, HY_BQKV), true, s.ws), "colsum bqkv");
   float* dln1 = s.hmid;  // hmid dead after ln2 bwd
@@ -210,7 +213,7 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
 }
 
 void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, float* grads,
-                  const TaskIO& io, Scratch& s) {
+                  const TaskIO& io, Scratch& s, const std::function<void()>& before_grads) {
   const long n = static_cast<long>(s.M) * m.d;
   const int b0 = std::max(g.l0, 1);
   const int nb = g.n_blocks;
@@ -224,6 +227,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   for (int i = 0; i < nb; ++i) {
     block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, s.stash + (i + 1) * n, s);
   }
+  if (before_grads) before_grads();
   // 2) gradient wrt the shard output
   float* dh = s.tmp_h;
   if (g.has_head) {

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 
 #include "hydra_gpt.h"
 
@@ -58,8 +59,10 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
 // When the shard has the head but not the embed, the ln_f output z is left in s.z for the
 // caller to demote; when it has the embed but not the head, io.z_in drives the deferred
 // tied-wte gradient.
+// `before_grads` runs (on the host, enqueue order) after the forward recompute and before
+// anything writes `grads` — the caller inserts its stream waits / zeroing there.
 void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, float* grads,
-                  const TaskIO& io, Scratch& s);
+                  const TaskIO& io, Scratch& s, const std::function<void()>& before_grads);
 
 void check_cuda(cudaError_t e, const char* what);
 

@@ -46,10 +46,45 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
+struct TileInfo {
+  int m0, n0, z1, z2;
+  int kb0, nkb;  // first k-block, number of k-blocks
+  bool skip;     // tile not computed (causal upper)
+};
+
+template <int BN>
+__device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n, int M, int N, int K, int nb2,
+                                              int causal) {
+  TileInfo t;
+  const int per_batch = tiles_m * tiles_n;
+  const int z = tile / per_batch;
+  const int r = tile - z * per_batch;
+  t.z1 = z / nb2;
+  t.z2 = z - t.z1 * nb2;
+  t.m0 = (r % tiles_m) * BM;
+  t.n0 = (r / tiles_m) * BN;
+  const int kb_all = (K + BK - 1) / BK;
+  t.kb0 = 0;
+  t.nkb = kb_all;
+  t.skip = false;
+  if (causal == kCausalSkipUpper) {
+    t.skip = t.n0 >= t.m0 + BM;
+  } else if (causal == kCausalKLower) {
+    const int kend = min(K, t.m0 + BM);
+    t.nkb = (kend + BK - 1) / BK;
+  } else if (causal == kCausalKUpper) {
+    t.kb0 = t.m0 / BK;
+    t.nkb = max(0, kb_all - t.kb0);
+  }
+  (void)M;
+  (void)N;
+  return t;
+}
+
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
-                 int N, int K, GemmEpilogue epi) {
+                 int N, int K, GemmEpilogue epi, GemmBatch bat) {
   using L = Smem<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -62,8 +97,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   const uint32_t warp = warp_id();
   const int tiles_m = (M + BM - 1) / BM;
   const int tiles_n = (N + BN - 1) / BN;
-  const int n_tiles = tiles_m * tiles_n;
-  const int k_blocks = (K + BK - 1) / BK;
+  const int n_tiles = tiles_m * tiles_n * bat.nb1 * bat.nb2;
 
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&map_a);
@@ -89,9 +123,9 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int m0 = (tile % tiles_m) * BM;
-        const int n0 = (tile / tiles_m) * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal);
+        if (ti.skip) continue;
+        for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
@@ -99,15 +133,23 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
           const int k0 = kb * BK;
           if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 32; ++j) tma_load_2d(sa + j * (32 * BK * 4), &map_a, &full[stage], m0 + 32 * j, k0);
+            for (int j = 0; j < BM / 32; ++j) {
+              if (bat.a_perm) tma_load_4d(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, ti.z2, k0, ti.z1);
+              else tma_load_4d(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, k0, ti.z2, ti.z1);
+            }
           } else {
-            tma_load_2d(sa, &map_a, &full[stage], k0, m0);
+            if (bat.a_perm) tma_load_4d(sa, &map_a, &full[stage], k0, ti.z2, ti.m0, ti.z1);
+            else tma_load_4d(sa, &map_a, &full[stage], k0, ti.m0, ti.z2, ti.z1);
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) tma_load_2d(sb + j * (32 * BK * 4), &map_b, &full[stage], n0 + 32 * j, k0);
+            for (int j = 0; j < BN / 32; ++j) {
+              if (bat.b_perm) tma_load_4d(sb + j * (32 * BK * 4), &map_b, &full[stage], ti.n0 + 32 * j, ti.z2, k0, ti.z1);
+              else tma_load_4d(sb + j * (32 * BK * 4), &map_b, &full[stage], ti.n0 + 32 * j, k0, ti.z2, ti.z1);
+            }
           } else {
-            tma_load_2d(sb, &map_b, &full[stage], k0, n0);
+            if (bat.b_perm) tma_load_4d(sb, &map_b, &full[stage], k0, ti.z2, ti.n0, ti.z1);
+            else tma_load_4d(sb, &map_b, &full[stage], k0, ti.n0, ti.z2, ti.z1);
           }
           if (++stage == kStages) {
             stage = 0;
@@ -121,13 +163,21 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal);
+      if (ti.skip) continue;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
+      ++local;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < k_blocks; ++kb) {
+      if (ti.nkb == 0) {
+        if (elect_one()) mbar_arrive(&tfull[acc]);
+        __syncwarp();
+        continue;
+      }
+      for (int kb = 0; kb < ti.nkb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (elect_one()) {
@@ -145,7 +195,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
             mma_tf32(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           mma_commit(&empty[stage]);
-          if (kb == k_blocks - 1) mma_commit(&tfull[acc]);
+          if (kb == ti.nkb - 1) mma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == kStages) {
@@ -157,22 +207,33 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;  // TMEM lane quarter this warp may access
     int local = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++local) {
-      const int m0 = (tile % tiles_m) * BM;
-      const int n0 = (tile / tiles_m) * BN;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal);
+      if (ti.skip) continue;
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ++local;
       tc_fence_after();
-      const int row = m0 + static_cast<int>(q * 32 + lane_id());
+      const int row = ti.m0 + static_cast<int>(q * 32 + lane_id());
       const bool row_ok = row < M;
+      float* Cb = epi.C + ti.z1 * bat.c_s1 + ti.z2 * bat.c_s2;
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         float v[32];
-        tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, v);
-        const int col0 = n0 + c * 32;
+        if (ti.nkb > 0) {
+          tmem_ld_32x32b_x32(tmem_base + ((q * 32) << 16) + acc * BN + c * 32, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        const int col0 = ti.n0 + c * 32;
         if (!row_ok || col0 >= N) continue;
         const bool full_chunk = col0 + 32 <= N;
-        float* crow = epi.C + static_cast<long>(row) * epi.ldc + col0;
+        float* crow = Cb + static_cast<long>(row) * epi.ldc + col0;
+        if (epi.alpha != 1.f) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] *= epi.alpha;
+        }
         if (epi.mode == kEpiGeluBwd) {
           const float* hrow = epi.Hin + static_cast<long>(row) * epi.ldhi + col0;
 #pragma unroll
@@ -249,20 +310,28 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer`, row stride ld.
+// 4-D fp32 tensor map over {inner, outer, b2, b1}: row stride ld, batch strides s2, s1
+// (elements). Dimensions are ordered by increasing stride: {inner, outer, b2, b1}, or
+// {inner, b2, outer, b1} when b2's stride is below the row stride (*perm = 1).
 bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long ld, int box_inner, int box_outer,
-              bool mn_major) {
+              bool mn_major, long nb2 = 1, long s2 = 0, long nb1 = 1, long s1 = 0, int* perm = nullptr) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(outer)};
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+  const long st2 = s2 > 0 ? s2 : ld * outer;
+  const long st1 = s1 > 0 ? s1 : st2 * nb2;
+  const bool swap = nb2 > 1 && st2 < ld;
+  if (perm) *perm = swap ? 1 : 0;
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(swap ? nb2 : outer),
+                        static_cast<cuuint64_t>(swap ? outer : nb2), static_cast<cuuint64_t>(nb1)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(swap ? st2 : ld) * 4, static_cast<cuuint64_t>(swap ? ld : st2) * 4,
+                           static_cast<cuuint64_t>(st1) * 4};
+  cuuint32_t box[4] = {static_cast<cuuint32_t>(box_inner), swap ? 1u : static_cast<cuuint32_t>(box_outer),
+                       swap ? static_cast<cuuint32_t>(box_outer) : 1u, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(ptr), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE,
                   mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -278,10 +347,13 @@ int sm_count() {
 
 template <int BN, bool A_MN, bool B_MN>
 cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
-                   const GemmEpilogue& epi) {
+                   const GemmEpilogue& epi, const GemmBatch& bat) {
   CUtensorMap ma, mb;
-  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true) : make_map(&ma, A, K, M, lda, BK, BM, false);
-  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true) : make_map(&mb, B, K, N, ldb, BK, BN, false);
+  GemmBatch b = bat;
+  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true, b.nb2, b.a_s2, b.nb1, b.a_s1, &b.a_perm)
+                         : make_map(&ma, A, K, M, lda, BK, BM, false, b.nb2, b.a_s2, b.nb1, b.a_s1, &b.a_perm);
+  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true, b.nb2, b.b_s2, b.nb1, b.b_s1, &b.b_perm)
+                         : make_map(&mb, B, K, N, ldb, BK, BN, false, b.nb2, b.b_s2, b.nb1, b.b_s1, &b.b_perm);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
   auto kern = gemm_tf32_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;  // per instantiation
@@ -290,25 +362,26 @@ cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, lon
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
-  const int grid = tiles < sm_count() ? tiles : sm_count();
+  const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
+  const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
   count_launch();
-  kern<<<grid, kThreads, Smem<BN>::kTotal, stream>>>(ma, mb, M, N, K, epi);
+  kern<<<grid, kThreads, Smem<BN>::kTotal, stream>>>(ma, mb, M, N, K, epi, b);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
-                      const float* B, long ldb, bool b_mn, const GemmEpilogue& epi) {
+                      const float* B, long ldb, bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch) {
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
   if ((lda & 3) || (ldb & 3) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
     return cudaErrorInvalidValue;
   }
-  if (!a_mn && !b_mn) return launch<128, false, false>(stream, M, N, K, A, lda, B, ldb, epi);
-  if (!a_mn && b_mn) return launch<128, false, true>(stream, M, N, K, A, lda, B, ldb, epi);
-  if (a_mn && !b_mn) return launch<128, true, false>(stream, M, N, K, A, lda, B, ldb, epi);
-  return launch<128, true, true>(stream, M, N, K, A, lda, B, ldb, epi);
+  const GemmBatch bat = batch ? *batch : GemmBatch{};
+  if (!a_mn && !b_mn) return launch<128, false, false>(stream, M, N, K, A, lda, B, ldb, epi, bat);
+  if (!a_mn && b_mn) return launch<128, false, true>(stream, M, N, K, A, lda, B, ldb, epi, bat);
+  if (a_mn && !b_mn) return launch<128, true, false>(stream, M, N, K, A, lda, B, ldb, epi, bat);
+  return launch<128, true, true>(stream, M, N, K, A, lda, B, ldb, epi, bat);
 }
 
 }  // namespace hy

@@ -12,6 +12,7 @@ enum EpiMode : int {
 };
 
 struct GemmEpilogue {
+  float alpha = 1.f;  // C = alpha * acc + ...
   float* C = nullptr;
   long ldc = 0;
   const float* bias = nullptr;  // [N]
@@ -25,11 +26,28 @@ struct GemmEpilogue {
   int mode = kEpiStore;
 };
 
+// Batched / causal extensions (used by tensor-core attention). A batch index z in
+// [0, nb1*nb2) splits as z1 = z / nb2, z2 = z % nb2; operand X of batch z starts at
+// X + z1*x_s1 + z2*x_s2 (elements). Causal modes assume square [T x T] score tiles:
+//   kCausalSkipUpper : output tiles strictly above the diagonal are not computed
+//   kCausalKLower    : K range limited to [0, m0 + BM)   (O = P V, dQ = dS K)
+//   kCausalKUpper    : K range limited to [m0, K)        (dK = dS^T Q, dV = P^T dO)
+enum CausalMode : int { kCausalNone = 0, kCausalSkipUpper = 1, kCausalKLower = 2, kCausalKUpper = 3 };
+
+struct GemmBatch {
+  int nb1 = 1, nb2 = 1;
+  long a_s1 = 0, a_s2 = 0, b_s1 = 0, b_s2 = 0, c_s1 = 0, c_s2 = 0;
+  int causal = kCausalNone;
+  // set by the launcher: TMA dimension order {inner, b2, outer, b1} when b2's stride is
+  // smaller than the row stride (e.g. heads interleaved inside a row)
+  int a_perm = 0, b_perm = 0;
+};
+
 // C[M,N] = op(A)[M,K] * op(B)[N,K]^T.
 //  a_mn == false: A stored row-major [M][lda] (K contiguous).   true: stored [K][lda] (M contiguous).
 //  b_mn == false: B stored row-major [N][ldb] (K contiguous).   true: stored [K][ldb] (N contiguous).
 // All leading dims in elements, multiples of 4 (16-byte TMA strides); pointers 16-byte aligned.
 cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
-                      const float* B, long ldb, bool b_mn, const GemmEpilogue& epi);
+                      const float* B, long ldb, bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch = nullptr);
 
 }  // namespace hy

@@ -35,11 +35,12 @@ struct AdamHyper {
 };
 cudaError_t adam_update(cudaStream_t s, long n, float* p, const float* g, float* m, float* v, const AdamHyper& h);
 
-// Causal flash attention, head dim 64. qkv: [B*T, 3*H*64] (q | k | v, head-major within each).
-// out: [B*T, H*64]; lse: [B*H*T].
-cudaError_t attention_fwd(cudaStream_t s, int B, int T, int H, const float* qkv, float* out, float* lse);
-// dqkv: [B*T, 3*H*64] (overwritten). ws: >= B*H*T floats (row dot(dout, out)).
-cudaError_t attention_bwd(cudaStream_t s, int B, int T, int H, const float* qkv, const float* out, const float* dout,
-                          const float* lse, float* dqkv, float* ws);
+// Tensor-core attention (attention_tc.cu). `work` holds score matrices: forward needs
+// T*T floats per (batch, head) processed at once, backward 2*T*T; chunks are sized to fit.
+cudaError_t attention_fwd_tc(cudaStream_t s, int B, int T, int H, const float* qkv, float* out, float* work,
+                             long work_floats);
+// dqkv overwritten ([B*T, 3*H*64]).
+cudaError_t attention_bwd_tc(cudaStream_t s, int B, int T, int H, const float* qkv, const float* dout, float* dqkv,
+                             float* work, long work_floats);
 
 }  // namespace hy

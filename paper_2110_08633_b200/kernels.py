@@ -70,17 +70,19 @@ def layernorm_bwd(x, g, mean, rstd, dy, dx=None, accumulate=False):
     return dx, dg, db
 
 
-def attention_fwd(qkv, B, T, H):
+def attention_fwd(qkv, B, T, H, work_floats=None):
     out = torch.empty(B * T, H * 64, device=qkv.device)
-    lse = torch.empty(B * H * T, device=qkv.device)
-    check(lib().hy_attention_fwd(_s(), B, T, H, 64, _p(qkv), _p(out), _p(lse)))
-    return out, lse
+    wf = work_floats or B * H * T * T
+    work = torch.empty(wf, device=qkv.device)
+    check(lib().hy_attention_fwd(_s(), B, T, H, 64, _p(qkv), _p(out), _p(work), wf))
+    return out
 
 
-def attention_bwd(qkv, out, dout, lse, B, T, H):
+def attention_bwd(qkv, dout, B, T, H, work_floats=None):
     dqkv = torch.empty_like(qkv)
-    ws = torch.empty(B * H * T, device=qkv.device)
-    check(lib().hy_attention_bwd(_s(), B, T, H, 64, _p(qkv), _p(out), _p(dout), _p(lse), _p(dqkv), _p(ws)))
+    wf = work_floats or 2 * B * H * T * T
+    work = torch.empty(wf, device=qkv.device)
+    check(lib().hy_attention_bwd(_s(), B, T, H, 64, _p(qkv), _p(dout), _p(dqkv), _p(work), wf))
     return dqkv
 
 

@@ -118,18 +118,20 @@ def ref_attention(qkv, B, T, H):
     return (att @ v).permute(0, 2, 1, 3).reshape(B * T, D)
 
 
-@pytest.mark.parametrize("B,T,H", [(2, 32, 1), (2, 100, 3), (1, 512, 2), (4, 128, 12)])
-def test_attention(B, T, H):
-    torch.manual_seed(T)
+@pytest.mark.parametrize("B,T,H,chunk", [(2, 32, 1, None), (2, 100, 3, None), (1, 512, 2, None),
+                                         (4, 128, 12, None), (8, 512, 12, 2), (2, 384, 4, 3), (3, 200, 5, 7)])
+def test_attention(B, T, H, chunk):
+    torch.manual_seed(T + H)
     qkv = torch.randn(B * T, 3 * H * 64, device=dev)
-    out, lse = K.attention_fwd(qkv, B, T, H)
+    wf = None if chunk is None else chunk * T * T  # forces (batch, head) chunking
+    out = K.attention_fwd(qkv, B, T, H, work_floats=wf)
     qr = qkv.clone().requires_grad_(True)
     ref = ref_attention(qr, B, T, H)
-    assert rel(out, ref) < 1e-4
+    assert rel(out, ref) < 3e-3
     dout = torch.randn_like(out)
     ref.backward(dout)
-    dqkv = K.attention_bwd(qkv, out, dout, lse, B, T, H)
-    assert rel(dqkv, qr.grad) < 1e-4
+    dqkv = K.attention_bwd(qkv, dout, B, T, H, work_floats=None if chunk is None else 2 * chunk * T * T)
+    assert rel(dqkv, qr.grad) < 3e-3
 
 
 def test_embedding():
