@@ -80,6 +80,11 @@ long hy_kernel_launches(void);
  * GPU parity tests; each maps to one hand-written sm_100a kernel (csrc/kernels/).
  * --------------------------------------------------------------------------------- */
 
+/* GEMM configuration of the calling host thread: precision_fp32 = 1 selects the 3xTF32
+ * split ("fp32", ~fp32 accuracy), 0 plain TF32; splitk_ws (device, may be NULL) lets
+ * low-occupancy GEMMs split K. */
+int hy_gemm_config(int precision_fp32, float* splitk_ws, long splitk_floats);
+
 /* C[M,N] = beta*C + op(A) op(B)^T (+bias[N]) (+R[M,N]) with tcgen05 kind::tf32.
  * a_mn=0: A is [M][lda] (K contiguous); a_mn=1: A is [K][lda] (M contiguous). Same for B
  * with N. mode 0 store, 1 GELU (Hout = pre-activation), 2 GELU-backward (C = acc*gelu'(Hin)). */

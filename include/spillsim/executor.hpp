@@ -32,6 +32,7 @@ struct ExecOptions {
   int warmup_passes = 0;           // replays before the timed ones (not in the trace)
   long opt_chunk_floats = 4L << 20;  // Adam m/v streaming chunk
   std::string params_out_dir;      // if set: final params of every executed job as job<j>.f32
+  bool precision_fp32 = false;     // GEMMs as 3xTF32 (~fp32) instead of TF32
   double hbm_slack_bytes = 0;      // physical arena may exceed mem_bytes by this much (toy configs
                                    // whose cost model leaves no room for real activations)
 };
@@ -46,6 +47,7 @@ struct ExecStats {
   std::vector<double> device_busy_s;
   std::vector<double> pinned_bytes;
   int kernel_launches = 0;
+  int elided_compute_tasks = 0;  // head-shard forwards folded into their backward
   double setup_s = 0;
 };
 

@@ -128,6 +128,12 @@ void hy_executor_destroy(void* handle) {
 
 long hy_kernel_launches(void) { return hy::g_kernel_launches.load(); }
 
+int hy_gemm_config(int precision_fp32, float* splitk_ws, long splitk_floats) {
+  hy::gemm_set_precision_fp32(precision_fp32 != 0);
+  hy::gemm_set_splitk_workspace(splitk_ws, splitk_floats);
+  return HY_OK;
+}
+
 int hy_gemm(void* stream, int M, int N, int K, const float* A, long lda, int a_mn, const float* B, long ldb, int b_mn,
             float* C, long ldc, const float* bias, const float* R, long ldr, float beta, int mode, float* Hout,
             const float* Hin, long ldh) {

@@ -86,6 +86,9 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   ex.warmup_passes = req.value("warmup_passes", 0);
   ex.params_out_dir = req.value("params_out_dir", std::string());
   ex.hbm_slack_bytes = req.value("hbm_slack_bytes", 0.0);
+  const std::string prec = req.value("precision", std::string("tf32"));
+  if (prec != "tf32" && prec != "fp32") throw InvalidArgument("precision must be 'tf32' or 'fp32'");
+  ex.precision_fp32 = prec == "fp32";
   if (req.contains("device_ids")) ex.device_ids = req["device_ids"].get<std::vector<int>>();
   if (req.contains("run_devices")) ex.run_devices = req["run_devices"].get<std::vector<int>>();
   if (req.contains("opt_chunk_floats")) ex.opt_chunk_floats = req["opt_chunk_floats"].get<long>();

@@ -31,6 +31,7 @@
 #include <mutex>
 #include <thread>
 
+#include "../kernels/gemm.cuh"
 #include "../kernels/ops.cuh"
 #include "gpt_runner.hpp"
 #include "spillsim/errors.hpp"
@@ -168,6 +169,8 @@ struct Worker {
   int last_tok = 1;
   bool stg_alias = false;
   long stg_chunk = 0;
+  float* splitk = nullptr;
+  long splitk_floats = 0;
   std::vector<TaskTiming> timing;  // per local task index
   cudaEvent_t t0 = nullptr, t_end = nullptr;
   cudaEvent_t join[3] = {nullptr, nullptr, nullptr};
@@ -332,7 +335,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
     for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
     scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, max_blocks));
   }
-  const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(grad_f) + 5 * hy_pad32(act_f) +
+  const long splitk_f = 4L << 20;  // 16 MB split-K partials
+  const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(grad_f) + 5 * hy_pad32(act_f) + splitk_f +
                            2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
                            hy_pad32(2 * static_cast<long>(w.tasks.size()) + 2);
   const DeviceSpec& dev = cluster.devices[static_cast<size_t>(w.plan_dev)];
@@ -371,6 +375,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
     for (int i = 0; i < kStaging; ++i) w.stg[i] = take(2 * chunk);
   }
   w.scratch = take(scratch_f);
+  w.splitk = take(splitk_f);
+  w.splitk_floats = splitk_f;
   if (w.stg_alias) {
     // staging inside the scratch fc/act block of the largest job on this GPU
     long best = 0;
@@ -696,12 +702,23 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   }
   // targets live in the second half of the token buffer ([tokens | targets], 2*M ints)
   io.targets = need_tokens ? w.tok[tok_i] + hj.M : nullptr;
-  if (fwd) {
+  // F of the head shard has no boundary output: when its B follows on this GPU (always
+  // with double buffering) the B task's forward recompute is the forward, and reports the
+  // loss. The plan and the transfers are unchanged; only the duplicate compute is elided.
+  bool skip_fwd = false;
+  if (fwd && g.has_head && local + 1 < static_cast<int>(w.tasks.size())) {
+    const ShardTask& nx = tasks[static_cast<size_t>(w.tasks[static_cast<size_t>(local) + 1])].t;
+    skip_fwd = nx.job == j && nx.minibatch == task.t.minibatch && nx.shard == s &&
+               nx.direction == Direction::kBackward;
+  }
+  if (fwd && !skip_fwd) {
     hy::run_forward(w.comp, hj.m, g, w.slot[slot], io, sc);
     if (g.has_head) {
       check_cuda(cudaMemcpyAsync(w.loss_dev + local, sc.loss, sizeof(double), cudaMemcpyDeviceToDevice, w.comp),
                  "loss copy");
     }
+  } else if (fwd) {
+    w.st.elided_compute_tasks += 1;
   } else {
     // The previous shard's Adam (opt stream) may still read the grad buffer: wait for it
     // only after this shard's forward recompute, then zero it.
@@ -718,6 +735,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       check_cuda(cudaMemcpyAsync(w.zbuf, sc.z, act_bytes, cudaMemcpyDeviceToDevice, w.comp), "z save");
       w.z_tr.after_write(w.comp);
       w.z_tag = Tag{j, gmb, 0, 2};
+    }
+    if (g.has_head) {  // the backward's recompute produced this minibatch's loss
+      check_cuda(cudaMemcpyAsync(w.loss_dev + local, sc.loss, sizeof(double), cudaMemcpyDeviceToDevice, w.comp),
+                 "loss copy");
     }
     w.gbuf_tr.after_write(w.comp);
   }
@@ -792,6 +813,8 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
       Worker& w = *workers[i];
       try {
         check_cuda(cudaSetDevice(w.cuda_dev), "set device");
+        hy::gemm_set_splitk_workspace(w.splitk, w.splitk_floats);
+        hy::gemm_set_precision_fp32(exec.precision_fp32);
         check_cuda(cudaDeviceSynchronize(), "pre-pass sync");
         check_cuda(cudaEventRecord(w.t0, w.comp), "t0");
         for (cudaStream_t s : {w.down, w.up, w.opt}) check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");
@@ -877,7 +900,7 @@ void ExecutorImpl::collect(int pass, ExecResult& res) {
         tr.events.push_back(SimEvent{up_res[static_cast<size_t>(w.plan_dev)], k, t, d0, d1});
       }
       tr.makespan_s = std::max(tr.makespan_s, std::max(c1, d1));
-      if (task.t.direction == Direction::kForward && g.has_head) {
+      if (task.t.direction == Direction::kBackward && g.has_head) {
         const int gmb = pass * job_mb[static_cast<size_t>(task.t.job)] + task.t.minibatch;
         auto& L = res.losses[static_cast<size_t>(task.t.job)];
         if (static_cast<int>(L.size()) <= gmb) L.resize(static_cast<size_t>(gmb) + 1, 0.0);

@@ -12,6 +12,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -26,14 +27,24 @@ constexpr int BK = 32;  // one 128-byte swizzle atom of fp32
 constexpr int kStages = 4;
 constexpr int kThreads = 256;
 
-template <int BN>
+// P3 (3xTF32, "fp32" precision): every stage also holds the low parts A_lo, B_lo
+// (x = hi + lo, hi = tf32_rna(x)); D += A_lo B_hi + A_hi B_lo + A_hi B_hi.
+template <int BN, bool P3 = false>
 struct Smem {
+  static constexpr int kStagesN = P3 ? 3 : kStages;
   static constexpr int kABytes = BM * BK * 4;
   static constexpr int kBBytes = BN * BK * 4;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kRing = kStages * kStageBytes;
+  static constexpr int kOpBytes = kABytes + kBBytes;
+  static constexpr int kStageBytes = P3 ? 2 * kOpBytes : kOpBytes;
+  static constexpr int kRing = kStagesN * kStageBytes;
   static constexpr int kTotal = kRing + 1024 /*align slack*/ + 256 /*barriers*/;
 };
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
 
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
@@ -54,7 +65,7 @@ struct TileInfo {
 
 template <int BN>
 __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n, int M, int N, int K, int nb2,
-                                              int causal) {
+                                              int causal, int nb1 = 1) {
   TileInfo t;
   const int per_batch = tiles_m * tiles_n;
   const int z = tile / per_batch;
@@ -75,24 +86,31 @@ __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n
   } else if (causal == kCausalKUpper) {
     t.kb0 = t.m0 / BK;
     t.nkb = max(0, kb_all - t.kb0);
+  } else if (causal == kSplitK) {
+    // z1 indexes the K slice; the operands themselves are not batched (TMA z = 0)
+    const int per = (kb_all + nb1 - 1) / nb1;
+    t.kb0 = t.z1 * per;
+    t.nkb = max(0, min(per, kb_all - t.kb0));
   }
   (void)M;
   (void)N;
   return t;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool P3>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                  int N, int K, GemmEpilogue epi, GemmBatch bat) {
-  using L = Smem<BN>;
+  using L = Smem<BN, P3>;
+  constexpr int kStages = L::kStagesN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kRing);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* conv = tempty + 2;  // P3: hi/lo split of the stage done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + kStages);
 
   const uint32_t warp = warp_id();
   const int tiles_m = (M + BM - 1) / BM;
@@ -105,6 +123,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 64);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -123,13 +142,14 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal);
+        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
         if (ti.skip) continue;
+        if (bat.causal == kSplitK) ti.z1 = ti.z2 = 0;  // K slices read the same operands
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
-          mbar_expect_tx(&full[stage], L::kStageBytes);
+          mbar_expect_tx(&full[stage], L::kOpBytes);
           const int k0 = kb * BK;
           if constexpr (A_MN) {
 #pragma unroll
@@ -164,7 +184,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     uint32_t phase = 0;
     int local = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal);
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -178,13 +198,32 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         continue;
       }
       for (int kb = 0; kb < ti.nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
+        if constexpr (P3) {
+          mbar_wait(&conv[stage], phase);
+        } else {
+          mbar_wait(&full[stage], phase);
+        }
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
           const uint32_t sb = sa + L::kABytes;
 #pragma unroll
           for (int kk = 0; kk < BK / 8; ++kk) {
+            if constexpr (P3) {
+              const uint32_t la = sa + L::kOpBytes, lb = sb + L::kOpBytes;
+              const uint64_t dah = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
+                                        : smem_desc_sw128(sa + kk * 32, 16, 1024);
+              const uint64_t dbh = B_MN ? smem_desc_sw128_b32(sb + kk * 1024, BK * 128, 512)
+                                        : smem_desc_sw128(sb + kk * 32, 16, 1024);
+              const uint64_t dal = A_MN ? smem_desc_sw128_b32(la + kk * 1024, BK * 128, 512)
+                                        : smem_desc_sw128(la + kk * 32, 16, 1024);
+              const uint64_t dbl = B_MN ? smem_desc_sw128_b32(lb + kk * 1024, BK * 128, 512)
+                                        : smem_desc_sw128(lb + kk * 32, 16, 1024);
+              mma_tf32(d_tmem, dal, dbh, idesc, (kb | kk) != 0 ? 1u : 0u);
+              mma_tf32(d_tmem, dah, dbl, idesc, 1u);
+              mma_tf32(d_tmem, dah, dbh, idesc, 1u);
+              continue;
+            }
             // K-major: advance 8 fp32 = 32 B inside the swizzled row; SBO = 8 rows * 128 B.
             // MN-major: advance 8 k-rows = 1024 B; LBO = one 32-element MN column (BK rows * 128 B),
             // SBO = 4 k-rows (512 B) of the 32-byte-atom swizzle.
@@ -204,11 +243,45 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
         }
       }
     }
+  } else if (P3 && (warp == 2 || warp == 3)) {
+    // Split each landed stage into tf32 hi (in place) + lo (second half of the stage).
+    const int tid = static_cast<int>(threadIdx.x) - 64;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+      if (ti.skip) continue;
+      for (int kb = 0; kb < ti.nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        float4* hi = reinterpret_cast<float4*>(smem + stage * L::kStageBytes);
+        float4* lo = reinterpret_cast<float4*>(smem + stage * L::kStageBytes + L::kOpBytes);
+        for (int i = tid; i < L::kOpBytes / 16; i += 64) {
+          float4 x = hi[i];
+          float4 h, l;
+          h.x = __uint_as_float(tf32_rna(x.x));
+          h.y = __uint_as_float(tf32_rna(x.y));
+          h.z = __uint_as_float(tf32_rna(x.z));
+          h.w = __uint_as_float(tf32_rna(x.w));
+          l.x = x.x - h.x;
+          l.y = x.y - h.y;
+          l.z = x.z - h.z;
+          l.w = x.w - h.w;
+          hi[i] = h;
+          lo[i] = l;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&conv[stage]);
+        if (++stage == kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
   } else if (warp >= 4) {
     const uint32_t q = warp - 4;  // TMEM lane quarter this warp may access
     int local = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal);
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
@@ -335,6 +408,24 @@ bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long l
   return r == CUDA_SUCCESS;
 }
 
+thread_local float* t_splitk_ws = nullptr;
+thread_local bool t_prec3 = false;
+thread_local long t_splitk_floats = 0;
+
+// C = alpha * sum_s part[s] + beta * C   (fixed summation order: deterministic)
+__global__ void splitk_reduce_kernel(int M, int N, int S, const float* __restrict__ part, float* __restrict__ C,
+                                     long ldc, float alpha, float beta) {
+  const long total = static_cast<long>(M) * N;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < S; ++s) acc += part[s * total + i];
+    const long m = i / N, n = i % N;
+    float* c = C + m * ldc + n;
+    *c = alpha * acc + (beta != 0.f ? beta * *c : 0.f);
+  }
+}
+
 int sm_count() {
   static int n = 0;
   if (n == 0) {
@@ -345,31 +436,48 @@ int sm_count() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool P3>
 cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
                    const GemmEpilogue& epi, const GemmBatch& bat) {
   CUtensorMap ma, mb;
   GemmBatch b = bat;
-  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true, b.nb2, b.a_s2, b.nb1, b.a_s1, &b.a_perm)
-                         : make_map(&ma, A, K, M, lda, BK, BM, false, b.nb2, b.a_s2, b.nb1, b.a_s1, &b.a_perm);
-  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true, b.nb2, b.b_s2, b.nb1, b.b_s1, &b.b_perm)
-                         : make_map(&mb, B, K, N, ldb, BK, BN, false, b.nb2, b.b_s2, b.nb1, b.b_s1, &b.b_perm);
+  const long mb1 = b.causal == kSplitK ? 1 : b.nb1;  // K slices share the (unbatched) operands
+  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm)
+                         : make_map(&ma, A, K, M, lda, BK, BM, false, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm);
+  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm)
+                         : make_map(&mb, B, K, N, ldb, BK, BN, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, P3>;
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::kTotal);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN, P3>::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
   count_launch();
-  kern<<<grid, kThreads, Smem<BN>::kTotal, stream>>>(ma, mb, M, N, K, epi, b);
+  kern<<<grid, kThreads, Smem<BN, P3>::kTotal, stream>>>(ma, mb, M, N, K, epi, b);
   return cudaGetLastError();
 }
 
+cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+                     long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
+  if (t_prec3) {
+    if (!a_mn && !b_mn) return launch<128, false, false, true>(st, M, N, K, A, lda, B, ldb, e, bat);
+    if (!a_mn && b_mn) return launch<128, false, true, true>(st, M, N, K, A, lda, B, ldb, e, bat);
+    if (a_mn && !b_mn) return launch<128, true, false, true>(st, M, N, K, A, lda, B, ldb, e, bat);
+    return launch<128, true, true, true>(st, M, N, K, A, lda, B, ldb, e, bat);
+  }
+  if (!a_mn && !b_mn) return launch<128, false, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (!a_mn && b_mn) return launch<128, false, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (a_mn && !b_mn) return launch<128, true, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+  return launch<128, true, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+}
+
 }  // namespace
+
+void gemm_set_precision_fp32(bool three_pass) { t_prec3 = three_pass; }
 
 cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
                       const float* B, long ldb, bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch) {
@@ -377,11 +485,39 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   if ((lda & 3) || (ldb & 3) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
     return cudaErrorInvalidValue;
   }
-  const GemmBatch bat = batch ? *batch : GemmBatch{};
-  if (!a_mn && !b_mn) return launch<128, false, false>(stream, M, N, K, A, lda, B, ldb, epi, bat);
-  if (!a_mn && b_mn) return launch<128, false, true>(stream, M, N, K, A, lda, B, ldb, epi, bat);
-  if (a_mn && !b_mn) return launch<128, true, false>(stream, M, N, K, A, lda, B, ldb, epi, bat);
-  return launch<128, true, true>(stream, M, N, K, A, lda, B, ldb, epi, bat);
+  GemmBatch bat = batch ? *batch : GemmBatch{};
+  GemmEpilogue e = epi;
+  // Split K when the output has too few tiles to fill the GPU (e.g. the LM-head dz GEMM:
+  // 24 tiles, K = 50257; dW of the attention projection: 36 tiles, K = B*T).
+  int split = 1;
+  const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + 127) / 128);
+  const int kb_all = (K + BK - 1) / BK;
+  const bool plain = !batch && e.mode == kEpiStore && !e.bias && !e.R;
+  if (plain && t_splitk_ws && tiles * 2 <= sm_count() && kb_all >= 32) {
+    split = static_cast<int>(std::min<long>(sm_count() / tiles, kb_all / 16));
+    split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
+  }
+  if (split >= 2) {
+    bat.nb1 = split;
+    bat.causal = kSplitK;
+    bat.c_s1 = static_cast<long>(M) * N;
+    GemmEpilogue pe;
+    pe.C = t_splitk_ws;
+    pe.ldc = N;
+    const cudaError_t r = dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, pe, bat);
+    if (r != cudaSuccess) return r;
+    const long total = static_cast<long>(M) * N;
+    const int grid = static_cast<int>(std::min<long>((total + 255) / 256, sm_count() * 8L));
+    count_launch();
+    splitk_reduce_kernel<<<grid, 256, 0, stream>>>(M, N, split, t_splitk_ws, e.C, e.ldc, e.alpha, e.beta);
+    return cudaGetLastError();
+  }
+  return dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+}
+
+void gemm_set_splitk_workspace(float* ws, long floats) {
+  t_splitk_ws = ws;
+  t_splitk_floats = floats;
 }
 
 }  // namespace hy

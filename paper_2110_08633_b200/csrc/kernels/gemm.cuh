@@ -32,7 +32,7 @@ struct GemmEpilogue {
 //   kCausalSkipUpper : output tiles strictly above the diagonal are not computed
 //   kCausalKLower    : K range limited to [0, m0 + BM)   (O = P V, dQ = dS K)
 //   kCausalKUpper    : K range limited to [m0, K)        (dK = dS^T Q, dV = P^T dO)
-enum CausalMode : int { kCausalNone = 0, kCausalSkipUpper = 1, kCausalKLower = 2, kCausalKUpper = 3 };
+enum CausalMode : int { kCausalNone = 0, kCausalSkipUpper = 1, kCausalKLower = 2, kCausalKUpper = 3, kSplitK = 4 };
 
 struct GemmBatch {
   int nb1 = 1, nb2 = 1;
@@ -49,5 +49,12 @@ struct GemmBatch {
 // All leading dims in elements, multiples of 4 (16-byte TMA strides); pointers 16-byte aligned.
 cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
                       const float* B, long ldb, bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch = nullptr);
+
+// Split-K scratch for low-occupancy GEMMs (few output tiles, long K). Per host thread
+// (each executor worker drives one GPU); without one, GEMMs never split.
+void gemm_set_splitk_workspace(float* ws, long floats);
+// Per host thread: true = "fp32" precision (3xTF32 split on the tensor cores, ~fp32
+// accuracy at 3x the MMA work), false = plain TF32 (default).
+void gemm_set_precision_fp32(bool three_pass);
 
 }  // namespace hy

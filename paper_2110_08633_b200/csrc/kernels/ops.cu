@@ -162,13 +162,24 @@ __global__ void ln_bwd_kernel(int rows, int d, const float* __restrict__ x, cons
 }
 
 // out[n] (+)= sum_b part[b][n], fixed order => deterministic.
+// Block (32 columns x 8 part-lanes): lane y sums parts y, y+8, ... then lane 0 adds the 8
+// partials in fixed order => deterministic, and 8x the memory parallelism of one thread/column.
 __global__ void reduce_parts_kernel(int parts, int N, const float* __restrict__ part, float* __restrict__ out,
                                     int accumulate) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= N) return;
+  __shared__ float acc[8][33];
+  const int n = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
-  for (int b = 0; b < parts; ++b) s += part[static_cast<long>(b) * N + n];
-  out[n] = accumulate ? out[n] + s : s;
+  if (n < N) {
+    for (int b = threadIdx.y; b < parts; b += 8) s += part[static_cast<long>(b) * N + n];
+  }
+  acc[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && n < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += acc[y][threadIdx.x];
+    out[n] = accumulate ? out[n] + t : t;
+  }
 }
 
 // Partial column sums over a row range per block; 256 threads stride the columns.
@@ -364,9 +375,9 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
     ln_bwd_kernel<32><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
   }
   count_launch();
-  reduce_parts_kernel<<<(d + 255) / 256, 256, 0, s>>>(nb, d, ws_dg, dg, 1);
+  reduce_parts_kernel<<<(d + 31) / 32, dim3(32, 8), 0, s>>>(nb, d, ws_dg, dg, 1);
   count_launch();
-  reduce_parts_kernel<<<(d + 255) / 256, 256, 0, s>>>(nb, d, ws_db, db, 1);
+  reduce_parts_kernel<<<(d + 31) / 32, dim3(32, 8), 0, s>>>(nb, d, ws_db, db, 1);
   return cudaGetLastError();
 }
 
@@ -377,7 +388,7 @@ cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float
   count_launch();
   colsum_part_kernel<<<grid, 256, 0, s>>>(M, N, X, ldx, ws, rpb);
   count_launch();
-  reduce_parts_kernel<<<(N + 255) / 256, 256, 0, s>>>(nb, N, ws, out, accumulate ? 1 : 0);
+  reduce_parts_kernel<<<(N + 31) / 32, dim3(32, 8), 0, s>>>(nb, N, ws, out, accumulate ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -21,6 +21,11 @@ def _p(t):
     return None if t is None else t.data_ptr()
 
 
+def gemm_config(precision_fp32=False, splitk_ws=None):
+    """Per-thread GEMM settings: 3xTF32 ("fp32") precision and the split-K workspace."""
+    check(lib().hy_gemm_config(int(precision_fp32), _p(splitk_ws), 0 if splitk_ws is None else splitk_ws.numel()))
+
+
 def gemm(A, B, *, a_mn=False, b_mn=False, M=None, N=None, K=None, C=None, bias=None, R=None, beta=0.0,
          mode=0, H=None, lda=None, ldb=None, ldc=None):
     """C = op(A) op(B)^T. a_mn=False: A is [M,K]; True: A is [K,M]. Likewise B with N."""

@@ -36,14 +36,14 @@ def tiny_config(mem=50e6, n_blocks=2, d=64, T=32, B=2, mbs=2, jobs=2):
     return cfg
 
 
-def compare(cfg, tmp_path, strategy="sharp", **kw):
+def compare(cfg, tmp_path, strategy="sharp", loss_tol=1e-3, param_tol=1e-3, **kw):
     res = P.execute(cfg, strategy=strategy, params_out_dir=str(tmp_path), **kw)
     starts = res["shard_starts"] or [[0]] * len(cfg["jobs"])
     losses, params = O.run_workload_cpu(cfg, starts)
     for j in losses:
         gl = np.array(res["losses"][j][: len(losses[j])])
         cl = np.array(losses[j])
-        assert np.all(np.abs(gl - cl) / cl < 1e-3), (j, gl, cl)
+        assert np.all(np.abs(gl - cl) / cl < loss_tol), (j, gl, cl)
         pg = np.fromfile(os.path.join(tmp_path, f"job{j}.f32"), dtype=np.float32)
         pc = params[j]
         assert pg.shape == pc.shape
@@ -52,25 +52,31 @@ def compare(cfg, tmp_path, strategy="sharp", **kw):
         for l in range(m.L + 2):
             a, b = O.layer_offset(m, l), O.layer_offset(m, l + 1)
             rel = np.linalg.norm(pg[a:b] - pc[a:b]) / np.linalg.norm(pc[a:b])
-            assert rel < 1e-3, (j, l, rel)
+            assert rel < param_tol, (j, l, rel)
     return res
 
 
-def test_c1_sharp_two_shards(tmp_path):
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+def test_c1_sharp_two_shards(tmp_path, precision):
     # C1's 40e6 virtual device leaves ~0.1 MB beyond params+grads+prefetch for real
     # activations/logits; 50e6 keeps the same cut [0,3] with room for them.
     cfg = tiny_config()
-    res = compare(cfg, tmp_path)
+    tol = dict(loss_tol=1e-5, param_tol=1e-4) if precision == "fp32" else {}
+    res = compare(cfg, tmp_path, precision=precision, **tol)
     assert res["shard_starts"] == [[0, 3], [0, 3]]
     assert res["stats"]["arena_bytes"][0] <= 50e6
 
 
 @pytest.mark.parametrize("mem,starts", [(51e6, [0, 18]), (54e6, [0, 25])])
-def test_head_shard_without_embedding(tmp_path, mem, starts):
+@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+def test_head_shard_without_embedding(tmp_path, mem, starts, precision):
     # 24 blocks: [0,18] puts blocks + head (tied wte copy) in shard 1; [0,25] a head-only
     # shard. Exercises the tied-wte load, deferred dwte (saved ln_f output z) and grads.
+    # lr 1e-3 for 3 steps: Adam turns TF32 noise in near-zero gradients (most of wte) into
+    # +-lr sign flips, so the TF32 parameter bound is 2e-3; fp32 (3xTF32) holds 1e-4.
     cfg = tiny_config(mem=mem, n_blocks=24, d=64, T=32, B=2, mbs=3, jobs=1)
-    res = compare(cfg, tmp_path, hbm_slack_bytes=8e6)
+    tol = dict(loss_tol=1e-5, param_tol=1e-4) if precision == "fp32" else dict(param_tol=2e-3)
+    res = compare(cfg, tmp_path, hbm_slack_bytes=8e6, precision=precision, **tol)
     assert res["shard_starts"][0] == starts
     assert res["stats"]["arena_bytes"][0] <= mem + 8e6
 

@@ -44,6 +44,44 @@ def test_gemm_majors(shape, a_mn, b_mn):
     assert rel(C, ref) < 3e-3, (shape, a_mn, b_mn, rel(C, ref))
 
 
+@pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, True), (True, False)])
+def test_gemm_precision_fp32(a_mn, b_mn):
+    """3xTF32 split: ~fp32 accuracy (rel <= 2e-6 vs an fp64 product)."""
+    M, N, Kd = 384, 256, 1024
+    A = torch.randn(M, Kd, device=dev)
+    B = torch.randn(N, Kd, device=dev)
+    ref = (A.double() @ B.double().T)
+    try:
+        K.gemm_config(precision_fp32=True)
+        C = K.gemm(A.T.contiguous() if a_mn else A, B.T.contiguous() if b_mn else B, a_mn=a_mn, b_mn=b_mn,
+                   M=M, N=N, K=Kd)
+    finally:
+        K.gemm_config(precision_fp32=False)
+    assert rel(C.double(), ref) < 2e-6
+    C32 = K.gemm(A, B)
+    assert rel(C32.double(), ref) > 1e-5  # plain TF32 is measurably coarser
+
+
+@pytest.mark.parametrize("M,N,Kd,b_mn,a_mn", [(500, 768, 50257, True, False), (768, 768, 4096, True, True),
+                                              (96, 200, 8192, False, False)])
+def test_gemm_splitk(M, N, Kd, b_mn, a_mn):
+    """Low-occupancy GEMMs split K through the workspace; deterministic fixed-order reduce."""
+    A = torch.randn(M, Kd, device=dev) * 0.1
+    B = torch.randn(N, Kd, device=dev) * 0.1
+    C0 = torch.randn(M, N, device=dev)
+    ws = torch.empty(4 << 20, device=dev)
+    try:
+        K.gemm_config(splitk_ws=ws)
+        Ain = A.T.contiguous() if a_mn else A
+        Bin = B.T.contiguous() if b_mn else B
+        C = K.gemm(Ain, Bin, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=Kd, C=C0.clone(), beta=1.0)
+        C2 = K.gemm(Ain, Bin, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=Kd, C=C0.clone(), beta=1.0)
+    finally:
+        K.gemm_config()
+    assert rel(C, C0 + A @ B.T) < 3e-3
+    assert torch.equal(C, C2)
+
+
 def test_gemm_epilogues():
     M, N, Kd = 512, 640, 256
     A = torch.randn(M, Kd, device=dev)
