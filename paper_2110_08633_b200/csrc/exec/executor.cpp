@@ -335,20 +335,23 @@ void ExecutorImpl::setup_worker(Worker& w) {
     for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
     scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, max_blocks));
   }
-  const long splitk_f = 4L << 20;  // 16 MB split-K partials
-  const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(grad_f) + 5 * hy_pad32(act_f) + splitk_f +
+  const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(grad_f) + 5 * hy_pad32(act_f) +
                            2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
                            hy_pad32(2 * static_cast<long>(w.tasks.size()) + 2);
   const DeviceSpec& dev = cluster.devices[static_cast<size_t>(w.plan_dev)];
   // Adam m/v staging: a dedicated ring when the HBM cap leaves room, otherwise it aliases
   // the dead MLP activations of the scratch (then compute waits for the m/v write-back).
   const double cap = dev.mem_bytes + exec.hbm_slack_bytes;
-  const long budget_floats = static_cast<long>(cap / 4) - base_floats - 2048;
+  long budget_floats = static_cast<long>(cap / 4) - base_floats - 2048;
+  // split-K partials (<= 16 MB) from what the cap leaves, then the Adam staging ring
+  long splitk_f = std::min(4L << 20, std::max(0L, budget_floats / 4)) / 1024 * 1024;
+  if (splitk_f < (256L << 10)) splitk_f = 0;
+  budget_floats -= splitk_f;
   long chunk = std::min(exec.opt_chunk_floats, budget_floats / (2 * kStaging));
   chunk = chunk / 1024 * 1024;
   w.stg_alias = chunk < (1L << 20);
   if (w.stg_alias) chunk = 0;
-  const long floats = base_floats + kStaging * 2 * hy_pad32(chunk);
+  const long floats = base_floats + splitk_f + kStaging * 2 * hy_pad32(chunk);
   w.arena_bytes = floats * 4 + 4096;
   if (static_cast<double>(w.arena_bytes) > cap) {
     throw InfeasibleOOM("sharp-executor", "(all jobs on this device)", dev.device_id,
@@ -375,7 +378,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
     for (int i = 0; i < kStaging; ++i) w.stg[i] = take(2 * chunk);
   }
   w.scratch = take(scratch_f);
-  w.splitk = take(splitk_f);
+  w.splitk = splitk_f > 0 ? take(splitk_f) : nullptr;
   w.splitk_floats = splitk_f;
   if (w.stg_alias) {
     // staging inside the scratch fc/act block of the largest job on this GPU
@@ -542,7 +545,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   w.st.model_d2h_bytes += task.t.activation_out_bytes + task.t.grad_offload_bytes;
 
   // ---- ParamLoad (down) -----------------------------------------------------------
-  const Tag want{j, -1, s, hj.version[static_cast<size_t>(s)]};
+  // A head shard without the embedding carries a copy of the tied wte: its content also
+  // depends on shard 0's version (updated by B(0)'s Adam).
+  const int wte_ver = g.wte_offset >= 0 ? hj.version[0] : -1;
+  const Tag want{j, wte_ver, s, hj.version[static_cast<size_t>(s)]};
   int slot = -1;
   for (int i = 0; i < 2; ++i) {
     if (w.slot_tag[i] == want) slot = i;
@@ -794,7 +800,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     const int step = gmb + 1;
     adam_writeback(w, hj, s, slot, step, local);
     hj.version[static_cast<size_t>(s)] += 1;
-    w.slot_tag[slot] = Tag{j, -1, s, hj.version[static_cast<size_t>(s)]};
+    w.slot_tag[slot] = Tag{j, g.wte_offset >= 0 ? hj.version[0] : -1, s, hj.version[static_cast<size_t>(s)]};
   } else {
     check_cuda(cudaEventRecord(tm.d1, w.up), "d1");
   }
