@@ -23,7 +23,7 @@ HOST_OBJS := $(patsubst $(CSRC)/%.cpp,$(B)/%.o,$(HOST_SRCS) $(EXEC_SRCS) $(CAPI_
 CU_OBJS   := $(patsubst $(CSRC)/%.cu,$(B)/%.o,$(CU_SRCS))
 HDRS      := $(wildcard include/*.h include/spillsim/*.hpp $(CSRC)/kernels/*.cuh $(CSRC)/exec/*.hpp)
 
-all: $(PKG)/libhydra.so $(B)/plan_dump_b200 oracle/liboracle_gpt.so
+all: $(PKG)/libhydra.so $(B)/plan_dump_b200 $(B)/test_spillsim oracle/liboracle_gpt.so
 
 $(B)/%.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
@@ -37,6 +37,9 @@ $(PKG)/libhydra.so: $(HOST_OBJS) $(CU_OBJS)
 	$(CXX) -shared $^ -o $@ -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -pthread -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp
 
 $(B)/plan_dump_b200: oracle/plan_dump.cpp $(PKG)/libhydra.so
+	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lhydra -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+$(B)/test_spillsim: tests/native/test_spillsim.cpp $(PKG)/libhydra.so
 	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lhydra -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle/liboracle_gpt.so: oracle/gpt_oracle.c oracle/gpt_oracle.h
