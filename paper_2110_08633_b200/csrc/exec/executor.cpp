@@ -26,6 +26,7 @@
 #include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -147,8 +148,20 @@ struct Worker {
   float* slot[2] = {nullptr, nullptr};
   Tag slot_tag[2];
   Tracked slot_tr[2];
-  float* gbuf = nullptr;
-  Tracked gbuf_tr;
+  // Parameter gradients: the embedding's in its own buffer, every other layer in a ring
+  // (FIFO, released as each layer's Adam finishes reading), so the optimizer streams a
+  // layer's state while the backward is still working on earlier layers.
+  float* gembed = nullptr;
+  cudaEvent_t gembed_free = nullptr;  // Adam of the last embedding gradient done
+  float* ring = nullptr;
+  long ring_floats = 0, ring_head = 0;
+  struct RingEntry {
+    long off, len;
+    cudaEvent_t done;
+  };
+  std::deque<RingEntry> ring_live;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
   float* abuf[2] = {nullptr, nullptr};
   Tag abuf_tag[2];
   Tracked abuf_tr[2];
@@ -171,6 +184,8 @@ struct Worker {
   long stg_chunk = 0;
   float* splitk = nullptr;
   long splitk_floats = 0;
+  int stg_round = 0;
+  bool opt_pending = false;
   std::vector<TaskTiming> timing;  // per local task index
   cudaEvent_t t0 = nullptr, t_end = nullptr;
   cudaEvent_t join[3] = {nullptr, nullptr, nullptr};
@@ -207,7 +222,8 @@ struct ExecutorImpl {
   void setup_worker(Worker& w);
   void run_pass(int pass, bool timed, ExecResult& res);
   void enqueue_task(Worker& w, int t, int pass);
-  void adam_writeback(Worker& w, HostJob& hj, int s, int slot, int step, int local);
+  void adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer, const float* grads, int step,
+                  cudaEvent_t done);
   void collect(int pass, ExecResult& res);
 };
 
@@ -228,7 +244,8 @@ ExecutorImpl::~ExecutorImpl() {
       w.tok_tr[i].destroy();
     }
     for (int i = 0; i < kStaging; ++i) w.stg_tr[i].destroy();
-    w.gbuf_tr.destroy();
+    for (cudaEvent_t e : w.ev_pool) cudaEventDestroy(e);
+    if (w.gembed_free) cudaEventDestroy(w.gembed_free);
     w.z_tr.destroy();
     for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2]}) {
       if (e) cudaEventDestroy(e);
@@ -323,19 +340,20 @@ void ExecutorImpl::setup_worker(Worker& w) {
   check_cuda(cudaStreamCreateWithFlags(&w.up, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.opt, cudaStreamNonBlocking), "stream");
   // Size the arena from the tasks this GPU will run.
-  long slot_f = 0, grad_f = 0, act_f = 0, scratch_f = 0, tok_n = 0;
+  long slot_f = 0, embed_f = 0, layer_f = 0, act_f = 0, scratch_f = 0, tok_n = 0;
   for (int t : w.tasks) {
     const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
     const ShardGeom& g = hj.geom[static_cast<size_t>(tasks[static_cast<size_t>(t)].t.shard)];
     slot_f = std::max(slot_f, g.slot_floats);
-    grad_f = std::max(grad_f, g.param_floats);
+    if (g.has_embed) embed_f = std::max(embed_f, hy_layer_floats(&hj.m, 0));
+    for (int l = std::max(g.l0, 1); l < g.l1; ++l) layer_f = std::max(layer_f, hy_layer_floats(&hj.m, l));
     act_f = std::max(act_f, hj.n_act);
     tok_n = std::max(tok_n, hj.M);
     int max_blocks = 0;
     for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
     scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, max_blocks));
   }
-  const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(grad_f) + 5 * hy_pad32(act_f) +
+  const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(embed_f) + 5 * hy_pad32(act_f) +
                            2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
                            hy_pad32(2 * static_cast<long>(w.tasks.size()) + 2);
   const DeviceSpec& dev = cluster.devices[static_cast<size_t>(w.plan_dev)];
@@ -343,6 +361,9 @@ void ExecutorImpl::setup_worker(Worker& w) {
   // the dead MLP activations of the scratch (then compute waits for the m/v write-back).
   const double cap = dev.mem_bytes + exec.hbm_slack_bytes;
   long budget_floats = static_cast<long>(cap / 4) - base_floats - 2048;
+  // gradient ring: at least two of the largest non-embedding layers
+  long ring_f = 2 * hy_pad32(layer_f) + 64;
+  budget_floats -= ring_f;
   // split-K partials (<= 16 MB) from what the cap leaves, then the Adam staging ring
   long splitk_f = std::min(4L << 20, std::max(0L, budget_floats / 4)) / 1024 * 1024;
   if (splitk_f < (256L << 10)) splitk_f = 0;
@@ -351,7 +372,23 @@ void ExecutorImpl::setup_worker(Worker& w) {
   chunk = chunk / 1024 * 1024;
   w.stg_alias = chunk < (1L << 20);
   if (w.stg_alias) chunk = 0;
-  const long floats = base_floats + splitk_f + kStaging * 2 * hy_pad32(chunk);
+  budget_floats -= kStaging * 2 * hy_pad32(chunk);
+  if (w.stg_alias) {
+    // deferred optimizer: the ring must hold every non-embedding layer of a shard
+    long shard_f = 0;
+    for (int t : w.tasks) {
+      const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
+      const ShardGeom& g = hj.geom[static_cast<size_t>(tasks[static_cast<size_t>(t)].t.shard)];
+      long sum = 0;
+      for (int l = std::max(g.l0, 1); l < g.l1; ++l) sum += hy_pad32(hy_layer_floats(&hj.m, l));
+      shard_f = std::max(shard_f, sum + 64);
+    }
+    budget_floats -= std::max(0L, shard_f - ring_f);
+    ring_f = std::max(ring_f, shard_f);
+  }
+  // spare budget deepens the gradient ring (up to 4 layers)
+  if (budget_floats > 0) ring_f += std::min(budget_floats, 2 * hy_pad32(layer_f)) / 32 * 32;
+  const long floats = base_floats + ring_f + splitk_f + kStaging * 2 * hy_pad32(chunk);
   w.arena_bytes = floats * 4 + 4096;
   if (static_cast<double>(w.arena_bytes) > cap) {
     throw InfeasibleOOM("sharp-executor", "(all jobs on this device)", dev.device_id,
@@ -366,7 +403,9 @@ void ExecutorImpl::setup_worker(Worker& w) {
   };
   w.slot[0] = take(slot_f);
   w.slot[1] = take(slot_f);
-  w.gbuf = take(grad_f);
+  w.gembed = embed_f > 0 ? take(embed_f) : nullptr;
+  w.ring = take(ring_f);
+  w.ring_floats = ring_f;
   w.abuf[0] = take(act_f);
   w.abuf[1] = take(act_f);
   w.gbd[0] = take(act_f);
@@ -404,6 +443,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
   for (TaskTiming& tm : w.timing) {
     for (cudaEvent_t* e : {&tm.pl0, &tm.pl1, &tm.pr0, &tm.pr1, &tm.c0, &tm.c1, &tm.d0, &tm.d1}) *e = new_event(true);
   }
+  for (int i = 0; i < 256; ++i) w.ev_pool.push_back(new_event(false));
+  w.gembed_free = new_event(false);
   w.t0 = new_event(true);
   w.t_end = new_event(true);
   for (auto& e : w.join) e = new_event(false);
@@ -465,59 +506,129 @@ float lr_of(const ExecJob& j) { return j.lr; }
 
 }  // namespace
 
-void ExecutorImpl::adam_writeback(Worker& w, HostJob& hj, int s, int slot, int step, int local) {
+// Fused Adam for one layer of shard s, on the opt stream, as soon as its gradient is final:
+// m, v chunks H2D -> adam (params updated in place in the slot) -> params, m, v D2H (up).
+// `done` is recorded once Adam no longer reads `grads`.
+void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer, const float* grads, int step,
+                              cudaEvent_t done) {
   const ShardGeom& g = hj.geom[static_cast<size_t>(s)];
-  const long base = hy_layer_offset(&hj.m, g.l0);
+  const long host_off = hy_layer_offset(&hj.m, layer);
+  const long slot_off = host_off - hy_layer_offset(&hj.m, g.l0);
+  const long nfl = hy_layer_floats(&hj.m, layer);
   const long chunk = w.stg_chunk;
   const ExecJob& spec = *hj.spec;
-  hy::AdamHyper h{lr_of(spec), spec.beta1, spec.beta2, spec.eps, spec.weight_decay, 0.f, 0.f};
+  hy::AdamHyper h{spec.lr, spec.beta1, spec.beta2, spec.eps, spec.weight_decay, 0.f, 0.f};
   h.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta1), step));
   h.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta2), step));
-  Tracked& ptr = *hj.params_tr[static_cast<size_t>(s)];
-  Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
-  // host regions: m/v read by opt (H2D), written by up (D2H); params written by up
-  mvt.before_read(w.opt);
-  ptr.before_write(w.up);
-  mvt.before_write(w.up);
-  // Adam runs on the opt stream (not comp): the next shard's compute overlaps this shard's
-  // optimizer-state streaming. It reads the grads and rewrites the slot's params in place.
-  w.slot_tr[slot].before_write(w.opt);
-  w.gbuf_tr.before_read(w.opt);
+  // the layer's gradient is final and its params are no longer read by the compute stream
+  cudaEvent_t ready = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
+  check_cuda(cudaEventRecord(ready, w.comp), "layer ready");
+  check_cuda(cudaStreamWaitEvent(w.opt, ready, 0), "layer ready wait");
   int c = 0;
-  for (long off = 0; off < g.param_floats; off += chunk, ++c) {
-    const long n = std::min(chunk, g.param_floats - off);
+  for (long off = 0; off < nfl; off += chunk, ++c) {
+    const long n = std::min(chunk, nfl - off);
     const size_t bytes = sizeof(float) * static_cast<size_t>(n);
-    const int si = c % kStaging;
+    const int si = w.stg_round++ % kStaging;
     float* sm = w.stg[si];
     float* sv = w.stg[si] + chunk;
     Tracked& stg = w.stg_tr[si];
-    // opt stream: m, v chunk -> staging, then fused Adam on (params, grads, m, v)
     stg.before_write(w.opt);
-    check_cuda(cudaMemcpyAsync(sm, hj.mom + base + off, bytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
-    check_cuda(cudaMemcpyAsync(sv, hj.var + base + off, bytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
+    check_cuda(cudaMemcpyAsync(sm, hj.mom + host_off + off, bytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
+    check_cuda(cudaMemcpyAsync(sv, hj.var + host_off + off, bytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
     w.st.opt_h2d_bytes += 2.0 * bytes;
     w.st.h2d_bytes += 2.0 * bytes;
-    check_cuda(hy::adam_update(w.opt, n, w.slot[slot] + off, w.gbuf + off, sm, sv, h), "adam");
+    check_cuda(hy::adam_update(w.opt, n, w.slot[slot] + slot_off + off, grads + off, sm, sv, h), "adam");
     ++w.st.kernel_launches;
     stg.after_write(w.opt);
-    // up: updated params + m, v -> host
     stg.before_read(w.up);
-    check_cuda(cudaMemcpyAsync(hj.params + base + off, w.slot[slot] + off, bytes, cudaMemcpyDeviceToHost, w.up),
+    check_cuda(cudaMemcpyAsync(hj.params + host_off + off, w.slot[slot] + slot_off + off, bytes,
+                               cudaMemcpyDeviceToHost, w.up),
                "p d2h");
-    check_cuda(cudaMemcpyAsync(hj.mom + base + off, sm, bytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
-    check_cuda(cudaMemcpyAsync(hj.var + base + off, sv, bytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
+    check_cuda(cudaMemcpyAsync(hj.mom + host_off + off, sm, bytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
+    check_cuda(cudaMemcpyAsync(hj.var + host_off + off, sv, bytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
     stg.after_read(w.up);
     w.st.opt_d2h_bytes += 2.0 * bytes;
     w.st.d2h_bytes += 3.0 * bytes;
   }
-  mvt.after_read(w.opt);
-  w.slot_tr[slot].after_write(w.opt);
-  w.slot_tr[slot].after_read(w.up);
-  w.gbuf_tr.after_read(w.opt);
-  check_cuda(cudaEventRecord(w.timing[static_cast<size_t>(local)].d1, w.up), "d1");
-  ptr.after_write(w.up);
-  mvt.after_write(w.up);
+  check_cuda(cudaEventRecord(done, w.opt), "adam done");
 }
+
+namespace {
+
+// GradSink of one backward task: embedding grads in their own buffer, the other layers in
+// the worker's FIFO ring; release() hands each layer to adam_layer immediately.
+struct StreamingSink : hy::GradSink {
+  ExecutorImpl& ex;
+  Worker& w;
+  HostJob& hj;
+  int s, slot, step;
+  std::map<int, float*> live;
+
+  StreamingSink(ExecutorImpl& e, Worker& wk, HostJob& h, int shard, int sl, int st)
+      : ex(e), w(wk), hj(h), s(shard), slot(sl), step(st) {}
+
+  float* acquire(int layer) override {
+    const long len = hy_pad32(hy_layer_floats(&hj.m, layer));
+    float* p;
+    if (layer == 0) {
+      check_cuda(cudaStreamWaitEvent(w.comp, w.gembed_free, 0), "gembed wait");
+      p = w.gembed;
+    } else {
+      if (w.ring_head + len > w.ring_floats) w.ring_head = 0;
+      const long lo = w.ring_head, hi = w.ring_head + len;
+      // retire (wait for) every in-flight layer overlapping [lo, hi)
+      std::deque<Worker::RingEntry> keep;
+      for (const Worker::RingEntry& e : w.ring_live) {
+        if (e.off < hi && lo < e.off + e.len) {
+          if (!e.done) throw InvalidArgument("gradient ring too small for an unreleased layer");
+          check_cuda(cudaStreamWaitEvent(w.comp, e.done, 0), "ring wait");
+        } else {
+          keep.push_back(e);
+        }
+      }
+      w.ring_live.swap(keep);
+      p = w.ring + lo;
+      w.ring_head = hi;
+      w.ring_live.push_back(Worker::RingEntry{lo, len, nullptr});
+    }
+    check_cuda(cudaMemsetAsync(p, 0, sizeof(float) * static_cast<size_t>(len), w.comp), "zero grads");
+    live[layer] = p;
+    return p;
+  }
+
+  // With the Adam staging aliased onto the backward's scratch (tiny HBM caps), layers are
+  // queued and handed to the optimizer only after the backward (flush()).
+  bool deferred = false;
+  std::vector<int> queued;
+
+  void release(int layer) override {
+    if (deferred) {
+      queued.push_back(layer);
+      return;
+    }
+    emit(layer);
+  }
+
+  void flush() {
+    for (int l : queued) emit(l);
+    queued.clear();
+  }
+
+  void emit(int layer) {
+    float* p = live.at(layer);
+    cudaEvent_t done = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
+    if (layer == 0) {
+      done = w.gembed_free;
+    } else {
+      for (auto& e : w.ring_live) {
+        if (w.ring + e.off == p) e.done = done;
+      }
+    }
+    ex.adam_layer(w, hj, s, slot, layer, p, step, done);
+  }
+};
+
+}  // namespace
 
 void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   const SimTask& task = tasks[static_cast<size_t>(t)];
@@ -726,16 +837,27 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   } else if (fwd) {
     w.st.elided_compute_tasks += 1;
   } else {
-    // The previous shard's Adam (opt stream) may still read the grad buffer: wait for it
-    // only after this shard's forward recompute, then zero it.
-    hy::run_backward(w.comp, hj.m, g, w.slot[slot], w.gbuf, io, sc, [&] {
-      w.gbuf_tr.before_write(w.comp);
-      check_cuda(cudaMemsetAsync(w.gbuf, 0, sizeof(float) * static_cast<size_t>(g.param_floats), w.comp),
-                 "zero grads");
-    });
+    // Gradients stream into the optimizer layer by layer (StreamingSink -> adam_layer on
+    // the opt stream); host params / m / v of the shard are rewritten by the up stream.
+    Tracked& ptr = *hj.params_tr[static_cast<size_t>(s)];
+    Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
+    mvt.before_read(w.opt);
+    ptr.before_write(w.up);
+    mvt.before_write(w.up);
+    check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
+    StreamingSink sink(*this, w, hj, s, slot, gmb + 1);
+    sink.deferred = w.stg_alias;
+    hy::run_backward(w.comp, hj.m, g, w.slot[slot], sink, io, sc);
     if (w.stg_alias) {
-      for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // m/v loads wait for the backward
+      for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // staging = scratch: after the backward
     }
+    sink.flush();
+    mvt.after_read(w.opt);
+    ptr.after_write(w.up);
+    mvt.after_write(w.up);
+    w.slot_tr[slot].after_write(w.opt);  // Adam rewrote the params in place
+    w.slot_tr[slot].after_read(w.up);    // ... and the up stream wrote them back
+    w.opt_pending = true;
     if (g.has_head && !g.has_embed) {
       w.z_tr.before_write(w.comp);
       check_cuda(cudaMemcpyAsync(w.zbuf, sc.z, act_bytes, cudaMemcpyDeviceToDevice, w.comp), "z save");
@@ -746,7 +868,6 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       check_cuda(cudaMemcpyAsync(w.loss_dev + local, sc.loss, sizeof(double), cudaMemcpyDeviceToDevice, w.comp),
                  "loss copy");
     }
-    w.gbuf_tr.after_write(w.comp);
   }
   check_cuda(cudaEventRecord(tm.c1, w.comp), "c1");
   w.slot_tr[slot].after_read(w.comp);
@@ -764,7 +885,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   }
 
   // ---- ActDemote + GradOffload (up) ---------------------------------------------------
-  check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
+  if (fwd) check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
   if (aout >= 0) {  // forward boundary activation -> checkpoint store
     Tracked& host = *hj.ckpt_tr[static_cast<size_t>(s)];
     w.abuf_tr[aout].before_read(w.up);
@@ -796,13 +917,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     w.z_tr.after_read(w.up);
     w.st.d2h_bytes += static_cast<double>(act_bytes);
   }
+  check_cuda(cudaEventRecord(tm.d1, w.up), "d1");
   if (!fwd) {
-    const int step = gmb + 1;
-    adam_writeback(w, hj, s, slot, step, local);
     hj.version[static_cast<size_t>(s)] += 1;
     w.slot_tag[slot] = Tag{j, g.wte_offset >= 0 ? hj.version[0] : -1, s, hj.version[static_cast<size_t>(s)]};
-  } else {
-    check_cuda(cudaEventRecord(tm.d1, w.up), "d1");
   }
   {
     std::lock_guard<std::mutex> lk(flag_mu);

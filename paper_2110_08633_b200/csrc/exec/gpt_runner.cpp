@@ -212,8 +212,8 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
   }
 }
 
-void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, float* grads,
-                  const TaskIO& io, Scratch& s, const std::function<void()>& before_grads) {
+void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, GradSink& sink,
+                  const TaskIO& io, Scratch& s) {
   const long n = static_cast<long>(s.M) * m.d;
   const int b0 = std::max(g.l0, 1);
   const int nb = g.n_blocks;
@@ -227,29 +227,38 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   for (int i = 0; i < nb; ++i) {
     block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, s.stash + (i + 1) * n, s);
   }
-  if (before_grads) before_grads();
+  // The last block's intermediates survive in scratch unless the head pass (whose logits
+  // alias the MLP buffers) runs in between: then its recompute can be skipped.
+  bool last_block_live = nb > 0 && !g.has_head;
   // 2) gradient wrt the shard output
   float* dh = s.tmp_h;
+  float* gembed = nullptr;
+  if (g.has_embed) gembed = sink.acquire(0);  // wte/wpe grads: head (k == 1) + embedding
   if (g.has_head) {
     const float* lnf = slot + lo(m, m.L + 1, g.l0);
-    float* glnf = grads + lo(m, m.L + 1, g.l0);
+    float* glnf = sink.acquire(m.L + 1);
     const float* wte = g.has_embed ? slot : slot + g.wte_offset;
-    float* dwte = g.has_embed ? grads : nullptr;  // otherwise deferred to shard 0 via z
+    float* dwte = g.has_embed ? gembed : nullptr;  // otherwise deferred to shard 0 via z
     const float* hfin = s.stash + nb * n;
     head_pass(st, m, lnf, wte, hfin, io.targets, s, true, dwte);
     check_cuda(layernorm_bwd(st, s.M, m.d, hfin, lnf, s.zmean, s.zrstd, s.dz, dh, false, glnf, glnf + hy_pad32(m.d),
                              s.ws),
                "ln_f bwd");
+    sink.release(m.L + 1);
   } else {
     check_cuda(cudaMemcpyAsync(dh, io.grad_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad in");
   }
-  // 3) blocks, last to first: recompute intermediates, back-propagate
+  // 3) blocks, last to first: recompute intermediates, back-propagate; each block's
+  //    gradients are handed to the optimizer as soon as they are final.
   for (int i = nb - 1; i >= 0; --i) {
-    const float* w = slot + lo(m, b0 + i, g.l0);
-    float* gw = grads + lo(m, b0 + i, g.l0);
-    float* scratch_out = s.stash + (i + 1) * n;  // block output no longer needed
-    block_forward(st, m, w, s.stash + i * n, scratch_out, s);
+    const int layer = b0 + i;
+    const float* w = slot + lo(m, layer, g.l0);
+    if (!(last_block_live && i == nb - 1)) {
+      block_forward(st, m, w, s.stash + i * n, s.stash + (i + 1) * n, s);  // block output is scratch here
+    }
+    float* gw = sink.acquire(layer);
     block_backward(st, m, w, gw, s.stash + i * n, dh, s);
+    sink.release(layer);
   }
   // 4) embedding (+ deferred tied-wte gradient from the head's saved z)
   if (g.has_embed) {
@@ -259,12 +268,13 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
       }
       float* saved_dz = s.dz;
       s.dz = nullptr;  // only dwte is wanted
-      head_pass(st, m, nullptr, slot, nullptr, io.targets, s, true, grads, /*z_ready=*/true);
+      head_pass(st, m, nullptr, slot, nullptr, io.targets, s, true, gembed, /*z_ready=*/true);
       s.dz = saved_dz;
     }
-    check_cuda(embed_bwd(st, s.M, m.T, m.d, io.tokens, dh, grads, grads + hy_pad32(static_cast<long>(m.V) * m.d),
+    check_cuda(embed_bwd(st, s.M, m.T, m.d, io.tokens, dh, gembed, gembed + hy_pad32(static_cast<long>(m.V) * m.d),
                          nullptr),
                "embed bwd");
+    sink.release(0);
   } else if (io.grad_out) {
     check_cuda(cudaMemcpyAsync(io.grad_out, dh, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "grad out");
   }

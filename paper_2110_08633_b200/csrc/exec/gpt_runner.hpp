@@ -59,10 +59,19 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
 // When the shard has the head but not the embed, the ln_f output z is left in s.z for the
 // caller to demote; when it has the embed but not the head, io.z_in drives the deferred
 // tied-wte gradient.
-// `before_grads` runs (on the host, enqueue order) after the forward recompute and before
-// anything writes `grads` — the caller inserts its stream waits / zeroing there.
-void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, float* grads,
-                  const TaskIO& io, Scratch& s, const std::function<void()>& before_grads);
+// Where a backward task's parameter gradients go. acquire(layer) returns zeroed device
+// storage for that layer's gradient (layout of hy_layer_floats; the caller may insert stream
+// waits), release(layer) is called once the layer's gradient is final so the optimizer can
+// consume it immediately. Layers are acquired last-to-first; the embedding (layer 0) is
+// acquired before the head when both are in the shard and released last.
+struct GradSink {
+  virtual ~GradSink() = default;
+  virtual float* acquire(int layer) = 0;
+  virtual void release(int layer) = 0;
+};
+
+void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, GradSink& sink,
+                  const TaskIO& io, Scratch& s);
 
 void check_cuda(cudaError_t e, const char* what);
 
