@@ -30,7 +30,8 @@ struct ExecOptions {
   uint64_t seed = 0;               // synthetic tokens
   int passes = 1;                  // times the whole plan is replayed (minibatch index continues)
   int warmup_passes = 0;           // replays before the timed ones (not in the trace)
-  long opt_chunk_floats = 4L << 20;  // Adam m/v streaming chunk
+  long opt_chunk_floats = 2L << 20;  // Adam m/v streaming chunk (elements)
+  bool opt_state_bf16 = false;       // Adam moments stored/streamed as bf16 (halves their link bytes)
   std::string params_out_dir;      // if set: final params of every executed job as job<j>.f32
   bool precision_fp32 = false;     // GEMMs as 3xTF32 (~fp32) instead of TF32
   double hbm_slack_bytes = 0;      // physical arena may exceed mem_bytes by this much (toy configs

@@ -460,6 +460,32 @@ int oracle_shard_bwd(const hy_dims* m, const float* params, float* grads, int l0
   return 0;
 }
 
+/* round-to-nearest-even to bfloat16, kept in a float */
+static float bf16_rne(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  u &= 0xFFFF0000u;
+  memcpy(&x, &u, 4);
+  return x;
+}
+
+void oracle_adam_state(long n, float* p, const float* g, float* m, float* v, float lr, float beta1, float beta2,
+                       float eps, float weight_decay, int step, int bf16_state) {
+  const float bc1 = (float)(1.0 - pow((double)beta1, step));
+  const float bc2 = (float)(1.0 - pow((double)beta2, step));
+  const float c1 = 1.f - beta1, c2 = 1.f - beta2;
+#pragma omp parallel for schedule(static)
+  for (long i = 0; i < n; ++i) {
+    const float mi = beta1 * m[i] + c1 * g[i];
+    const float vi = beta2 * v[i] + c2 * g[i] * g[i];
+    const float upd = (mi / bc1) / (sqrtf(vi / bc2) + eps);
+    p[i] = p[i] - lr * (upd + weight_decay * p[i]);
+    m[i] = bf16_state ? bf16_rne(mi) : mi;
+    v[i] = bf16_state ? bf16_rne(vi) : vi;
+  }
+}
+
 void oracle_adam(long n, float* p, const float* g, float* m, float* v, float lr, float beta1, float beta2, float eps,
                  float weight_decay, int step) {
   const float bc1 = (float)(1.0 - pow((double)beta1, step));

@@ -37,6 +37,11 @@ int oracle_shard_bwd(const hy_dims* m, const float* params, float* grads, int l0
 void oracle_adam(long n, float* p, const float* g, float* m, float* v, float lr, float beta1, float beta2, float eps,
                  float weight_decay, int step);
 
+/* Same with the moments rounded to bfloat16 (RNE) after each update when bf16_state != 0
+ * (the update itself uses the unrounded fp32 moments), as the bf16-state GPU kernel does. */
+void oracle_adam_state(long n, float* p, const float* g, float* m, float* v, float lr, float beta1, float beta2,
+                       float eps, float weight_decay, int step, int bf16_state);
+
 /* Whole-model train step (single shard) — the unsharded reference. Returns the loss. */
 double oracle_train_step(const hy_dims* m, float* params, float* mom, float* var, int step, float lr,
                          const int32_t* tokens, const int32_t* targets);

@@ -29,6 +29,7 @@ def lib():
         _lib.oracle_shard_fwd.argtypes = [P, P, ctypes.c_int, ctypes.c_int, P, P, P, P, P]
         _lib.oracle_shard_bwd.argtypes = [P, P, P, ctypes.c_int, ctypes.c_int, P, P, P, P, P]
         _lib.oracle_adam.argtypes = [ctypes.c_long, P, P, P, P] + [ctypes.c_float] * 5 + [ctypes.c_int]
+        _lib.oracle_adam_state.argtypes = [ctypes.c_long, P, P, P, P] + [ctypes.c_float] * 5 + [ctypes.c_int] * 2
         _lib.oracle_train_step.argtypes = [P, P, P, P, ctypes.c_int, ctypes.c_float, P, P]
         _lib.oracle_train_step.restype = ctypes.c_double
         _lib.oracle_init_params.argtypes = [P, ctypes.c_uint64, P]
@@ -94,11 +95,12 @@ def shard_bwd(m, params, grads, l0, l1, tok, tgt, act_in, grad_out):
     return grad_in
 
 
-def adam(p, g, mom, var, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0):
-    lib().oracle_adam(p.size, _p(p), _p(g), _p(mom), _p(var), lr, beta1, beta2, eps, wd, step)
+def adam(p, g, mom, var, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, wd=0.0, bf16_state=False):
+    lib().oracle_adam_state(p.size, _p(p), _p(g), _p(mom), _p(var), lr, beta1, beta2, eps, wd, step,
+                            int(bf16_state))
 
 
-def sharded_step(m, params, mom, var, starts, step, lr, tok, tgt):
+def sharded_step(m, params, mom, var, starts, step, lr, tok, tgt, bf16_state=False):
     """One minibatch through the SHARP shard chain F(0..k-1), B(k-1..0), then Adam —
     the reference's task order (strategies.cpp:743-782). Returns the loss."""
     n_layers = m.L + 2
@@ -118,7 +120,7 @@ def sharded_step(m, params, mom, var, starts, step, lr, tok, tgt):
     for s in reversed(range(k)):
         ckpt = acts[s - 1] if s > 0 else None
         g = shard_bwd(m, params, grads, bounds[s], bounds[s + 1], tok, tgt, ckpt, g)
-    adam(params, grads, mom, var, lr, step)
+    adam(params, grads, mom, var, lr, step, bf16_state=bf16_state)
     return loss
 
 
@@ -138,7 +140,7 @@ def model_key(config_seed, model_index):
     return mix64((config_seed * 0x100000001B3 + model_index) & M64)
 
 
-def run_workload_cpu(config, shard_starts, max_minibatches=None, jobs=None):
+def run_workload_cpu(config, shard_starts, max_minibatches=None, jobs=None, bf16_state=False):
     """Execute every job of a workload config on the CPU oracle in the SHARP chain order
     (per job: minibatches in order, each F(0..k-1), B(k-1..0), Adam). Returns
     (losses[job][mb], params[job])."""
@@ -160,6 +162,6 @@ def run_workload_cpu(config, shard_starts, max_minibatches=None, jobs=None):
         ls = []
         for mb in range(n_mb):
             tok, tgt = tokens(m, seed, j, mb)
-            ls.append(sharded_step(m, p, mom, var, shard_starts[j], mb + 1, lr, tok, tgt))
+            ls.append(sharded_step(m, p, mom, var, shard_starts[j], mb + 1, lr, tok, tgt, bf16_state=bf16_state))
         losses[j], params_out[j] = ls, p
     return losses, params_out

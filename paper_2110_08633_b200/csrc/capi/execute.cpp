@@ -89,6 +89,9 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   const std::string prec = req.value("precision", std::string("tf32"));
   if (prec != "tf32" && prec != "fp32") throw InvalidArgument("precision must be 'tf32' or 'fp32'");
   ex.precision_fp32 = prec == "fp32";
+  const std::string state = req.value("opt_state", std::string("fp32"));
+  if (state != "fp32" && state != "bf16") throw InvalidArgument("opt_state must be 'fp32' or 'bf16'");
+  ex.opt_state_bf16 = state == "bf16";
   if (req.contains("device_ids")) ex.device_ids = req["device_ids"].get<std::vector<int>>();
   if (req.contains("run_devices")) ex.run_devices = req["run_devices"].get<std::vector<int>>();
   if (req.contains("opt_chunk_floats")) ex.opt_chunk_floats = req["opt_chunk_floats"].get<long>();

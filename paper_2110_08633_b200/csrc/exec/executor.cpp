@@ -43,7 +43,7 @@ namespace {
 using hy::check_cuda;
 using hy::ShardGeom;
 
-constexpr int kStaging = 2;
+constexpr int kStaging = 4;
 
 cudaEvent_t new_event(bool timing) {
   cudaEvent_t e;
@@ -174,7 +174,7 @@ struct Worker {
   int32_t* tok[2] = {nullptr, nullptr};
   Tag tok_tag[2];
   Tracked tok_tr[2];
-  float* stg[kStaging] = {nullptr, nullptr};
+  float* stg[kStaging] = {nullptr, nullptr, nullptr, nullptr};
   Tracked stg_tr[kStaging];
   float* scratch = nullptr;
   double* loss_dev = nullptr;  // per task slot
@@ -298,13 +298,14 @@ void ExecutorImpl::setup_host_job(int j) {
                                      s + 1 < k ? starts[static_cast<size_t>(s) + 1] : n_layers));
   }
   hj.params = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.total)));
-  hj.mom = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.total)));
-  hj.var = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.total)));
+  const size_t state_bytes = (exec.opt_state_bf16 ? 2 : 4) * static_cast<size_t>(hj.total);
+  hj.mom = static_cast<float*>(pinned(state_bytes));
+  hj.var = static_cast<float*>(pinned(state_bytes));
   // GPT-2 init, layers in parallel (each layer's stream is independent of the others).
 #pragma omp parallel for schedule(dynamic)
   for (int l = 0; l < n_layers; ++l) hy_init_layer(&hj.m, spec.model_key, l, hj.params + hy_layer_offset(&hj.m, l));
-  std::memset(hj.mom, 0, sizeof(float) * static_cast<size_t>(hj.total));
-  std::memset(hj.var, 0, sizeof(float) * static_cast<size_t>(hj.total));
+  std::memset(hj.mom, 0, state_bytes);
+  std::memset(hj.var, 0, state_bytes);
   for (int b = 0; b + 1 < k; ++b) {
     hj.ckpt.push_back(static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.n_act))));
     hj.grad.push_back(static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.n_act))));
@@ -524,31 +525,45 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer
   cudaEvent_t ready = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
   check_cuda(cudaEventRecord(ready, w.comp), "layer ready");
   check_cuda(cudaStreamWaitEvent(w.opt, ready, 0), "layer ready wait");
+  const bool bf16 = exec.opt_state_bf16;
+  const size_t es = bf16 ? 2 : 4;  // bytes per moment element
+  char* hm = reinterpret_cast<char*>(hj.mom);
+  char* hv = reinterpret_cast<char*>(hj.var);
   int c = 0;
   for (long off = 0; off < nfl; off += chunk, ++c) {
     const long n = std::min(chunk, nfl - off);
     const size_t bytes = sizeof(float) * static_cast<size_t>(n);
+    const size_t sbytes = es * static_cast<size_t>(n);
     const int si = w.stg_round++ % kStaging;
-    float* sm = w.stg[si];
-    float* sv = w.stg[si] + chunk;
+    char* sm = reinterpret_cast<char*>(w.stg[si]);
+    char* sv = sm + es * static_cast<size_t>(chunk);
     Tracked& stg = w.stg_tr[si];
+    const size_t hoff = es * static_cast<size_t>(host_off + off);
     stg.before_write(w.opt);
-    check_cuda(cudaMemcpyAsync(sm, hj.mom + host_off + off, bytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
-    check_cuda(cudaMemcpyAsync(sv, hj.var + host_off + off, bytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
-    w.st.opt_h2d_bytes += 2.0 * bytes;
-    w.st.h2d_bytes += 2.0 * bytes;
-    check_cuda(hy::adam_update(w.opt, n, w.slot[slot] + slot_off + off, grads + off, sm, sv, h), "adam");
+    check_cuda(cudaMemcpyAsync(sm, hm + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
+    check_cuda(cudaMemcpyAsync(sv, hv + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
+    w.st.opt_h2d_bytes += 2.0 * sbytes;
+    w.st.h2d_bytes += 2.0 * sbytes;
+    if (bf16) {
+      check_cuda(hy::adam_update_bf16(w.opt, n, w.slot[slot] + slot_off + off, grads + off,
+                                      reinterpret_cast<uint16_t*>(sm), reinterpret_cast<uint16_t*>(sv), h),
+                 "adam bf16");
+    } else {
+      check_cuda(hy::adam_update(w.opt, n, w.slot[slot] + slot_off + off, grads + off, reinterpret_cast<float*>(sm),
+                                 reinterpret_cast<float*>(sv), h),
+                 "adam");
+    }
     ++w.st.kernel_launches;
     stg.after_write(w.opt);
     stg.before_read(w.up);
     check_cuda(cudaMemcpyAsync(hj.params + host_off + off, w.slot[slot] + slot_off + off, bytes,
                                cudaMemcpyDeviceToHost, w.up),
                "p d2h");
-    check_cuda(cudaMemcpyAsync(hj.mom + host_off + off, sm, bytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
-    check_cuda(cudaMemcpyAsync(hj.var + host_off + off, sv, bytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
+    check_cuda(cudaMemcpyAsync(hm + hoff, sm, sbytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
+    check_cuda(cudaMemcpyAsync(hv + hoff, sv, sbytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
     stg.after_read(w.up);
-    w.st.opt_d2h_bytes += 2.0 * bytes;
-    w.st.d2h_bytes += 3.0 * bytes;
+    w.st.opt_d2h_bytes += 2.0 * sbytes;
+    w.st.d2h_bytes += static_cast<double>(bytes) + 2.0 * sbytes;
   }
   check_cuda(cudaEventRecord(done, w.opt), "adam done");
 }

@@ -13,6 +13,7 @@
 
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -131,7 +132,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<2 * BN>(tmem_slot);
+  constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -363,7 +365,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<2 * BN>(tmem_base);
+    tmem_dealloc<kTmemCols>(tmem_base);
   }
 }
 
@@ -461,8 +463,48 @@ cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, lon
   return cudaGetLastError();
 }
 
+template <int BN>
+cudaError_t dispatch_bn(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+                        long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
+  if (!a_mn && !b_mn) return launch<BN, false, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (!a_mn && b_mn) return launch<BN, false, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (a_mn && !b_mn) return launch<BN, true, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+  return launch<BN, true, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+}
+
+// Output tile width: wider tiles cut the shared-memory traffic per MMA (the TF32 pipe is
+// smem-bound at BN=128), but fewer tiles can leave SMs idle in the last wave. Pick the
+// width minimising waves x relative per-tile cost.
+int pick_bn(int M, int N, long batches) {
+  static const int forced = [] {
+    const char* e = std::getenv("HY_GEMM_BN");  // experiments only
+    return e ? std::atoi(e) : 0;
+  }();
+  if (forced == 128 || forced == 192 || forced == 256) return forced;
+  static const int kBN[3] = {128, 192, 256};
+  static const double kCost[3] = {128 / 0.50, 192 / 0.60, 256 / 0.66};  // relative time per tile
+  const long tm = (M + BM - 1) / BM;
+  int best = 128;
+  double best_t = 1e300;
+  for (int i = 0; i < 3; ++i) {
+    if (kBN[i] > 128 && N <= 128) break;
+    const long tiles = tm * ((N + kBN[i] - 1) / kBN[i]) * batches;
+    const double t = static_cast<double>((tiles + sm_count() - 1) / sm_count()) * kCost[i];
+    if (t < best_t - 1e-9) {
+      best_t = t;
+      best = kBN[i];
+    }
+  }
+  return best;
+}
+
 cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
                      long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
+  if (!t_prec3 && bat.causal == kCausalNone) {
+    const int bn = pick_bn(M, N, static_cast<long>(bat.nb1) * bat.nb2);
+    if (bn == 256) return dispatch_bn<256>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+    if (bn == 192) return dispatch_bn<192>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+  }
   if (t_prec3) {
     if (!a_mn && !b_mn) return launch<128, false, false, true>(st, M, N, K, A, lda, B, ldb, e, bat);
     if (!a_mn && b_mn) return launch<128, false, true, true>(st, M, N, K, A, lda, B, ldb, e, bat);

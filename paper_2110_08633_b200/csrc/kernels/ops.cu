@@ -1,5 +1,7 @@
 // HBM-bound kernels: one warp per row for row reductions (128-bit loads, warp shuffles),
 // grid-stride float4 loops for elementwise work, two-stage deterministic column sums.
+#include <cuda_bf16.h>
+
 #include <cfloat>
 
 #include "launch_count.cuh"
@@ -315,6 +317,35 @@ __global__ void adam_kernel(long n4, float4* __restrict__ p, const float4* __res
   }
 }
 
+// Same update with the moments stored in bf16 (round-to-nearest-even after each update):
+// halves the optimizer state a spilled shard streams over the host link.
+__global__ void adam_bf16_kernel(long n4, float4* __restrict__ p, const float4* __restrict__ g,
+                                 uint2* __restrict__ m, uint2* __restrict__ v, AdamHyper h) {
+  const float c1 = 1.f - h.beta1, c2 = 1.f - h.beta2;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    float4 pp = p[i], gg = g[i];
+    const uint2 mm = m[i], vv = v[i];
+    __nv_bfloat16 mb[4], vb[4];
+    *reinterpret_cast<uint2*>(mb) = mm;
+    *reinterpret_cast<uint2*>(vb) = vv;
+    float* pe = &pp.x;
+    const float* ge = &gg.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float mk = h.beta1 * __bfloat162float(mb[k]) + c1 * ge[k];
+      const float vk = h.beta2 * __bfloat162float(vb[k]) + c2 * ge[k] * ge[k];
+      mb[k] = __float2bfloat16_rn(mk);
+      vb[k] = __float2bfloat16_rn(vk);
+      const float upd = (mk / h.bc1) / (sqrtf(vk / h.bc2) + h.eps);
+      pe[k] = pe[k] - h.lr * (upd + h.weight_decay * pe[k]);
+    }
+    p[i] = pp;
+    m[i] = *reinterpret_cast<uint2*>(mb);
+    v[i] = *reinterpret_cast<uint2*>(vb);
+  }
+}
+
 int grid_for(long n, int block) {
   long g = (n + block - 1) / block;
   const long cap = static_cast<long>(sms()) * 8;
@@ -422,6 +453,17 @@ cudaError_t softmax_xent(cudaStream_t s, int rows, int V, float* logits, long ld
 cudaError_t sum_to_double(cudaStream_t s, int n, const float* x, double* out, bool accumulate) {
   count_launch();
   sum_double_kernel<<<1, 256, 0, s>>>(n, x, out, accumulate ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t adam_update_bf16(cudaStream_t s, long n, float* p, const float* g, uint16_t* m, uint16_t* v,
+                             const AdamHyper& h) {
+  if (n % 4) return cudaErrorInvalidValue;
+  const long n4 = n / 4;
+  count_launch();
+  adam_bf16_kernel<<<grid_for(n4, 256), 256, 0, s>>>(n4, reinterpret_cast<float4*>(p),
+                                                     reinterpret_cast<const float4*>(g), reinterpret_cast<uint2*>(m),
+                                                     reinterpret_cast<uint2*>(v), h);
   return cudaGetLastError();
 }
 

@@ -34,6 +34,9 @@ struct AdamHyper {
   float lr, beta1, beta2, eps, weight_decay, bc1, bc2;  // bc = 1 - beta^step
 };
 cudaError_t adam_update(cudaStream_t s, long n, float* p, const float* g, float* m, float* v, const AdamHyper& h);
+// Moments stored as bf16 bit patterns (RNE after each update); params/grads fp32.
+cudaError_t adam_update_bf16(cudaStream_t s, long n, float* p, const float* g, uint16_t* m, uint16_t* v,
+                             const AdamHyper& h);
 
 // Tensor-core attention (attention_tc.cu). `work` holds score matrices: forward needs
 // T*T floats per (batch, head) processed at once, backward 2*T*T; chunks are sized to fit.

@@ -39,7 +39,7 @@ def tiny_config(mem=50e6, n_blocks=2, d=64, T=32, B=2, mbs=2, jobs=2):
 def compare(cfg, tmp_path, strategy="sharp", loss_tol=1e-3, param_tol=1e-3, **kw):
     res = P.execute(cfg, strategy=strategy, params_out_dir=str(tmp_path), **kw)
     starts = res["shard_starts"] or [[0]] * len(cfg["jobs"])
-    losses, params = O.run_workload_cpu(cfg, starts)
+    losses, params = O.run_workload_cpu(cfg, starts, bf16_state=kw.get("opt_state") == "bf16")
     for j in losses:
         gl = np.array(res["losses"][j][: len(losses[j])])
         cl = np.array(losses[j])
@@ -79,6 +79,14 @@ def test_head_shard_without_embedding(tmp_path, mem, starts, precision):
     res = compare(cfg, tmp_path, hbm_slack_bytes=8e6, precision=precision, **tol)
     assert res["shard_starts"][0] == starts
     assert res["stats"]["arena_bytes"][0] <= mem + 8e6
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", dict(loss_tol=1e-5, param_tol=1e-4)), ("tf32", {})])
+def test_bf16_optimizer_state(tmp_path, precision, tol):
+    """Adam moments stored/streamed as bf16 (halves optimizer-state link bytes); compared with
+    the oracle applying the same bf16 rounding to its moments."""
+    cfg = tiny_config(mbs=3)
+    compare(cfg, tmp_path, precision=precision, opt_state="bf16", **tol)
 
 
 def test_single_shard_resident(tmp_path):

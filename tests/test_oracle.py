@@ -100,3 +100,15 @@ def test_sharded_equals_unsharded(tiny, starts):
         lb = O.sharded_step(m, p_b, mb_, vb, starts, step, 1e-3, tok, tgt)
         assert la == lb
     assert np.array_equal(p_a, p_b)
+
+
+def test_bf16_state_rounding_is_rne():
+    p = np.zeros(4, dtype=np.float32)
+    g = np.array([1.0, -3.0, 1e-3, 7.7], dtype=np.float32)
+    m = np.zeros(4, dtype=np.float32)
+    v = np.zeros(4, dtype=np.float32)
+    O.adam(p, g, m, v, 1e-3, 1, bf16_state=True)
+    for x in np.concatenate([m, v]):
+        bits = np.array([x], dtype=np.float32).view(np.uint32)[0]
+        assert bits & 0xFFFF == 0  # representable in bfloat16
+    assert abs(m[3] - 0.77) / 0.77 < 1 / 128
