@@ -34,7 +34,8 @@ $(B)/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 $(PKG)/libhydra.so: $(HOST_OBJS) $(CU_OBJS)
-	$(CXX) -shared $^ -o $@ -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -pthread -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp
+	$(CXX) -shared $^ -o $@ -Wl,-Bsymbolic -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -pthread \
+	  -L/usr/lib/gcc/x86_64-linux-gnu/13 -lgomp
 
 $(B)/plan_dump_b200: oracle/plan_dump.cpp $(PKG)/libhydra.so
 	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lhydra -Wl,-rpath,'$$ORIGIN/../$(PKG)'

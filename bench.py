@@ -93,16 +93,30 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------- CPU leg
-def cpu_sample(cfg, rows=1):
+def reference_shard_starts(cfg):
+    """Job 0's partition from the reference partitioner compiled from its own sources
+    (oracle/_ref/libspillsim_ref.so); the B200 build produces the identical cut
+    (tests/test_plan_parity.py)."""
+    import ctypes
+    lib = ctypes.CDLL(os.path.join(ROOT, "oracle", "_ref", "libspillsim_ref.so"))
+    lib.ref_shard_starts.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.c_int]
+    buf = (ctypes.c_int * 64)()
+    n = lib.ref_shard_starts(json.dumps(cfg).encode(), 0, buf, 64)
+    if n <= 0:
+        raise RuntimeError("reference partitioner failed")
+    return list(buf[:n])
+
+
+def cpu_sample(cfg, rows=1, starts=None):
     """CPU port (oracle/gpt_oracle.c, OpenMP over all host cores) of one bounded sample:
     `rows` sequence(s) of job 0 minibatch 0 through all its shard tasks F(0..k-1),
     B(k-1..0) + Adam, with the partition of the real workload. Returns seconds."""
     import numpy as np
 
     from oracle import oracle as O
-    import paper_2110_08633_b200 as P
 
-    starts = P.plan(cfg)["partitions"][0]["shard_starts"]
+    if starts is None:
+        starts = reference_shard_starts(cfg)
     g = cfg["models"][0]["generator"]
     m = O.make_dims(d=g["d_model"], L=g["n_blocks"], T=g["seq_len"], B=rows)
     p = O.init_params(m, O.model_key(int(cfg.get("seed", 0)), 0))
@@ -249,7 +263,8 @@ def run_hydra(args, cfg):
         "bytes_per_step": {k: v for k, v in st.items() if k.endswith("_per_pass")},
         "arena_bytes": st["arena_bytes"],
         "setup_s": round(setup_s, 2),
-        "losses_job0": [round(x, 5) for x in res["losses"][0][:4]] if res["losses"] and res["losses"][0] else [],
+        "losses_job0_last_step": [round(x, 5) for x in res["losses"][0][-cfg["jobs"][0]["minibatches_per_epoch"]:]]
+        if res["losses"] and res["losses"][0] else [],
         "device_busy_frac": round(st["device_busy_s_last_pass"] / res["pass_seconds"][-1], 4),
     }
     # shard roofline (north_star): per task max(compute at peak, link bytes / link BW), cost-model bytes
@@ -272,7 +287,7 @@ def run_hydra(args, cfg):
         out["roofline"] = {"error": str(e)}
     if not args.no_cpu_baseline:
         try:
-            secs, cores, _ = cpu_sample(cfg)
+            secs, cores, _ = cpu_sample(cfg, starts=res["shard_starts"][0])
             out["cpu_baseline"] = {"value": round(1.0 / secs, 5), "unit": "samples/s", "cores": cores, "kind": "port",
                                    "sample": "1 sequence (of 8) of job 0 minibatch 0 through all shard tasks "
                                              f"F+B+Adam on the CPU oracle ({secs:.1f} s)"}

@@ -46,4 +46,19 @@ int ref_run_strategy(const char* config_json, const char* strategy, int gpus, do
   }
 }
 
+// Shard starts of job `job` under SHARP for the config (the reference partitioner).
+int ref_shard_starts(const char* config_json, int job, int* out, int max_out) {
+  try {
+    const WorkloadConfig cfg = parse_workload_config(config_json);
+    const auto jobs = materialize_jobs(cfg);
+    const auto cs = build_strategy(strategy_for(cfg, StrategyKind::kSharp), jobs, cfg.cluster, cfg.options.buffer_policy);
+    const auto& starts = cs.partitionings.at(static_cast<size_t>(job)).shard_starts;
+    const int n = static_cast<int>(starts.size());
+    for (int i = 0; i < n && i < max_out; ++i) out[i] = starts[static_cast<size_t>(i)];
+    return n;
+  } catch (...) {
+    return -1;
+  }
+}
+
 }
