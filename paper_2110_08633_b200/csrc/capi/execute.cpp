@@ -86,6 +86,7 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   ex.warmup_passes = req.value("warmup_passes", 0);
   ex.params_out_dir = req.value("params_out_dir", std::string());
   ex.hbm_slack_bytes = req.value("hbm_slack_bytes", 0.0);
+  ex.debug_skip = req.value("debug_skip", 0);
   const std::string prec = req.value("precision", std::string("tf32"));
   if (prec != "tf32" && prec != "fp32") throw InvalidArgument("precision must be 'tf32' or 'fp32'");
   ex.precision_fp32 = prec == "fp32";

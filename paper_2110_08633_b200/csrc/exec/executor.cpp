@@ -45,6 +45,15 @@ using hy::ShardGeom;
 
 constexpr int kStaging = 4;
 
+// Diagnostics only (ExecOptions::debug_skip): 1 = skip host<->device copies, 2 = skip the
+// shard compute — to split a pass into its link-bound and compute-bound parts.
+int g_debug_skip = 0;
+
+cudaError_t xfer(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+  if (g_debug_skip == 1 && (kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost)) return cudaSuccess;
+  return cudaMemcpyAsync(dst, src, bytes, kind, st);
+}
+
 cudaEvent_t new_event(bool timing) {
   cudaEvent_t e;
   check_cuda(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming), "event create");
@@ -540,8 +549,8 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer
     Tracked& stg = w.stg_tr[si];
     const size_t hoff = es * static_cast<size_t>(host_off + off);
     stg.before_write(w.opt);
-    check_cuda(cudaMemcpyAsync(sm, hm + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
-    check_cuda(cudaMemcpyAsync(sv, hv + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
+    check_cuda(xfer(sm, hm + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
+    check_cuda(xfer(sv, hv + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
     w.st.opt_h2d_bytes += 2.0 * sbytes;
     w.st.h2d_bytes += 2.0 * sbytes;
     if (bf16) {
@@ -556,11 +565,11 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer
     ++w.st.kernel_launches;
     stg.after_write(w.opt);
     stg.before_read(w.up);
-    check_cuda(cudaMemcpyAsync(hj.params + host_off + off, w.slot[slot] + slot_off + off, bytes,
+    check_cuda(xfer(hj.params + host_off + off, w.slot[slot] + slot_off + off, bytes,
                                cudaMemcpyDeviceToHost, w.up),
                "p d2h");
-    check_cuda(cudaMemcpyAsync(hm + hoff, sm, sbytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
-    check_cuda(cudaMemcpyAsync(hv + hoff, sv, sbytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
+    check_cuda(xfer(hm + hoff, sm, sbytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
+    check_cuda(xfer(hv + hoff, sv, sbytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
     stg.after_read(w.up);
     w.st.opt_d2h_bytes += 2.0 * sbytes;
     w.st.d2h_bytes += static_cast<double>(bytes) + 2.0 * sbytes;
@@ -685,14 +694,14 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     const long base = hy_layer_offset(&hj.m, g.l0);
     w.slot_tr[slot].before_write(w.down);
     hj.params_tr[static_cast<size_t>(s)]->before_read(w.down);
-    check_cuda(cudaMemcpyAsync(w.slot[slot], hj.params + base, sizeof(float) * static_cast<size_t>(g.param_floats),
+    check_cuda(xfer(w.slot[slot], hj.params + base, sizeof(float) * static_cast<size_t>(g.param_floats),
                                cudaMemcpyHostToDevice, w.down),
                "param h2d");
     double bytes = 4.0 * g.param_floats;
     if (g.wte_offset >= 0) {  // tied wte for a head shard without the embedding
       hj.params_tr[0]->before_read(w.down);
       const size_t wb = sizeof(float) * static_cast<size_t>(hj.m.V) * static_cast<size_t>(hj.m.d);
-      check_cuda(cudaMemcpyAsync(w.slot[slot] + g.wte_offset, hj.params, wb, cudaMemcpyHostToDevice, w.down),
+      check_cuda(xfer(w.slot[slot] + g.wte_offset, hj.params, wb, cudaMemcpyHostToDevice, w.down),
                  "wte h2d");
       hj.params_tr[0]->after_read(w.down);
       bytes += static_cast<double>(wb);
@@ -723,10 +732,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       w.last_tok = tok_i;
       w.tok_tr[tok_i].before_write(w.down);
       const size_t tb = sizeof(int32_t) * static_cast<size_t>(hj.M);
-      check_cuda(cudaMemcpyAsync(w.tok[tok_i], hj.tokens + static_cast<long>(gmb) * hj.M, tb, cudaMemcpyHostToDevice,
+      check_cuda(xfer(w.tok[tok_i], hj.tokens + static_cast<long>(gmb) * hj.M, tb, cudaMemcpyHostToDevice,
                                  w.down),
                  "tok h2d");
-      check_cuda(cudaMemcpyAsync(w.tok[tok_i] + hj.M, hj.targets + static_cast<long>(gmb) * hj.M, tb,
+      check_cuda(xfer(w.tok[tok_i] + hj.M, hj.targets + static_cast<long>(gmb) * hj.M, tb,
                                  cudaMemcpyHostToDevice, w.down),
                  "tgt h2d");
       w.tok_tr[tok_i].after_write(w.down);
@@ -751,7 +760,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       if (w.abuf_tag[0].job >= 0 && w.abuf_tag[1].job < 0) ain = 1;
       w.abuf_tr[ain].before_write(w.down);
       hj.ckpt_tr[static_cast<size_t>(s - 1)]->before_read(w.down);
-      check_cuda(cudaMemcpyAsync(w.abuf[ain], hj.ckpt[static_cast<size_t>(s - 1)], act_bytes, cudaMemcpyHostToDevice,
+      check_cuda(xfer(w.abuf[ain], hj.ckpt[static_cast<size_t>(s - 1)], act_bytes, cudaMemcpyHostToDevice,
                                  w.down),
                  "act h2d");
       hj.ckpt_tr[static_cast<size_t>(s - 1)]->after_read(w.down);
@@ -771,7 +780,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       gin = 0;
       w.gbd_tr[gin].before_write(w.down);
       hj.grad_tr[static_cast<size_t>(s)]->before_read(w.down);
-      check_cuda(cudaMemcpyAsync(w.gbd[gin], hj.grad[static_cast<size_t>(s)], act_bytes, cudaMemcpyHostToDevice,
+      check_cuda(xfer(w.gbd[gin], hj.grad[static_cast<size_t>(s)], act_bytes, cudaMemcpyHostToDevice,
                                  w.down),
                  "grad h2d");
       hj.grad_tr[static_cast<size_t>(s)]->after_read(w.down);
@@ -789,7 +798,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     if (!(w.z_tag == zt)) {
       w.z_tr.before_write(w.down);
       hj.z_tr->before_read(w.down);
-      check_cuda(cudaMemcpyAsync(w.zbuf, hj.z, act_bytes, cudaMemcpyHostToDevice, w.down), "z h2d");
+      check_cuda(xfer(w.zbuf, hj.z, act_bytes, cudaMemcpyHostToDevice, w.down), "z h2d");
       hj.z_tr->after_read(w.down);
       w.z_tr.after_write(w.down);
       w.z_tag = zt;
@@ -843,6 +852,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     skip_fwd = nx.job == j && nx.minibatch == task.t.minibatch && nx.shard == s &&
                nx.direction == Direction::kBackward;
   }
+  if (g_debug_skip == 2) skip_fwd = true;
   if (fwd && !skip_fwd) {
     hy::run_forward(w.comp, hj.m, g, w.slot[slot], io, sc);
     if (g.has_head) {
@@ -862,7 +872,20 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
     StreamingSink sink(*this, w, hj, s, slot, gmb + 1);
     sink.deferred = w.stg_alias;
-    hy::run_backward(w.comp, hj.m, g, w.slot[slot], sink, io, sc);
+    if (g_debug_skip == 2) {  // gradients "computed": only the optimizer/transfer pipeline runs
+      if (g.has_embed) sink.acquire(0);
+      if (g.has_head) {
+        sink.acquire(hj.m.L + 1);
+        sink.release(hj.m.L + 1);
+      }
+      for (int l = std::min(g.l1, hj.m.L + 1) - 1; l >= std::max(g.l0, 1); --l) {
+        sink.acquire(l);
+        sink.release(l);
+      }
+      if (g.has_embed) sink.release(0);
+    } else {
+      hy::run_backward(w.comp, hj.m, g, w.slot[slot], sink, io, sc);
+    }
     if (w.stg_alias) {
       for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // staging = scratch: after the backward
     }
@@ -905,7 +928,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     Tracked& host = *hj.ckpt_tr[static_cast<size_t>(s)];
     w.abuf_tr[aout].before_read(w.up);
     host.before_write(w.up);
-    check_cuda(cudaMemcpyAsync(hj.ckpt[static_cast<size_t>(s)], w.abuf[aout], act_bytes, cudaMemcpyDeviceToHost, w.up),
+    check_cuda(xfer(hj.ckpt[static_cast<size_t>(s)], w.abuf[aout], act_bytes, cudaMemcpyDeviceToHost, w.up),
                "act d2h");
     host.after_write(w.up);
     w.abuf_tr[aout].after_read(w.up);
@@ -916,7 +939,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     Tracked& host = *hj.grad_tr[static_cast<size_t>(s - 1)];
     w.gbd_tr[gout].before_read(w.up);
     host.before_write(w.up);
-    check_cuda(cudaMemcpyAsync(hj.grad[static_cast<size_t>(s - 1)], w.gbd[gout], act_bytes, cudaMemcpyDeviceToHost,
+    check_cuda(xfer(hj.grad[static_cast<size_t>(s - 1)], w.gbd[gout], act_bytes, cudaMemcpyDeviceToHost,
                                w.up),
                "grad d2h");
     host.after_write(w.up);
@@ -927,7 +950,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   if (!fwd && g.has_head && !g.has_embed) {  // saved ln_f output for shard 0's tied-wte grad
     w.z_tr.before_read(w.up);
     hj.z_tr->before_write(w.up);
-    check_cuda(cudaMemcpyAsync(hj.z, w.zbuf, act_bytes, cudaMemcpyDeviceToHost, w.up), "z d2h");
+    check_cuda(xfer(hj.z, w.zbuf, act_bytes, cudaMemcpyDeviceToHost, w.up), "z d2h");
     hj.z_tr->after_write(w.up);
     w.z_tr.after_read(w.up);
     w.st.d2h_bytes += static_cast<double>(act_bytes);
@@ -954,6 +977,7 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
         check_cuda(cudaSetDevice(w.cuda_dev), "set device");
         hy::gemm_set_splitk_workspace(w.splitk, w.splitk_floats);
         hy::gemm_set_precision_fp32(exec.precision_fp32);
+        g_debug_skip = exec.debug_skip;
         check_cuda(cudaDeviceSynchronize(), "pre-pass sync");
         check_cuda(cudaEventRecord(w.t0, w.comp), "t0");
         for (cudaStream_t s : {w.down, w.up, w.opt}) check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");

@@ -1,0 +1,12 @@
+"""Split a pass into link-bound and compute-bound parts (debug_skip modes)."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2110_08633_b200 as P
+cfg = json.load(open(sys.argv[1] if len(sys.argv) > 1 else "configs/c2_gpt2small_x8.json"))
+extra = json.loads(sys.argv[2]) if len(sys.argv) > 2 else {}
+for name, skip in (("full", 0), ("no-transfers", 1), ("no-compute", 2)):
+    ex = P.Executor(cfg, gpus=1, passes=2, warmup_passes=1, debug_skip=skip, **extra)
+    ex.run(1, timed=False)
+    r = ex.run(2)
+    print(name, extra, [round(x, 3) for x in r["pass_seconds"]], flush=True)
+    ex.close()
