@@ -72,6 +72,8 @@ int hy_executor_run(void* handle, int passes, int timed, int with_trace, char* o
                     size_t* needed);
 int hy_executor_dump_params(void* handle, const char* dir);
 void hy_executor_destroy(void* handle);
+/* Diagnostics: host microseconds per back-to-back launch (kind 0 GEMM, 1 LayerNorm). */
+double hy_host_launch_us(void* stream, int kind, int n, float* a, float* b, float* c);
 /* Kernel launches issued by this library since load (for the bench's gpu_launches). */
 long hy_kernel_launches(void);
 

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -47,6 +48,7 @@ struct ExecStats {
   double elided_param_bytes = 0, elided_act_bytes = 0;
   std::vector<double> arena_bytes;  // per executed device: HBM reserved (<= mem_bytes)
   std::vector<double> device_busy_s;
+  std::vector<double> enqueue_s;    // host time to enqueue a pass (per executed GPU)
   std::vector<double> pinned_bytes;
   int kernel_launches = 0;
   int elided_compute_tasks = 0;  // head-shard forwards folded into their backward
@@ -57,6 +59,7 @@ struct ExecResult {
   SimTrace trace;                              // measured, last timed pass
   std::vector<std::vector<double>> losses;     // [job][global minibatch] (executed jobs)
   std::vector<double> pass_seconds;            // per timed pass (max over devices)
+  std::map<std::string, double> op_profile_ms; // HY_PROFILE=1: compute-stream time per op (last pass)
   ExecStats stats;
 };
 

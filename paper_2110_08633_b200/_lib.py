@@ -24,6 +24,8 @@ _SIGS = {
     "hy_executor_dump_params": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
     "hy_executor_destroy": (None, [ctypes.c_void_p]),
     "hy_kernel_launches": (ctypes.c_long, []),
+    "hy_host_launch_us": (ctypes.c_double, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                            ctypes.c_void_p, ctypes.c_void_p]),
     "hy_gemm_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_long]),
     "hy_gemm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,
                                ctypes.c_int, ctypes.c_void_p, ctypes.c_long, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,

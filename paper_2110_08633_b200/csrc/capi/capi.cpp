@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -127,6 +128,24 @@ void hy_executor_destroy(void* handle) {
 }
 
 long hy_kernel_launches(void) { return hy::g_kernel_launches.load(); }
+
+// Diagnostics: host microseconds per launch of `kind` (0 = GEMM 128x128x64, 1 = LayerNorm
+// 64x64) issued back to back from C++ on `stream`, n times. Buffers are caller-provided.
+double hy_host_launch_us(void* stream, int kind, int n, float* a, float* b, float* c) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int i = 0; i < n; ++i) {
+    if (kind == 0) {
+      hy::GemmEpilogue e;
+      e.C = c;
+      e.ldc = 128;
+      hy::gemm_tf32(static_cast<cudaStream_t>(stream), 128, 128, 64, a, 64, false, b, 64, false, e);
+    } else {
+      hy::layernorm_fwd(static_cast<cudaStream_t>(stream), 64, 64, a, b, b + 64, c, c + 4096, c + 8192);
+    }
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  return std::chrono::duration<double, std::micro>(t1 - t0).count() / n;
+}
 
 int hy_gemm_config(int precision_fp32, float* splitk_ws, long splitk_floats) {
   hy::gemm_set_precision_fp32(precision_fp32 != 0);

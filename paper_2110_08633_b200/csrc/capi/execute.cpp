@@ -159,7 +159,9 @@ ojson session_result(Session& S, bool with_trace) {
   st["pinned_bytes"] = r.stats.pinned_bytes;
   st["device_busy_s_last_pass"] = r.stats.device_busy_s.empty() ? 0.0 : r.stats.device_busy_s.back();
   st["setup_s"] = r.stats.setup_s;
+  st["enqueue_s_last_pass"] = r.stats.enqueue_s.empty() ? 0.0 : r.stats.enqueue_s.back();
   out["stats"] = st;
+  if (!r.op_profile_ms.empty()) out["op_profile_ms"] = r.op_profile_ms;
   if (!r.pass_seconds.empty()) {
     out["report"] = ojson::parse(report_to_json(summarize(r.trace, S.cfg.cluster, S.strategy)));
     if (with_trace) out["chrome_trace"] = to_chrome_trace_json(r.trace);

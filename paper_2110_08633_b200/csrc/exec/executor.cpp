@@ -35,6 +35,7 @@
 #include "../kernels/gemm.cuh"
 #include "../kernels/ops.cuh"
 #include "gpt_runner.hpp"
+#include "prof.hpp"
 #include "spillsim/errors.hpp"
 
 namespace spillsim {
@@ -194,6 +195,7 @@ struct Worker {
   float* splitk = nullptr;
   long splitk_floats = 0;
   int stg_round = 0;
+  double enqueue_s = 0;
   bool opt_pending = false;
   std::vector<TaskTiming> timing;  // per local task index
   cudaEvent_t t0 = nullptr, t_end = nullptr;
@@ -981,7 +983,9 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
         check_cuda(cudaDeviceSynchronize(), "pre-pass sync");
         check_cuda(cudaEventRecord(w.t0, w.comp), "t0");
         for (cudaStream_t s : {w.down, w.up, w.opt}) check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");
+        const auto h0 = std::chrono::steady_clock::now();
         for (int t : w.tasks) enqueue_task(w, t, pass);
+        w.enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         // join all streams into comp, then record the end
         cudaStream_t others[3] = {w.down, w.up, w.opt};
         for (int k = 0; k < 3; ++k) {
@@ -1071,7 +1075,9 @@ void ExecutorImpl::collect(int pass, ExecResult& res) {
       }
     }
     res.stats.device_busy_s.push_back(busy);
+    res.stats.enqueue_s.push_back(w.enqueue_s);
   }
+  if (hy::OpProfiler::get().enabled) res.op_profile_ms = hy::OpProfiler::get().drain();
   std::sort(tr.events.begin(), tr.events.end(), [](const SimEvent& a, const SimEvent& b) {
     return std::tie(a.resource, a.start_s, a.end_s) < std::tie(b.resource, b.start_s, b.end_s);
   });

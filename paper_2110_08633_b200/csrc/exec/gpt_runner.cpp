@@ -4,6 +4,7 @@
 // compute = fwd recompute + bwd, strategies.cpp:775). Backward temporaries alias dead
 // forward intermediates, so a block needs ~12 M*d floats of scratch in total.
 #include "gpt_runner.hpp"
+#include "prof.hpp"
 
 #include <algorithm>
 #include <string>
@@ -61,15 +62,29 @@ void gemm(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a
 
 void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const float* h_in, float* h_out, Scratch& s) {
   const int M = s.M, d = m.d;
+  { HY_PROF(st, "ln1");
   check_cuda(layernorm_fwd(st, M, d, h_in, bt(w, d, HY_LN1_G), bt(w, d, HY_LN1_B), s.ln1, s.mean1, s.rstd1), "ln1");
+  }
+  { HY_PROF(st, "qkv");
   gemm(st, M, 3 * d, d, s.ln1, d, false, bt(w, d, HY_WQKV), d, false, s.qkv, 3 * d, bt(w, d, HY_BQKV));
+  }
   // scores live in the (not yet written) MLP buffers fc+act: 8*M*d floats, contiguous
+  { HY_PROF(st, "attn_fwd");
   check_cuda(attention_fwd_tc(st, m.B, m.T, m.H, s.qkv, s.att, s.fc, s.act + 4L * M * d - s.fc), "attn_fwd");
+  }
+  { HY_PROF(st, "o_proj");
   gemm(st, M, d, d, s.att, d, false, bt(w, d, HY_WO), d, false, s.hmid, d, bt(w, d, HY_BO), h_in, d);
+  }
+  { HY_PROF(st, "ln2");
   check_cuda(layernorm_fwd(st, M, d, s.hmid, bt(w, d, HY_LN2_G), bt(w, d, HY_LN2_B), s.ln2, s.mean2, s.rstd2), "ln2");
+  }
+  { HY_PROF(st, "fc");
   gemm(st, M, 4 * d, d, s.ln2, d, false, bt(w, d, HY_WFC), d, false, s.act, 4 * d, bt(w, d, HY_BFC), nullptr, 0, 0.f,
        kEpiGelu, s.fc, nullptr, 4 * d);
+  }
+  { HY_PROF(st, "mlp_proj");
   gemm(st, M, d, 4 * d, s.act, 4 * d, false, bt(w, d, HY_WPR), 4 * d, false, h_out, d, bt(w, d, HY_BPR), s.hmid, d);
+  }
 }
 
 // dh: in dL/dh_out, out dL/dh_in. Requires the intermediates of block_forward(h_in).
@@ -77,34 +92,64 @@ void block_backward(cudaStream_t st, const hy_dims& m, const float* w, float* gw
                     Scratch& s) {
   const int M = s.M, d = m.d;
   // MLP out: h_out = hmid + act Wpr^T + bpr
+  { HY_PROF(st, "bwd_dW_proj");
   gemm(st, d, 4 * d, M, dh, d, true, s.act, 4 * d, true, btw(gw, d, HY_WPR), 4 * d, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
   check_cuda(colsum(st, M, d, dh, d, btw(gw, d, HY_BPR), true, s.ws), "colsum bpr");
+  }
   float* dact = s.act;  // act is dead after dWpr
+  { HY_PROF(st, "bwd_dact");
   gemm(st, M, 4 * d, d, dh, d, false, bt(w, d, HY_WPR), 4 * d, true, dact, 4 * d, nullptr, nullptr, 0, 0.f, kEpiGeluBwd,
        nullptr, s.fc, 4 * d);
+  }
+  { HY_PROF(st, "bwd_dW_fc");
   gemm(st, 4 * d, d, M, dact, 4 * d, true, s.ln2, d, true, btw(gw, d, HY_WFC), d, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
   check_cuda(colsum(st, M, 4 * d, dact, 4 * d, btw(gw, d, HY_BFC), true, s.ws), "colsum bfc");
+  }
   float* dln2 = s.fc;  // fc dead after dact
+  { HY_PROF(st, "bwd_dln2");
   gemm(st, M, d, 4 * d, dact, 4 * d, false, bt(w, d, HY_WFC), d, true, dln2, d);
+  }
+  { HY_PROF(st, "bwd_ln");
   check_cuda(layernorm_bwd(st, M, d, s.hmid, bt(w, d, HY_LN2_G), s.mean2, s.rstd2, dln2, dh, true,
                            btw(gw, d, HY_LN2_G), btw(gw, d, HY_LN2_B), s.ws),
              "ln2 bwd");
+  }
   // attention out: hmid = h_in + att Wo^T + bo   (dh now holds dL/dhmid)
+  { HY_PROF(st, "bwd_dW_o");
   gemm(st, d, d, M, dh, d, true, s.att, d, true, btw(gw, d, HY_WO), d, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
   check_cuda(colsum(st, M, d, dh, d, btw(gw, d, HY_BO), true, s.ws), "colsum bo");
+  }
   float* datt = s.ln2;  // ln2 dead after dWfc
+  { HY_PROF(st, "bwd_datt");
   gemm(st, M, d, d, dh, d, false, bt(w, d, HY_WO), d, true, datt, d);
+  }
   // fc (dln2) and act (dact) are dead here: dqkv takes fc[0, 3Md), scores the rest of fc+act
   float* dqkv = s.fc;
   float* work = s.fc + 3L * M * d;
+  { HY_PROF(st, "attn_bwd");
   check_cuda(attention_bwd_tc(st, m.B, m.T, m.H, s.qkv, datt, dqkv, work, s.act + 4L * M * d - work), "attn bwd");
+  }
+  { HY_PROF(st, "bwd_dW_qkv");
   gemm(st, 3 * d, d, M, dqkv, 3 * d, true, s.ln1, d, true, btw(gw, d, HY_WQKV), d, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
   check_cuda(colsum(st, M, 3 * d, dqkv, 3 * d, btw(gw, d, HY_BQKV), true, s.ws), "colsum bqkv");
+  }
   float* dln1 = s.hmid;  // hmid dead after ln2 bwd
+  { HY_PROF(st, "bwd_dln1");
   gemm(st, M, d, 3 * d, dqkv, 3 * d, false, bt(w, d, HY_WQKV), d, true, dln1, d);
+  }
+  { HY_PROF(st, "bwd_ln");
   check_cuda(layernorm_bwd(st, M, d, h_in, bt(w, d, HY_LN1_G), s.mean1, s.rstd1, dln1, dh, true,
                            btw(gw, d, HY_LN1_G), btw(gw, d, HY_LN1_B), s.ws),
              "ln1 bwd");
+  }
 }
 
 // z = ln_f(h); logits chunks -> xent. want_grad: dlogits scaled by 1/M; dz, dwte (if given).
@@ -112,19 +157,29 @@ void head_pass(cudaStream_t st, const hy_dims& m, const float* lnf, const float*
                const int32_t* targets, Scratch& s, bool want_grad, float* dwte, bool z_ready = false) {
   const int M = s.M, d = m.d, V = m.V;
   if (!z_ready) {
+    { HY_PROF(st, "head_lnf");
     check_cuda(layernorm_fwd(st, M, d, h, lnf, lnf + hy_pad32(d), s.z, s.zmean, s.zrstd), "ln_f");
+    }
   }
   check_cuda(cudaMemsetAsync(s.loss, 0, sizeof(double), st), "memset loss");
   for (int r0 = 0; r0 < M; r0 += s.logits_rows) {
     const int rows = std::min(s.logits_rows, M - r0);
+    { HY_PROF(st, "head_logits");
     gemm(st, rows, V, d, s.z + static_cast<long>(r0) * d, d, false, wte, d, false, s.logits, HY_VOCAB_PAD);
+    }
+    { HY_PROF(st, "head_xent");
     check_cuda(softmax_xent(st, rows, V, s.logits, HY_VOCAB_PAD, targets + r0, 1.f / M, s.row_loss + r0), "xent");
+    }
     if (want_grad && s.dz) {
+      { HY_PROF(st, "head_dz");
       gemm(st, rows, d, V, s.logits, HY_VOCAB_PAD, false, wte, d, true, s.dz + static_cast<long>(r0) * d, d);
+      }
     }
     if (want_grad && dwte) {
+      { HY_PROF(st, "head_dwte");
       gemm(st, V, d, rows, s.logits, HY_VOCAB_PAD, true, s.z + static_cast<long>(r0) * d, d, true, dwte, d, nullptr,
            nullptr, 0, 1.f);
+      }
     }
   }
   check_cuda(sum_to_double(st, M, s.row_loss, s.loss, false), "loss sum");

@@ -38,7 +38,8 @@ struct Smem {
   static constexpr int kOpBytes = kABytes + kBBytes;
   static constexpr int kStageBytes = P3 ? 2 * kOpBytes : kOpBytes;
   static constexpr int kRing = kStagesN * kStageBytes;
-  static constexpr int kTotal = kRing + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int kEpi = 4 * 32 * 36 * 4;  // per epilogue warp: 32x32 transpose tile, row stride 36
+  static constexpr int kTotal = kRing + kEpi + 1024 /*align slack*/ + 256 /*barriers*/;
 };
 
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
@@ -106,7 +107,8 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   constexpr int kStages = L::kStagesN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kRing);
+  float* epi_smem = reinterpret_cast<float*>(smem + L::kRing);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kRing + L::kEpi);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -289,9 +291,16 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       ++local;
       tc_fence_after();
-      const int row = ti.m0 + static_cast<int>(q * 32 + lane_id());
-      const bool row_ok = row < M;
+      // Epilogue: TMEM -> registers (thread = row) -> smem transpose -> each lane takes 4
+      // consecutive columns of a row (8 lanes per 32-column row, 4 rows per instruction), so
+      // bias / residual / GELU operands and the stores move as coalesced 128-bit accesses.
+      const uint32_t lane = lane_id();
+      float* stile = epi_smem + q * (32 * 36);
+      const int row0 = ti.m0 + static_cast<int>(q * 32);
+      const int nrows = min(32, M - row0);
       float* Cb = epi.C + ti.z1 * bat.c_s1 + ti.z2 * bat.c_s2;
+      const int sub_r = static_cast<int>(lane >> 3);       // row within a group of 4
+      const int sub_c = static_cast<int>(lane & 7) * 4;    // first of this lane's 4 columns
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         float v[32];
@@ -302,59 +311,105 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
           for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
         const int col0 = ti.n0 + c * 32;
-        if (!row_ok || col0 >= N) continue;
-        const bool full_chunk = col0 + 32 <= N;
-        float* crow = Cb + static_cast<long>(row) * epi.ldc + col0;
-        if (epi.alpha != 1.f) {
+        if (nrows <= 0 || col0 >= N) continue;  // warp-uniform
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] *= epi.alpha;
+        for (int k = 0; k < 8; ++k) {
+          reinterpret_cast<float4*>(stile + lane * 36)[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
         }
-        if (epi.mode == kEpiGeluBwd) {
-          const float* hrow = epi.Hin + static_cast<long>(row) * epi.ldhi + col0;
+        __syncwarp();
+        const int col = col0 + sub_c;
+        if (col0 + 32 <= N) {
+          float4 x[8];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (full_chunk || col0 + i < N) v[i] *= gelu_tanh_grad(hrow[i]);
+          for (int it = 0; it < 8; ++it) {
+            x[it] = reinterpret_cast<const float4*>(stile + (it * 4 + sub_r) * 36 + sub_c)[0];
+          }
+          float4 aux[8];  // residual / H / previous C operand, loaded up front for ILP
+          const float* src = nullptr;
+          long lds = 0;
+          if (epi.mode == kEpiGeluBwd) {
+            src = epi.Hin;
+            lds = epi.ldhi;
+          } else if (epi.mode == kEpiStore && epi.R) {
+            src = epi.R;
+            lds = epi.ldr;
+          }
+          if (src) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = it * 4 + sub_r;
+              aux[it] = r < nrows ? *reinterpret_cast<const float4*>(src + (row0 + r) * lds + col)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          float4 prev[8];
+          const bool use_beta = epi.mode == kEpiStore && epi.beta != 0.f;
+          if (use_beta) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+              const int r = it * 4 + sub_r;
+              prev[it] = r < nrows ? *reinterpret_cast<const float4*>(Cb + (row0 + r) * epi.ldc + col)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+          float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (epi.bias && epi.mode != kEpiGeluBwd) bv = *reinterpret_cast<const float4*>(epi.bias + col);
+#pragma unroll
+          for (int it = 0; it < 8; ++it) {
+            const int r = it * 4 + sub_r;
+            if (r >= nrows) continue;
+            float* xe = &x[it].x;
+            const float* ae = &aux[it].x;
+            const float* pe = &prev[it].x;
+            const float* be = &bv.x;
+            float4 h;
+            float* he = &h.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float y = xe[e] * epi.alpha;
+              if (epi.mode == kEpiGeluBwd) {
+                y *= gelu_tanh_grad(ae[e]);
+              } else {
+                y += be[e];
+                if (epi.mode == kEpiGelu) {
+                  he[e] = y;
+                  y = gelu_tanh(y);
+                } else {
+                  if (src) y += ae[e];
+                  if (use_beta) y += epi.beta * pe[e];
+                }
+              }
+              xe[e] = y;
+            }
+            const long grow = row0 + r;
+            if (epi.mode == kEpiGelu) *reinterpret_cast<float4*>(epi.Hout + grow * epi.ldho + col) = h;
+            *reinterpret_cast<float4*>(Cb + grow * epi.ldc + col) = x[it];
           }
         } else {
-          if (epi.bias) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (full_chunk || col0 + i < N) v[i] += epi.bias[col0 + i];
-            }
-          }
-          if (epi.mode == kEpiGelu) {
-            float* hrow = epi.Hout + static_cast<long>(row) * epi.ldho + col0;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              if (full_chunk || col0 + i < N) {
-                hrow[i] = v[i];
-                v[i] = gelu_tanh(v[i]);
+          // ragged last chunk (N not a multiple of 32): scalar path, lanes over columns
+          const int colx = col0 + static_cast<int>(lane);
+          if (colx < N) {
+            const float bias_v = (epi.bias && epi.mode != kEpiGeluBwd) ? epi.bias[colx] : 0.f;
+            for (int r = 0; r < nrows; ++r) {
+              const long grow = row0 + r;
+              float y = stile[r * 36 + lane] * epi.alpha;
+              if (epi.mode == kEpiGeluBwd) {
+                y *= gelu_tanh_grad(epi.Hin[grow * epi.ldhi + colx]);
+              } else {
+                y += bias_v;
+                if (epi.mode == kEpiGelu) {
+                  epi.Hout[grow * epi.ldho + colx] = y;
+                  y = gelu_tanh(y);
+                } else {
+                  if (epi.R) y += epi.R[grow * epi.ldr + colx];
+                  if (epi.beta != 0.f) y += epi.beta * Cb[grow * epi.ldc + colx];
+                }
               }
-            }
-          } else {
-            if (epi.R) {
-              const float* rrow = epi.R + static_cast<long>(row) * epi.ldr + col0;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                if (full_chunk || col0 + i < N) v[i] += rrow[i];
-              }
-            }
-            if (epi.beta != 0.f) {
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                if (full_chunk || col0 + i < N) v[i] += epi.beta * crow[i];
-              }
+              Cb[grow * epi.ldc + colx] = y;
             }
           }
         }
-        if (full_chunk) {
-#pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            *reinterpret_cast<float4*>(crow + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          }
-        } else {
-          for (int i = 0; i < 32 && col0 + i < N; ++i) crow[i] = v[i];
-        }
+        __syncwarp();
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);

@@ -8,5 +8,15 @@ for name, skip in (("full", 0), ("no-transfers", 1), ("no-compute", 2)):
     ex = P.Executor(cfg, gpus=1, passes=2, warmup_passes=1, debug_skip=skip, **extra)
     ex.run(1, timed=False)
     r = ex.run(2)
-    print(name, extra, [round(x, 3) for x in r["pass_seconds"]], flush=True)
+    print(name, extra, [round(x, 3) for x in r["pass_seconds"]], "enqueue_s", round(r["stats"]["enqueue_s_last_pass"], 3), flush=True)
     ex.close()
+
+if os.environ.get("HY_PROFILE") == "1":
+    ex = P.Executor(cfg, gpus=1, passes=1, warmup_passes=1, **extra)
+    ex.run(1, timed=False)
+    r = ex.run(1)
+    prof = r.get("op_profile_ms", {})
+    tot = sum(prof.values())
+    print("compute-stream op profile (ms per pass), total", round(tot, 1), "pass", round(r["pass_seconds"][0], 3))
+    for k, v in sorted(prof.items(), key=lambda x: -x[1]):
+        print(f"  {k:14s} {v:9.1f} {100 * v / tot:5.1f}%")
