@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -155,9 +156,24 @@ struct Worker {
   cudaStream_t comp{}, down{}, up{}, opt{};
   char* arena = nullptr;
   long arena_bytes = 0;
-  float* slot[2] = {nullptr, nullptr};
-  Tag slot_tag[2];
-  Tracked slot_tr[2];
+  // Parameter cache: shards live anywhere in `pool` (2 x the largest shard), first-fit,
+  // evicting least-recently-used shards; a ParamLoad is skipped whenever the shard is still
+  // resident at its current version (generalises the reference's F(k-1)->B(k-1) elision).
+  struct PoolEntry {
+    Tag tag;
+    long off = 0, len = 0;
+    long last_use = -1;
+    Tracked tr;
+  };
+  float* pool = nullptr;
+  long pool_floats = 0;
+  std::list<std::unique_ptr<PoolEntry>> live, retired;
+  PoolEntry* prev_entry = nullptr;
+  long seq = 0;
+  // the embedding-gradient buffer doubles as a cache of the tied wte between F(0) and the
+  // head shard's tasks (a D2D copy instead of reloading V*d floats over the host link)
+  Tag gembed_tag;
+  Tracked gembed_tr;
   // Parameter gradients: the embedding's in its own buffer, every other layer in a ring
   // (FIFO, released as each layer's Adam finishes reading), so the optimizer streams a
   // layer's state while the backward is still working on earlier layers.
@@ -233,8 +249,9 @@ struct ExecutorImpl {
   void setup_worker(Worker& w);
   void run_pass(int pass, bool timed, ExecResult& res);
   void enqueue_task(Worker& w, int t, int pass);
-  void adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer, const float* grads, int step,
+  void adam_layer(Worker& w, HostJob& hj, int s, float* base, int layer, const float* grads, int step,
                   cudaEvent_t done);
+  Worker::PoolEntry* acquire_params(Worker& w, HostJob& hj, int j, int s, bool* loaded);
   void collect(int pass, ExecResult& res);
 };
 
@@ -249,7 +266,7 @@ ExecutorImpl::~ExecutorImpl() {
       }
     }
     for (int i = 0; i < 2; ++i) {
-      w.slot_tr[i].destroy();
+      (void)i;
       w.abuf_tr[i].destroy();
       w.gbd_tr[i].destroy();
       w.tok_tr[i].destroy();
@@ -257,6 +274,9 @@ ExecutorImpl::~ExecutorImpl() {
     for (int i = 0; i < kStaging; ++i) w.stg_tr[i].destroy();
     for (cudaEvent_t e : w.ev_pool) cudaEventDestroy(e);
     if (w.gembed_free) cudaEventDestroy(w.gembed_free);
+    for (auto& e : w.live) e->tr.destroy();
+    for (auto& e : w.retired) e->tr.destroy();
+    w.gembed_tr.destroy();
     w.z_tr.destroy();
     for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2]}) {
       if (e) cudaEventDestroy(e);
@@ -356,8 +376,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
   for (int t : w.tasks) {
     const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
     const ShardGeom& g = hj.geom[static_cast<size_t>(tasks[static_cast<size_t>(t)].t.shard)];
-    slot_f = std::max(slot_f, g.slot_floats);
-    if (g.has_embed) embed_f = std::max(embed_f, hy_layer_floats(&hj.m, 0));
+    slot_f = std::max(slot_f, g.param_floats);
+    if (g.has_embed || g.wte_offset >= 0) embed_f = std::max(embed_f, hy_layer_floats(&hj.m, 0));
     for (int l = std::max(g.l0, 1); l < g.l1; ++l) layer_f = std::max(layer_f, hy_layer_floats(&hj.m, l));
     act_f = std::max(act_f, hj.n_act);
     tok_n = std::max(tok_n, hj.M);
@@ -413,8 +433,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
     p += hy_pad32(n);
     return r;
   };
-  w.slot[0] = take(slot_f);
-  w.slot[1] = take(slot_f);
+  w.pool = take(2 * hy_pad32(slot_f));
+  w.pool_floats = 2 * hy_pad32(slot_f);
   w.gembed = embed_f > 0 ? take(embed_f) : nullptr;
   w.ring = take(ring_f);
   w.ring_floats = ring_f;
@@ -521,7 +541,7 @@ float lr_of(const ExecJob& j) { return j.lr; }
 // Fused Adam for one layer of shard s, on the opt stream, as soon as its gradient is final:
 // m, v chunks H2D -> adam (params updated in place in the slot) -> params, m, v D2H (up).
 // `done` is recorded once Adam no longer reads `grads`.
-void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer, const float* grads, int step,
+void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int layer, const float* grads, int step,
                               cudaEvent_t done) {
   const ShardGeom& g = hj.geom[static_cast<size_t>(s)];
   const long host_off = hy_layer_offset(&hj.m, layer);
@@ -556,18 +576,18 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, int slot, int layer
     w.st.opt_h2d_bytes += 2.0 * sbytes;
     w.st.h2d_bytes += 2.0 * sbytes;
     if (bf16) {
-      check_cuda(hy::adam_update_bf16(w.opt, n, w.slot[slot] + slot_off + off, grads + off,
+      check_cuda(hy::adam_update_bf16(w.opt, n, base + slot_off + off, grads + off,
                                       reinterpret_cast<uint16_t*>(sm), reinterpret_cast<uint16_t*>(sv), h),
                  "adam bf16");
     } else {
-      check_cuda(hy::adam_update(w.opt, n, w.slot[slot] + slot_off + off, grads + off, reinterpret_cast<float*>(sm),
+      check_cuda(hy::adam_update(w.opt, n, base + slot_off + off, grads + off, reinterpret_cast<float*>(sm),
                                  reinterpret_cast<float*>(sv), h),
                  "adam");
     }
     ++w.st.kernel_launches;
     stg.after_write(w.opt);
     stg.before_read(w.up);
-    check_cuda(xfer(hj.params + host_off + off, w.slot[slot] + slot_off + off, bytes,
+    check_cuda(xfer(hj.params + host_off + off, base + slot_off + off, bytes,
                                cudaMemcpyDeviceToHost, w.up),
                "p d2h");
     check_cuda(xfer(hm + hoff, sm, sbytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
@@ -587,17 +607,20 @@ struct StreamingSink : hy::GradSink {
   ExecutorImpl& ex;
   Worker& w;
   HostJob& hj;
-  int s, slot, step;
+  int s;
+  float* base;
+  int step;
   std::map<int, float*> live;
 
-  StreamingSink(ExecutorImpl& e, Worker& wk, HostJob& h, int shard, int sl, int st)
-      : ex(e), w(wk), hj(h), s(shard), slot(sl), step(st) {}
+  StreamingSink(ExecutorImpl& e, Worker& wk, HostJob& h, int shard, float* b, int st)
+      : ex(e), w(wk), hj(h), s(shard), base(b), step(st) {}
 
   float* acquire(int layer) override {
     const long len = hy_pad32(hy_layer_floats(&hj.m, layer));
     float* p;
     if (layer == 0) {
-      check_cuda(cudaStreamWaitEvent(w.comp, w.gembed_free, 0), "gembed wait");
+      w.gembed_tr.before_write(w.comp);
+      w.gembed_tag = Tag{};  // no longer a wte cache
       p = w.gembed;
     } else {
       if (w.ring_head + len > w.ring_floats) w.ring_head = 0;
@@ -618,6 +641,7 @@ struct StreamingSink : hy::GradSink {
       w.ring_live.push_back(Worker::RingEntry{lo, len, nullptr});
     }
     check_cuda(cudaMemsetAsync(p, 0, sizeof(float) * static_cast<size_t>(len), w.comp), "zero grads");
+    if (layer == 0) w.gembed_tr.after_write(w.comp);
     live[layer] = p;
     return p;
   }
@@ -643,18 +667,79 @@ struct StreamingSink : hy::GradSink {
   void emit(int layer) {
     float* p = live.at(layer);
     cudaEvent_t done = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
-    if (layer == 0) {
-      done = w.gembed_free;
-    } else {
+    if (layer != 0) {
       for (auto& e : w.ring_live) {
         if (w.ring + e.off == p) e.done = done;
       }
     }
-    ex.adam_layer(w, hj, s, slot, layer, p, step, done);
+    if (layer == 0) w.gembed_tr.before_read(w.opt);
+    ex.adam_layer(w, hj, s, base, layer, p, step, done);
+    if (layer == 0) w.gembed_tr.after_read(w.opt);
   }
 };
 
 }  // namespace
+
+// Resident entry for (job, shard, current version), loading it (first-fit into the pool,
+// evicting least-recently-used shards other than the previous task's) when absent.
+Worker::PoolEntry* ExecutorImpl::acquire_params(Worker& w, HostJob& hj, int j, int s, bool* loaded) {
+  const ShardGeom& g = hj.geom[static_cast<size_t>(s)];
+  const Tag want{j, -1, s, hj.version[static_cast<size_t>(s)]};
+  for (auto& e : w.live) {
+    if (e->tag == want) {
+      e->last_use = w.seq;
+      *loaded = false;
+      return e.get();
+    }
+  }
+  const long len = hy_pad32(g.param_floats);
+  auto find_gap = [&]() -> long {
+    std::vector<std::pair<long, long>> used;
+    for (auto& e : w.live) used.emplace_back(e->off, e->off + e->len);
+    std::sort(used.begin(), used.end());
+    long cur = 0;
+    for (auto& u : used) {
+      if (u.first - cur >= len) return cur;
+      cur = std::max(cur, u.second);
+    }
+    return w.pool_floats - cur >= len ? cur : -1;
+  };
+  long off = find_gap();
+  while (off < 0) {
+    auto victim = w.live.end();
+    for (auto it = w.live.begin(); it != w.live.end(); ++it) {
+      if (it->get() == w.prev_entry) continue;
+      if (victim == w.live.end() || (*it)->last_use < (*victim)->last_use) victim = it;
+    }
+    if (victim == w.live.end()) {  // only the previous task's shard is left: evict it too
+      for (auto it = w.live.begin(); it != w.live.end(); ++it) victim = it;
+    }
+    if (victim == w.live.end()) throw InvalidArgument("parameter pool smaller than a shard");
+    w.retired.splice(w.retired.end(), w.live, victim);
+    off = find_gap();
+  }
+  auto ent = std::make_unique<Worker::PoolEntry>();
+  ent->tag = want;
+  ent->off = off;
+  ent->len = len;
+  ent->last_use = w.seq;
+  // the new region may still be read/written by evicted shards' pending work
+  for (auto it = w.retired.begin(); it != w.retired.end();) {
+    Worker::PoolEntry& r = **it;
+    if (r.off < off + len && off < r.off + r.len) {
+      r.tr.before_write(w.down);
+      if (r.off >= off && r.off + r.len <= off + len) {
+        r.tr.destroy();
+        it = w.retired.erase(it);
+        continue;
+      }
+    }
+    ++it;
+  }
+  *loaded = true;
+  w.live.push_back(std::move(ent));
+  return w.live.back().get();
+}
 
 void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   const SimTask& task = tasks[static_cast<size_t>(t)];
@@ -682,42 +767,44 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   w.st.model_d2h_bytes += task.t.activation_out_bytes + task.t.grad_offload_bytes;
 
   // ---- ParamLoad (down) -----------------------------------------------------------
-  // A head shard without the embedding carries a copy of the tied wte: its content also
-  // depends on shard 0's version (updated by B(0)'s Adam).
-  const int wte_ver = g.wte_offset >= 0 ? hj.version[0] : -1;
-  const Tag want{j, wte_ver, s, hj.version[static_cast<size_t>(s)]};
-  int slot = -1;
-  for (int i = 0; i < 2; ++i) {
-    if (w.slot_tag[i] == want) slot = i;
-  }
+  ++w.seq;
   check_cuda(cudaEventRecord(tm.pl0, w.down), "pl0");
-  if (slot < 0) {
-    slot = w.last_slot < 0 ? 0 : 1 - w.last_slot;
+  bool loaded = false;
+  Worker::PoolEntry* pe = acquire_params(w, hj, j, s, &loaded);
+  float* pbase = w.pool + pe->off;
+  if (loaded) {
     const long base = hy_layer_offset(&hj.m, g.l0);
-    w.slot_tr[slot].before_write(w.down);
+    pe->tr.before_write(w.down);
     hj.params_tr[static_cast<size_t>(s)]->before_read(w.down);
-    check_cuda(xfer(w.slot[slot], hj.params + base, sizeof(float) * static_cast<size_t>(g.param_floats),
-                               cudaMemcpyHostToDevice, w.down),
+    check_cuda(xfer(pbase, hj.params + base, sizeof(float) * static_cast<size_t>(g.param_floats),
+                    cudaMemcpyHostToDevice, w.down),
                "param h2d");
-    double bytes = 4.0 * g.param_floats;
-    if (g.wte_offset >= 0) {  // tied wte for a head shard without the embedding
-      hj.params_tr[0]->before_read(w.down);
-      const size_t wb = sizeof(float) * static_cast<size_t>(hj.m.V) * static_cast<size_t>(hj.m.d);
-      check_cuda(xfer(w.slot[slot] + g.wte_offset, hj.params, wb, cudaMemcpyHostToDevice, w.down),
-                 "wte h2d");
-      hj.params_tr[0]->after_read(w.down);
-      bytes += static_cast<double>(wb);
-    }
     hj.params_tr[static_cast<size_t>(s)]->after_read(w.down);
-    w.slot_tr[slot].after_write(w.down);
-    w.slot_tag[slot] = want;
-    w.st.param_h2d_bytes += bytes;
-    w.st.h2d_bytes += bytes;
+    pe->tr.after_write(w.down);
+    w.st.param_h2d_bytes += 4.0 * g.param_floats;
+    w.st.h2d_bytes += 4.0 * g.param_floats;
   } else {
     w.st.elided_param_bytes += task.t.param_load_bytes;
   }
+  // Head shard without the embedding: the tied wte comes from the gembed cache (filled by a
+  // D2D copy at F(0)); reload it over the link only if the cache is stale or missing.
+  const float* wte_ext = nullptr;
+  if (g.wte_offset >= 0) {
+    const Tag wt{j, -1, -2, hj.version[0]};
+    if (!(w.gembed_tag == wt)) {
+      w.gembed_tr.before_write(w.down);
+      hj.params_tr[0]->before_read(w.down);
+      const size_t wb = sizeof(float) * static_cast<size_t>(hj.m.V) * static_cast<size_t>(hj.m.d);
+      check_cuda(xfer(w.gembed, hj.params, wb, cudaMemcpyHostToDevice, w.down), "wte h2d");
+      hj.params_tr[0]->after_read(w.down);
+      w.gembed_tr.after_write(w.down);
+      w.gembed_tag = wt;
+      w.st.param_h2d_bytes += static_cast<double>(wb);
+      w.st.h2d_bytes += static_cast<double>(wb);
+    }
+    wte_ext = w.gembed;
+  }
   check_cuda(cudaEventRecord(tm.pl1, w.down), "pl1");
-  w.last_slot = slot;
 
   // ---- ActPromote (down): tokens, boundary activation / checkpoint, grad_in, z --------
   check_cuda(cudaEventRecord(tm.pr0, w.down), "pr0");
@@ -817,7 +904,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   if (w.stg_alias) {
     for (int i = 0; i < kStaging; ++i) w.stg_tr[i].before_write(w.comp);  // scratch reused as staging
   }
-  w.slot_tr[slot].before_read(w.comp);
+  pe->tr.before_read(w.comp);
+  if (wte_ext) w.gembed_tr.before_read(w.comp);
   if (need_tokens) w.tok_tr[tok_i].before_read(w.comp);
   if (ain >= 0) w.abuf_tr[ain].before_read(w.comp);
   if (gin >= 0) w.gbd_tr[gin].before_read(w.comp);
@@ -843,6 +931,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     }
     if (needs_z) io.z_in = w.zbuf;
   }
+  io.wte = wte_ext;
   // targets live in the second half of the token buffer ([tokens | targets], 2*M ints)
   io.targets = need_tokens ? w.tok[tok_i] + hj.M : nullptr;
   // F of the head shard has no boundary output: when its B follows on this GPU (always
@@ -856,7 +945,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   }
   if (g_debug_skip == 2) skip_fwd = true;
   if (fwd && !skip_fwd) {
-    hy::run_forward(w.comp, hj.m, g, w.slot[slot], io, sc);
+    hy::run_forward(w.comp, hj.m, g, pbase, io, sc);
     if (g.has_head) {
       check_cuda(cudaMemcpyAsync(w.loss_dev + local, sc.loss, sizeof(double), cudaMemcpyDeviceToDevice, w.comp),
                  "loss copy");
@@ -872,7 +961,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     ptr.before_write(w.up);
     mvt.before_write(w.up);
     check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
-    StreamingSink sink(*this, w, hj, s, slot, gmb + 1);
+    StreamingSink sink(*this, w, hj, s, pbase, gmb + 1);
     sink.deferred = w.stg_alias;
     if (g_debug_skip == 2) {  // gradients "computed": only the optimizer/transfer pipeline runs
       if (g.has_embed) sink.acquire(0);
@@ -886,7 +975,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       }
       if (g.has_embed) sink.release(0);
     } else {
-      hy::run_backward(w.comp, hj.m, g, w.slot[slot], sink, io, sc);
+      hy::run_backward(w.comp, hj.m, g, pbase, sink, io, sc);
     }
     if (w.stg_alias) {
       for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // staging = scratch: after the backward
@@ -895,8 +984,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     mvt.after_read(w.opt);
     ptr.after_write(w.up);
     mvt.after_write(w.up);
-    w.slot_tr[slot].after_write(w.opt);  // Adam rewrote the params in place
-    w.slot_tr[slot].after_read(w.up);    // ... and the up stream wrote them back
+    pe->tr.after_write(w.opt);  // Adam rewrote the params in place
+    pe->tr.after_read(w.up);    // ... and the up stream wrote them back
     w.opt_pending = true;
     if (g.has_head && !g.has_embed) {
       w.z_tr.before_write(w.comp);
@@ -910,7 +999,20 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     }
   }
   check_cuda(cudaEventRecord(tm.c1, w.comp), "c1");
-  w.slot_tr[slot].after_read(w.comp);
+  pe->tr.after_read(w.comp);
+  if (wte_ext) w.gembed_tr.after_read(w.comp);
+  // F(0) of a job whose head shard lacks the embedding: cache the (current) wte in gembed
+  if (fwd && g.has_embed && !g.has_head && hj.geom.back().wte_offset >= 0 && w.gembed) {
+    const Tag wt{j, -1, -2, hj.version[0]};
+    if (!(w.gembed_tag == wt)) {
+      w.gembed_tr.before_write(w.comp);
+      check_cuda(cudaMemcpyAsync(w.gembed, pbase, sizeof(float) * static_cast<size_t>(hj.m.V) * hj.m.d,
+                                 cudaMemcpyDeviceToDevice, w.comp),
+                 "wte cache");
+      w.gembed_tr.after_write(w.comp);
+      w.gembed_tag = wt;
+    }
+  }
   if (need_tokens) w.tok_tr[tok_i].after_read(w.comp);
   if (ain >= 0) w.abuf_tr[ain].after_read(w.comp);
   if (gin >= 0) w.gbd_tr[gin].after_read(w.comp);
@@ -960,8 +1062,9 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   check_cuda(cudaEventRecord(tm.d1, w.up), "d1");
   if (!fwd) {
     hj.version[static_cast<size_t>(s)] += 1;
-    w.slot_tag[slot] = Tag{j, g.wte_offset >= 0 ? hj.version[0] : -1, s, hj.version[static_cast<size_t>(s)]};
+    pe->tag = Tag{j, -1, s, hj.version[static_cast<size_t>(s)]};
   }
+  w.prev_entry = pe;
   {
     std::lock_guard<std::mutex> lk(flag_mu);
     enqueued_pass[static_cast<size_t>(t)] = pass;

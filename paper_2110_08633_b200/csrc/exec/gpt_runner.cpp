@@ -260,7 +260,7 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
     cur = dst;
   }
   if (g.has_head) {
-    const float* wte = g.has_embed ? slot : slot + g.wte_offset;
+    const float* wte = g.has_embed ? slot : (io.wte ? io.wte : slot + g.wte_offset);
     head_pass(st, m, slot + lo(m, m.L + 1, g.l0), wte, cur, io.targets, s, false, nullptr);
   } else if (write_out && cur != io.act_out) {
     check_cuda(cudaMemcpyAsync(io.act_out, cur, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "act copy");
@@ -292,7 +292,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   if (g.has_head) {
     const float* lnf = slot + lo(m, m.L + 1, g.l0);
     float* glnf = sink.acquire(m.L + 1);
-    const float* wte = g.has_embed ? slot : slot + g.wte_offset;
+    const float* wte = g.has_embed ? slot : (io.wte ? io.wte : slot + g.wte_offset);
     float* dwte = g.has_embed ? gembed : nullptr;  // otherwise deferred to shard 0 via z
     const float* hfin = s.stash + nb * n;
     head_pass(st, m, lnf, wte, hfin, io.targets, s, true, dwte);

@@ -50,6 +50,7 @@ struct TaskIO {
   const float* grad_in = nullptr;    // dL/d act_out (backward, no head)
   float* grad_out = nullptr;         // dL/d act_in (backward, l0 > 0)
   const float* z_in = nullptr;       // saved ln_f output for the deferred tied-wte grad (B of shard 0)
+  const float* wte = nullptr;        // tied wte for a head shard without the embedding
 };
 
 // Forward task: leaves the loss (when the shard has the head) in s.loss[0].
