@@ -104,3 +104,11 @@ def test_dispatch_hash_matches_plan(tmp_path):
     cfg = tiny_config()
     res = P.execute(cfg)
     assert res["dispatch_hash"] == P.plan(cfg)["dispatch_hash"]
+
+
+def test_wide_model_gptj_dims(tmp_path):
+    """d_model 4096 (64 heads: the GPT-J-dims C4 layer shape) through a split shard chain:
+    exercises the wide LayerNorm path, 64-head attention, and large weight GEMMs."""
+    cfg = tiny_config(mem=2.5e9, n_blocks=2, d=4096, T=64, B=1, mbs=2, jobs=1)
+    res = compare(cfg, tmp_path, precision="fp32", loss_tol=1e-5, param_tol=1e-4)
+    assert len(res["shard_starts"][0]) >= 2
