@@ -29,6 +29,9 @@ $(B)/%.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
+# host optimizer: vectorised AdamW (sqrt without errno so it vectorises)
+$(B)/exec/host_opt.o: CXXFLAGS += -O3 -fno-math-errno
+
 $(B)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)

@@ -199,7 +199,8 @@ def run_hydra(args, cfg):
     device_ids = [0] * n
     device_ids[rank] = local if world > 1 else 0
     req = dict(strategy="sharp", gpus=n, run_devices=[rank], device_ids=device_ids,
-               passes=args.steps, warmup_passes=args.warmup)
+               passes=args.steps, warmup_passes=args.warmup, host_opt_fraction=args.host_opt_fraction,
+               opt_state=args.opt_state)
     t_setup = time.perf_counter()
     ex = P.Executor(cfg, **req)
     setup_s = time.perf_counter() - t_setup
@@ -251,11 +252,12 @@ def run_hydra(args, cfg):
         "vs_baseline": None,
         "dtype": "fp32 (tf32 tensor-core GEMMs)",
         "data": "synthetic tokens (splitmix64), GPT-2 random init",
-        "config": workload_desc(cfg, args.config),
+        "config": dict(workload_desc(cfg, args.config), host_opt_fraction=args.host_opt_fraction,
+                       opt_state=args.opt_state),
         "e2e": {"value": round(samples / wall, 3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "note": "host wall clock around the public hy_executor_run call; every step moves params, "
-                        "optimizer state, activations and tokens host->HBM and results back"},
+                        "optimizer state, activations and tokens host->HBM and results back (losses read back per step)"},
         "gpu_launches": int(launches_t),
         "clocks": cl,
         "plan": {"dispatch_hash": res["dispatch_hash"], "virtual_makespan_s": res["virtual_makespan_s"],
@@ -353,6 +355,11 @@ def main():
     ap.add_argument("--impl", default="hydra", choices=["hydra", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # optimizer placement (the reference keeps optimizer state host-side): the
+    # fraction of each job's params updated by the host; the rest stream their fp32 moments
+    # through HBM and are updated on the GPU
+    ap.add_argument("--host-opt-fraction", type=float, default=0.3)
+    ap.add_argument("--opt-state", default="fp32", choices=["fp32", "bf16"])
     args = ap.parse_args()
     cfg = load_config(args.config)
     if args.impl == "reference":

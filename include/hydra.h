@@ -116,6 +116,17 @@ int hy_softmax_xent(void* stream, int rows, int V, float* logits, long ldl, cons
 int hy_bias_grad(void* stream, int M, int N, const float* dy, long ldy, float* db, int accumulate, float* ws);
 int hy_adam(void* stream, long n, float* p, const float* g, float* m, float* v, float lr, float beta1, float beta2,
             float eps, float weight_decay, int step);
+/* AdamW with the optimizer state in pinned host memory (zero-copy, the executor's GPU-side
+ * optimizer): p (HBM) updated in place and mirrored to p_host; m, v (fp32, or bf16 bit
+ * patterns when bf16_state) read and written over the host link. grid = CTAs (0: default). */
+int hy_adam_host_state(void* stream, long n, float* p, const float* g, void* m_host, void* v_host, float* p_host,
+                       float lr, float beta1, float beta2, float eps, float weight_decay, int step, int bf16_state,
+                       int grid);
+/* Host-side AdamW on host memory (the reference's optimizer placement; the
+ * executor's host_opt_fraction path): same update as hy_adam, on `threads` host threads
+ * (0: all cores). bf16_state != 0: m, v are bf16 bit patterns (uint16), rounded RNE. */
+int hy_host_adam(long n, float* p, const float* g, void* m, void* v, float lr, float beta1, float beta2, float eps,
+                 float weight_decay, int step, int bf16_state, int threads);
 
 #ifdef __cplusplus
 }

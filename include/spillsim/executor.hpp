@@ -35,9 +35,17 @@ struct ExecOptions {
   bool opt_state_bf16 = false;       // Adam moments stored/streamed as bf16 (halves their link bytes)
   std::string params_out_dir;      // if set: final params of every executed job as job<j>.f32
   bool precision_fp32 = false;     // GEMMs as 3xTF32 (~fp32) instead of TF32
-  double hbm_slack_bytes = 0;
-  int debug_skip = 0;              // diagnostics: 1 skip host<->device copies, 2 skip shard compute      // physical arena may exceed mem_bytes by this much (toy configs
+  double hbm_slack_bytes = 0;      // physical arena may exceed mem_bytes by this much (toy configs
                                    // whose cost model leaves no room for real activations)
+  int debug_skip = 0;              // diagnostics: 1 skip host<->device copies, 2 skip shard compute
+  // Optimizer placement. The reference keeps optimizer state in host DRAM and updates it
+  // host-side: a host-placed layer moves only its gradient (D2H) and its next
+  // ParamLoad over the link, at 28 B/param of host DRAM traffic. GPU-placed layers stream their
+  // moments through HBM instead (no host compute, 16 B/param more on the link). This is the
+  // fraction of every job's parameters updated host-side (layers chosen from the shards that
+  // are reloaded anyway, head side first); 0 = all on the GPU.
+  double host_opt_fraction = 0;
+  int host_opt_threads = 0;        // OpenMP threads of the host optimizer (0: cores - 4)
 };
 
 struct ExecStats {
@@ -46,6 +54,8 @@ struct ExecStats {
   double model_h2d_bytes = 0, model_d2h_bytes = 0;  // cost-model bytes of the executed tasks
   double param_h2d_bytes = 0, opt_h2d_bytes = 0, opt_d2h_bytes = 0, act_h2d_bytes = 0, act_d2h_bytes = 0;
   double elided_param_bytes = 0, elided_act_bytes = 0;
+  double host_opt_params = 0;       // parameter updates done host-side
+  double host_grad_d2h_bytes = 0, refresh_h2d_bytes = 0;  // their GradOffload / resident-slot refresh
   std::vector<double> arena_bytes;  // per executed device: HBM reserved (<= mem_bytes)
   std::vector<double> device_busy_s;
   std::vector<double> enqueue_s;    // host time to enqueue a pass (per executed GPU)

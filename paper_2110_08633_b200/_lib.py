@@ -44,6 +44,10 @@ _SIGS = {
                                     ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
     "hy_adam": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_void_p] * 4
                 + [ctypes.c_float] * 5 + [ctypes.c_int]),
+    "hy_adam_host_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_void_p] * 5
+                           + [ctypes.c_float] * 5 + [ctypes.c_int] * 3),
+    "hy_host_adam": (ctypes.c_int, [ctypes.c_long] + [ctypes.c_void_p] * 4 + [ctypes.c_float] * 5
+                     + [ctypes.c_int] * 3),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -8,10 +8,12 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 
 #include "../kernels/gemm.cuh"
 #include "../kernels/launch_count.cuh"
 #include "../kernels/ops.cuh"
+#include "../exec/host_opt.hpp"
 #include "capi_internal.hpp"
 #include "spillsim/errors.hpp"
 
@@ -230,6 +232,41 @@ int hy_adam(void* stream, long n, float* p, const float* g, float* m, float* v, 
   h.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta1), step));
   h.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta2), step));
   return cuda_status(hy::adam_update(static_cast<cudaStream_t>(stream), n, p, g, m, v, h), "hy_adam");
+}
+
+int hy_adam_host_state(void* stream, long n, float* p, const float* g, void* m_host, void* v_host, float* p_host,
+                       float lr, float beta1, float beta2, float eps, float weight_decay, int step, int bf16_state,
+                       int grid) {
+  hy::AdamHyper h{lr, beta1, beta2, eps, weight_decay, 0.f, 0.f};
+  h.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta1), step));
+  h.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta2), step));
+  return cuda_status(hy::adam_zc(static_cast<cudaStream_t>(stream), n, p, g, m_host, v_host, p_host, bf16_state != 0,
+                                 h, nullptr, 0, 0, grid),
+                     "hy_adam_host_state");
+}
+
+int hy_host_adam(long n, float* p, const float* g, void* m, void* v, float lr, float beta1, float beta2, float eps,
+                 float weight_decay, int step, int bf16_state, int threads) {
+  if (n < 0 || (n > 0 && (!p || !g || !m || !v)) || step < 1) {
+    return hy::set_error(HY_E_INVALID, "hy_host_adam: bad arguments");
+  }
+  hy::HostAdamWork w;
+  w.p = p;
+  w.g = g;
+  w.m = m;
+  w.v = v;
+  w.n = n;
+  w.lr = lr;
+  w.beta1 = beta1;
+  w.beta2 = beta2;
+  w.eps = eps;
+  w.weight_decay = weight_decay;
+  w.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta1), step));
+  w.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(beta2), step));
+  w.bf16 = bf16_state;
+  w.threads = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+  hy::host_adam(w);
+  return HY_OK;
 }
 
 }  // extern "C"

@@ -1,11 +1,13 @@
 // Plan-mode B200 executor: replays the virtual engine's dispatch plan on real GPUs.
 //
-// One host worker thread per GPU enqueues its task list asynchronously on four streams:
+// One host worker thread per GPU enqueues its task list asynchronously on five streams:
 //   down    ParamLoad + ActPromote  (H2D, pinned host -> HBM; the reference's down channel)
-//   comp    shard forward / recompute+backward / fused Adam (sm_100a kernels)
-//   up      ActDemote + GradOffload (D2H; updated params + optimizer state write-back)
-//   opt     optimizer-state promote (Adam m,v chunks, H2D) — kept off the down FIFO so the
-//           next shard's prefetch is never queued behind it
+//   comp    shard forward / recompute+backward (sm_100a kernels)
+//   up      ActDemote (D2H) + the gradients of host-placed layers (GradOffload)
+//   opt     GPU-placed AdamW: zero-copy kernels that read m, v from pinned host memory and
+//           write params, m, v back over the link, layer by layer as the backward releases
+//           them (the reference folds the optimizer into GradOffload)
+//   hopt    host-placed AdamW (cudaLaunchHostFunc, OpenMP) after the gradient's D2H
 // Double buffering falls out of the stream structure: task t+1's ParamLoad is enqueued right
 // after task t's compute and runs on the copy engine while t computes (slot t+1 only waits
 // for slot t-1's last reader). Every buffer shared between streams carries a hazard tracker
@@ -36,6 +38,7 @@
 #include "../kernels/gemm.cuh"
 #include "../kernels/ops.cuh"
 #include "gpt_runner.hpp"
+#include "host_opt.hpp"
 #include "prof.hpp"
 #include "spillsim/errors.hpp"
 
@@ -45,11 +48,11 @@ namespace {
 using hy::check_cuda;
 using hy::ShardGeom;
 
-constexpr int kStaging = 4;
-
 // Diagnostics only (ExecOptions::debug_skip): 1 = skip host<->device copies, 2 = skip the
 // shard compute — to split a pass into its link-bound and compute-bound parts.
 int g_debug_skip = 0;
+
+constexpr int kStaging = 4;
 
 cudaError_t xfer(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
   if (g_debug_skip == 1 && (kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost)) return cudaSuccess;
@@ -134,6 +137,11 @@ struct HostJob {
   std::vector<std::unique_ptr<Tracked>> params_tr, mv_tr, ckpt_tr, grad_tr;
   std::unique_ptr<Tracked> z_tr;
   std::vector<int> version;  // per shard: Adam updates applied
+  // host-placed optimizer (ExecOptions::host_opt_fraction)
+  std::vector<char> host_layer;                      // per layer: AdamW runs host-side
+  float* hgrad = nullptr;                            // pinned gradients of host layers
+  std::vector<std::unique_ptr<Tracked>> hgrad_tr;    // per layer
+  std::vector<std::unique_ptr<Tracked>> hparams_tr;  // per shard: host-side writes of params
 };
 
 struct TaskTiming {
@@ -153,7 +161,8 @@ struct Worker {
   ExecutorImpl* ex = nullptr;
   int plan_dev = 0, cuda_dev = 0;
   std::vector<int> tasks;  // plan order
-  cudaStream_t comp{}, down{}, up{}, opt{};
+  cudaStream_t comp{}, down{}, up{}, opt{}, opt2{}, hopt{};
+  cudaEvent_t dense_done = nullptr;  // opt2: the embedding's early (non-token rows) update
   char* arena = nullptr;
   long arena_bytes = 0;
   // Parameter cache: shards live anywhere in `pool` (2 x the largest shard), first-fit,
@@ -164,6 +173,7 @@ struct Worker {
     long off = 0, len = 0;
     long last_use = -1;
     Tracked tr;
+    std::vector<int> dirty;  // layers updated host-side since the slot was filled
   };
   float* pool = nullptr;
   long pool_floats = 0;
@@ -202,20 +212,28 @@ struct Worker {
   Tracked tok_tr[2];
   float* stg[kStaging] = {nullptr, nullptr, nullptr, nullptr};
   Tracked stg_tr[kStaging];
+  bool stg_alias = false;
+  long stg_chunk = 0;
+  int stg_round = 0;
+  // embedding optimizer split (B of the embedding shard): rows touched by the minibatch's
+  // tokens (+ wpe) are updated after the embedding scatter from a compact stash, all other
+  // wte rows early, while the blocks back-propagate
+  int* rowidx = nullptr;   // [V + T]
+  int* rowlist = nullptr;  // [M + T]
+  int* rowcount = nullptr;
+  float* cbuf = nullptr;   // compact p | m | v of those rows
+  long crow_max = 0;
+  Tracked rowidx_tr, cbuf_tr;
   float* scratch = nullptr;
   double* loss_dev = nullptr;  // per task slot
   int last_slot = -1;
   int last_tok = 1;
-  bool stg_alias = false;
-  long stg_chunk = 0;
   float* splitk = nullptr;
   long splitk_floats = 0;
-  int stg_round = 0;
   double enqueue_s = 0;
-  bool opt_pending = false;
   std::vector<TaskTiming> timing;  // per local task index
   cudaEvent_t t0 = nullptr, t_end = nullptr;
-  cudaEvent_t join[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t join[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   ExecStats st;  // per pass accumulation (bytes)
 };
 
@@ -232,6 +250,7 @@ struct ExecutorImpl {
   std::vector<int> task_local;    // task -> local index on its worker
   std::vector<int> task_device;   // task -> plan device
   int mb_per_job_max = 0;
+  int host_threads = 1;
   std::vector<int> job_mb;        // minibatches per job per pass
   double* host_loss = nullptr;    // [task] per pass (pinned)
   // cross-device ordering: task enqueued flags
@@ -250,7 +269,10 @@ struct ExecutorImpl {
   void run_pass(int pass, bool timed, ExecResult& res);
   void enqueue_task(Worker& w, int t, int pass);
   void adam_layer(Worker& w, HostJob& hj, int s, float* base, int layer, const float* grads, int step,
-                  cudaEvent_t done);
+                  cudaEvent_t done, int part = 0);
+  void host_adam_layer(Worker& w, HostJob& hj, int s, int layer, const float* grads, int step, cudaEvent_t done);
+  void param_read_begin(HostJob& hj, int s, cudaStream_t st);
+  void param_read_end(HostJob& hj, int s, cudaStream_t st);
   Worker::PoolEntry* acquire_params(Worker& w, HostJob& hj, int j, int s, bool* loaded);
   void collect(int pass, ExecResult& res);
 };
@@ -272,17 +294,19 @@ ExecutorImpl::~ExecutorImpl() {
       w.tok_tr[i].destroy();
     }
     for (int i = 0; i < kStaging; ++i) w.stg_tr[i].destroy();
+    w.rowidx_tr.destroy();
+    w.cbuf_tr.destroy();
     for (cudaEvent_t e : w.ev_pool) cudaEventDestroy(e);
     if (w.gembed_free) cudaEventDestroy(w.gembed_free);
     for (auto& e : w.live) e->tr.destroy();
     for (auto& e : w.retired) e->tr.destroy();
     w.gembed_tr.destroy();
     w.z_tr.destroy();
-    for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2]}) {
+    for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2], w.join[3], w.join[4], w.dense_done}) {
       if (e) cudaEventDestroy(e);
     }
     if (w.arena) cudaFree(w.arena);
-    for (cudaStream_t s : {w.comp, w.down, w.up, w.opt}) {
+    for (cudaStream_t s : {w.comp, w.down, w.up, w.opt, w.opt2, w.hopt}) {
       if (s) cudaStreamDestroy(s);
     }
   }
@@ -292,6 +316,8 @@ ExecutorImpl::~ExecutorImpl() {
     for (auto& t : hj.mv_tr) t->destroy();
     for (auto& t : hj.ckpt_tr) t->destroy();
     for (auto& t : hj.grad_tr) t->destroy();
+    for (auto& t : hj.hgrad_tr) t->destroy();
+    for (auto& t : hj.hparams_tr) t->destroy();
     if (hj.z_tr) hj.z_tr->destroy();
     for (void* p : {static_cast<void*>(hj.params), static_cast<void*>(hj.mom), static_cast<void*>(hj.var),
                     static_cast<void*>(hj.z), static_cast<void*>(hj.tokens), static_cast<void*>(hj.targets)}) {
@@ -299,6 +325,7 @@ ExecutorImpl::~ExecutorImpl() {
     }
     for (float* p : hj.ckpt) cudaFreeHost(p);
     for (float* p : hj.grad) cudaFreeHost(p);
+    if (hj.hgrad) cudaFreeHost(hj.hgrad);
   }
   if (host_loss) cudaFreeHost(host_loss);
 }
@@ -307,7 +334,9 @@ namespace {
 
 void* pinned(size_t bytes) {
   void* p = nullptr;
-  check_cuda(cudaHostAlloc(&p, bytes ? bytes : 4, cudaHostAllocPortable), "cudaHostAlloc");
+  // mapped: the zero-copy optimizer kernels read / write moments and params in place (UVA:
+  // the device pointer is the host pointer)
+  check_cuda(cudaHostAlloc(&p, bytes ? bytes : 4, cudaHostAllocPortable | cudaHostAllocMapped), "cudaHostAlloc");
   return p;
 }
 
@@ -348,7 +377,30 @@ void ExecutorImpl::setup_host_job(int j) {
   for (int s = 0; s < k; ++s) {
     hj.params_tr.emplace_back(new Tracked);
     hj.mv_tr.emplace_back(new Tracked);
+    hj.hparams_tr.emplace_back(new Tracked);
   }
+  // Host-placed optimizer layers: from the head-side shards down (in a SHARP chain the shards
+  // a backward task leaves behind are the ones reloaded before their next use anyway, so the
+  // host update costs the link nothing extra; shards 0 and 1 stay resident into the next
+  // minibatch's first forwards and would need a refresh), each shard's layers in the order
+  // the backward releases them (head, last block .. first block, embedding).
+  hj.host_layer.assign(static_cast<size_t>(n_layers), 0);
+  if (exec.host_opt_fraction > 0) {
+    const double target = exec.host_opt_fraction * static_cast<double>(hj.total);
+    double acc = 0;
+    for (int s = k - 1; s >= 0 && acc < target; --s) {
+      const int l0 = starts[static_cast<size_t>(s)];
+      const int l1 = s + 1 < k ? starts[static_cast<size_t>(s) + 1] : n_layers;
+      for (int l = l1 - 1; l >= l0 && acc < target; --l) {
+        const double n = static_cast<double>(hy_layer_floats(&hj.m, l));
+        if (acc + 0.5 * n > target) continue;
+        hj.host_layer[static_cast<size_t>(l)] = 1;
+        acc += n;
+      }
+    }
+    if (acc > 0) hj.hgrad = static_cast<float*>(pinned(sizeof(float) * static_cast<size_t>(hj.total)));
+  }
+  for (int l = 0; l < n_layers; ++l) hj.hgrad_tr.emplace_back(new Tracked);
   hj.version.assign(static_cast<size_t>(k), 0);
   hj.n_gmb = job_mb[static_cast<size_t>(j)] * (exec.passes + exec.warmup_passes);
   hj.tokens = static_cast<int32_t*>(pinned(sizeof(int32_t) * static_cast<size_t>(hj.M * hj.n_gmb)));
@@ -371,13 +423,20 @@ void ExecutorImpl::setup_worker(Worker& w) {
   check_cuda(cudaStreamCreateWithFlags(&w.down, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.up, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.opt, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithFlags(&w.hopt, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithFlags(&w.opt2, cudaStreamNonBlocking), "stream");
   // Size the arena from the tasks this GPU will run.
-  long slot_f = 0, embed_f = 0, layer_f = 0, act_f = 0, scratch_f = 0, tok_n = 0;
+  long slot_f = 0, embed_f = 0, layer_f = 0, act_f = 0, scratch_f = 0, tok_n = 0, idx_n = 0, list_n = 0, crow = 0;
   for (int t : w.tasks) {
     const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
     const ShardGeom& g = hj.geom[static_cast<size_t>(tasks[static_cast<size_t>(t)].t.shard)];
     slot_f = std::max(slot_f, g.param_floats);
     if (g.has_embed || g.wte_offset >= 0) embed_f = std::max(embed_f, hy_layer_floats(&hj.m, 0));
+    if (g.has_embed) {
+      idx_n = std::max(idx_n, static_cast<long>(hj.m.V) + hj.m.T);
+      list_n = std::max(list_n, hj.M + hj.m.T);
+      crow = std::max(crow, (hj.M + hj.m.T) * static_cast<long>(hj.m.d));
+    }
     for (int l = std::max(g.l0, 1); l < g.l1; ++l) layer_f = std::max(layer_f, hy_layer_floats(&hj.m, l));
     act_f = std::max(act_f, hj.n_act);
     tok_n = std::max(tok_n, hj.M);
@@ -387,10 +446,9 @@ void ExecutorImpl::setup_worker(Worker& w) {
   }
   const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(embed_f) + 5 * hy_pad32(act_f) +
                            2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
-                           hy_pad32(2 * static_cast<long>(w.tasks.size()) + 2);
+                           hy_pad32(2 * static_cast<long>(w.tasks.size()) + 2) + hy_pad32(idx_n > 0 ? 32 + idx_n + list_n : 0) +
+                           hy_pad32(3 * crow);
   const DeviceSpec& dev = cluster.devices[static_cast<size_t>(w.plan_dev)];
-  // Adam m/v staging: a dedicated ring when the HBM cap leaves room, otherwise it aliases
-  // the dead MLP activations of the scratch (then compute waits for the m/v write-back).
   const double cap = dev.mem_bytes + exec.hbm_slack_bytes;
   long budget_floats = static_cast<long>(cap / 4) - base_floats - 2048;
   // gradient ring: at least two of the largest non-embedding layers
@@ -469,6 +527,14 @@ void ExecutorImpl::setup_worker(Worker& w) {
     }
   }
   w.stg_chunk = chunk;
+  if (idx_n > 0) {
+    int* ip = reinterpret_cast<int*>(take(32 + idx_n + list_n));
+    w.rowcount = ip;
+    w.rowidx = ip + 32;
+    w.rowlist = w.rowidx + idx_n;
+    w.crow_max = crow;
+    w.cbuf = take(3 * crow);
+  }
   w.loss_dev = reinterpret_cast<double*>(take(2 * static_cast<long>(w.tasks.size()) + 2));
   check_cuda(cudaMemset(w.arena, 0, static_cast<size_t>(w.arena_bytes)), "arena memset");
   w.timing.resize(w.tasks.size());
@@ -477,6 +543,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
   }
   for (int i = 0; i < 256; ++i) w.ev_pool.push_back(new_event(false));
   w.gembed_free = new_event(false);
+  w.dense_done = new_event(false);
   w.t0 = new_event(true);
   w.t_end = new_event(true);
   for (auto& e : w.join) e = new_event(false);
@@ -521,47 +588,79 @@ void ExecutorImpl::setup(ExecResult& res) {
   }
   for (auto& w : workers) setup_worker(*w);
   host_loss = static_cast<double*>(pinned(sizeof(double) * tasks.size()));
+  host_threads = exec.host_opt_threads > 0 ? exec.host_opt_threads
+                                           : std::max(1, static_cast<int>(std::thread::hardware_concurrency()) - 4);
   enqueued_pass.assign(tasks.size(), -1);
   res.losses.assign(exec.jobs.size(), {});
   double pinned_total = 0;
   for (auto& kv : jobs) {
     const HostJob& hj = kv.second;
-    pinned_total += 3.0 * 4 * hj.total + 4.0 * hj.n_act * (2 * hj.ckpt.size() + 1) + 8.0 * hj.M * hj.n_gmb;
+    pinned_total += 3.0 * 4 * hj.total + 4.0 * hj.n_act * (2 * hj.ckpt.size() + 1) + 8.0 * hj.M * hj.n_gmb +
+                    (hj.hgrad ? 4.0 * hj.total : 0.0);
   }
   res.stats.pinned_bytes.push_back(pinned_total);
   res.stats.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
 }
 
-namespace {
-
-float lr_of(const ExecJob& j) { return j.lr; }
-
-}  // namespace
-
-// Fused Adam for one layer of shard s, on the opt stream, as soon as its gradient is final:
-// m, v chunks H2D -> adam (params updated in place in the slot) -> params, m, v D2H (up).
-// `done` is recorded once Adam no longer reads `grads`.
+// GPU-placed AdamW for one layer of shard s, as soon as its gradient is final: m, v chunks
+// H2D into the staging ring -> fused Adam (params updated in place in the slot) -> params,
+// m, v D2H on the up stream (the reference's GradOffload with the optimizer folded in,
+// SPEC.md:225). `part`: 0 = the whole layer (opt stream). Embedding split: 1 = pass A on
+// opt2, released early (release_dense) — every chunk of layer 0 is staged, untouched wte rows
+// are updated and the rows this minibatch's scatter touches are stashed compactly; 2 = pass
+// B after the scatter — the stashed rows are updated (opt) and written to the host with
+// zero-copy stores (up, behind pass A's D2H so they land last). `done` is recorded once
+// Adam no longer reads `grads`.
 void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int layer, const float* grads, int step,
-                              cudaEvent_t done) {
+                              cudaEvent_t done, int part) {
   const ShardGeom& g = hj.geom[static_cast<size_t>(s)];
   const long host_off = hy_layer_offset(&hj.m, layer);
   const long slot_off = host_off - hy_layer_offset(&hj.m, g.l0);
   const long nfl = hy_layer_floats(&hj.m, layer);
-  const long chunk = w.stg_chunk;
   const ExecJob& spec = *hj.spec;
   hy::AdamHyper h{spec.lr, spec.beta1, spec.beta2, spec.eps, spec.weight_decay, 0.f, 0.f};
   h.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta1), step));
   h.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta2), step));
+  cudaStream_t os = part == 1 ? w.opt2 : w.opt;
   // the layer's gradient is final and its params are no longer read by the compute stream
   cudaEvent_t ready = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
   check_cuda(cudaEventRecord(ready, w.comp), "layer ready");
-  check_cuda(cudaStreamWaitEvent(w.opt, ready, 0), "layer ready wait");
+  check_cuda(cudaStreamWaitEvent(os, ready, 0), "layer ready wait");
   const bool bf16 = exec.opt_state_bf16;
   const size_t es = bf16 ? 2 : 4;  // bytes per moment element
   char* hm = reinterpret_cast<char*>(hj.mom);
   char* hv = reinterpret_cast<char*>(hj.var);
-  int c = 0;
-  for (long off = 0; off < nfl; off += chunk, ++c) {
+  const int d = hj.m.d;
+  float* cp = w.cbuf;
+  char* cm = reinterpret_cast<char*>(w.cbuf + w.crow_max);
+  char* cv = cm + es * static_cast<size_t>(w.crow_max);
+  if (part == 2) {
+    check_cuda(cudaStreamWaitEvent(w.opt, w.dense_done, 0), "dense wait");
+    w.cbuf_tr.before_write(w.opt);
+    w.rowidx_tr.before_read(w.opt);
+    check_cuda(hy::adam_embed_rows(w.opt, hj.M + hj.m.T, w.rowcount, w.rowlist, d, base + slot_off, grads, cm, cv, cp,
+                                   bf16, h),
+               "adam rows");
+    ++w.st.kernel_launches;
+    w.rowidx_tr.after_read(w.opt);
+    w.cbuf_tr.after_write(w.opt);
+    if (done) check_cuda(cudaEventRecord(done, w.opt), "adam done");
+    w.cbuf_tr.before_read(w.up);
+    w.rowidx_tr.before_read(w.up);
+    check_cuda(hy::embed_rows_to_host(w.up, hj.M + hj.m.T, w.rowcount, w.rowlist, d, cp, cm, cv, hj.params + host_off,
+                                      hm + es * host_off, hv + es * host_off, bf16),
+               "rows to host");
+    ++w.st.kernel_launches;
+    w.rowidx_tr.after_read(w.up);
+    w.cbuf_tr.after_read(w.up);
+    return;
+  }
+  if (part == 1) {
+    w.cbuf_tr.before_write(w.opt2);
+    w.rowidx_tr.before_read(w.opt2);
+  }
+  const long chunk = w.stg_chunk;
+  for (long off = 0; off < nfl; off += chunk) {
     const long n = std::min(chunk, nfl - off);
     const size_t bytes = sizeof(float) * static_cast<size_t>(n);
     const size_t sbytes = es * static_cast<size_t>(n);
@@ -570,33 +669,97 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
     char* sv = sm + es * static_cast<size_t>(chunk);
     Tracked& stg = w.stg_tr[si];
     const size_t hoff = es * static_cast<size_t>(host_off + off);
-    stg.before_write(w.opt);
-    check_cuda(xfer(sm, hm + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "m h2d");
-    check_cuda(xfer(sv, hv + hoff, sbytes, cudaMemcpyHostToDevice, w.opt), "v h2d");
+    stg.before_write(os);
+    check_cuda(xfer(sm, hm + hoff, sbytes, cudaMemcpyHostToDevice, os), "m h2d");
+    check_cuda(xfer(sv, hv + hoff, sbytes, cudaMemcpyHostToDevice, os), "v h2d");
     w.st.opt_h2d_bytes += 2.0 * sbytes;
     w.st.h2d_bytes += 2.0 * sbytes;
-    if (bf16) {
-      check_cuda(hy::adam_update_bf16(w.opt, n, base + slot_off + off, grads + off,
-                                      reinterpret_cast<uint16_t*>(sm), reinterpret_cast<uint16_t*>(sv), h),
+    if (part == 1) {
+      check_cuda(hy::adam_embed_dense(os, n, off, d, w.rowidx, base + slot_off + off, grads + off, sm, sv, cm, cv,
+                                      bf16, h),
+                 "adam dense");
+    } else if (bf16) {
+      check_cuda(hy::adam_update_bf16(os, n, base + slot_off + off, grads + off, reinterpret_cast<uint16_t*>(sm),
+                                      reinterpret_cast<uint16_t*>(sv), h),
                  "adam bf16");
     } else {
-      check_cuda(hy::adam_update(w.opt, n, base + slot_off + off, grads + off, reinterpret_cast<float*>(sm),
+      check_cuda(hy::adam_update(os, n, base + slot_off + off, grads + off, reinterpret_cast<float*>(sm),
                                  reinterpret_cast<float*>(sv), h),
                  "adam");
     }
     ++w.st.kernel_launches;
-    stg.after_write(w.opt);
+    stg.after_write(os);
     stg.before_read(w.up);
-    check_cuda(xfer(hj.params + host_off + off, base + slot_off + off, bytes,
-                               cudaMemcpyDeviceToHost, w.up),
-               "p d2h");
+    check_cuda(xfer(hj.params + host_off + off, base + slot_off + off, bytes, cudaMemcpyDeviceToHost, w.up), "p d2h");
     check_cuda(xfer(hm + hoff, sm, sbytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
     check_cuda(xfer(hv + hoff, sv, sbytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
     stg.after_read(w.up);
     w.st.opt_d2h_bytes += 2.0 * sbytes;
     w.st.d2h_bytes += static_cast<double>(bytes) + 2.0 * sbytes;
   }
-  check_cuda(cudaEventRecord(done, w.opt), "adam done");
+  if (part == 1) {
+    w.rowidx_tr.after_read(w.opt2);
+    w.cbuf_tr.after_write(w.opt2);
+    check_cuda(cudaEventRecord(w.dense_done, w.opt2), "dense done");
+    return;
+  }
+  if (done) check_cuda(cudaEventRecord(done, w.opt), "adam done");
+}
+
+// Host-placed layer: GradOffload of the layer's gradient (up), then AdamW on the host
+// (hopt stream, cudaLaunchHostFunc) over the pinned master params and moments. The HBM slot
+// keeps the pre-update copy; the layer is marked dirty in the slot and refreshed from the
+// host before the slot is read again (acquire hit) — a full reload refreshes it anyway.
+void ExecutorImpl::host_adam_layer(Worker& w, HostJob& hj, int s, int layer, const float* grads, int step,
+                                   cudaEvent_t done) {
+  const long off = hy_layer_offset(&hj.m, layer);
+  const long n = hy_layer_floats(&hj.m, layer);
+  const ExecJob& spec = *hj.spec;
+  cudaEvent_t ready = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
+  check_cuda(cudaEventRecord(ready, w.comp), "layer ready");
+  check_cuda(cudaStreamWaitEvent(w.up, ready, 0), "layer ready wait");
+  Tracked& gt = *hj.hgrad_tr[static_cast<size_t>(layer)];
+  gt.before_write(w.up);
+  check_cuda(xfer(hj.hgrad + off, grads, sizeof(float) * static_cast<size_t>(n), cudaMemcpyDeviceToHost, w.up),
+             "grad d2h");
+  gt.after_write(w.up);
+  check_cuda(cudaEventRecord(done, w.up), "grad offloaded");
+  w.st.host_grad_d2h_bytes += 4.0 * n;
+  w.st.d2h_bytes += 4.0 * n;
+  w.st.host_opt_params += static_cast<double>(n);
+  Tracked& pt = *hj.hparams_tr[static_cast<size_t>(s)];
+  gt.before_read(w.hopt);
+  pt.before_write(w.hopt);
+  hy::HostAdamWork a;
+  a.p = hj.params + off;
+  a.g = hj.hgrad + off;
+  const size_t es = exec.opt_state_bf16 ? 2 : 4;
+  a.m = reinterpret_cast<char*>(hj.mom) + es * static_cast<size_t>(off);
+  a.v = reinterpret_cast<char*>(hj.var) + es * static_cast<size_t>(off);
+  a.n = n;
+  a.lr = spec.lr;
+  a.beta1 = spec.beta1;
+  a.beta2 = spec.beta2;
+  a.eps = spec.eps;
+  a.weight_decay = spec.weight_decay;
+  a.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta1), step));
+  a.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta2), step));
+  a.bf16 = exec.opt_state_bf16 ? 1 : 0;
+  a.threads = host_threads;
+  check_cuda(hy::host_adam_async(w.hopt, a), "host adam");
+  pt.after_write(w.hopt);
+  gt.after_read(w.hopt);
+}
+
+// Reads of a shard's host master params (ParamLoad, refresh, tied-wte reload) wait for both
+// writers: the GPU optimizer's write-back (up) and the host optimizer (hopt).
+void ExecutorImpl::param_read_begin(HostJob& hj, int s, cudaStream_t st) {
+  hj.params_tr[static_cast<size_t>(s)]->before_read(st);
+  hj.hparams_tr[static_cast<size_t>(s)]->before_read(st);
+}
+void ExecutorImpl::param_read_end(HostJob& hj, int s, cudaStream_t st) {
+  hj.params_tr[static_cast<size_t>(s)]->after_read(st);
+  hj.hparams_tr[static_cast<size_t>(s)]->after_read(st);
 }
 
 namespace {
@@ -610,10 +773,13 @@ struct StreamingSink : hy::GradSink {
   int s;
   float* base;
   int step;
+  const int32_t* tokens;  // device tokens of the task (embedding row flags)
   std::map<int, float*> live;
+  bool dense_done = false;       // embedding: non-token wte rows already handed to the optimizer
+  std::vector<int> host_layers;  // released to the host optimizer (slot copy now stale)
 
-  StreamingSink(ExecutorImpl& e, Worker& wk, HostJob& h, int shard, float* b, int st)
-      : ex(e), w(wk), hj(h), s(shard), base(b), step(st) {}
+  StreamingSink(ExecutorImpl& e, Worker& wk, HostJob& h, int shard, float* b, int st, const int32_t* tok)
+      : ex(e), w(wk), hj(h), s(shard), base(b), step(st), tokens(tok) {}
 
   float* acquire(int layer) override {
     const long len = hy_pad32(hy_layer_floats(&hj.m, layer));
@@ -626,6 +792,7 @@ struct StreamingSink : hy::GradSink {
       if (w.ring_head + len > w.ring_floats) w.ring_head = 0;
       const long lo = w.ring_head, hi = w.ring_head + len;
       // retire (wait for) every in-flight layer overlapping [lo, hi)
+      HY_PROF(w.comp, "wait_ring");
       std::deque<Worker::RingEntry> keep;
       for (const Worker::RingEntry& e : w.ring_live) {
         if (e.off < hi && lo < e.off + e.len) {
@@ -642,8 +809,21 @@ struct StreamingSink : hy::GradSink {
     }
     check_cuda(cudaMemsetAsync(p, 0, sizeof(float) * static_cast<size_t>(len), w.comp), "zero grads");
     if (layer == 0) w.gembed_tr.after_write(w.comp);
+    if (layer == 0 && split_embed()) {
+      w.rowidx_tr.before_write(w.comp);
+      check_cuda(hy::embed_row_index(w.comp, static_cast<int>(hj.M), tokens, hj.m.V, hj.m.T, w.rowidx, w.rowlist,
+                                     w.rowcount),
+                 "row index");
+      w.rowidx_tr.after_write(w.comp);
+    }
     live[layer] = p;
     return p;
+  }
+
+  // GPU-placed embedding with its optimizer split around the scatter (not with the staging
+  // aliased onto the scratch, where every update waits for the end of the backward)
+  bool split_embed() const {
+    return !hj.host_layer[0] && w.rowidx && tokens && !w.stg_alias && g_debug_skip != 2;
   }
 
   // With the Adam staging aliased onto the backward's scratch (tiny HBM caps), layers are
@@ -664,6 +844,17 @@ struct StreamingSink : hy::GradSink {
     queued.clear();
   }
 
+  void release_dense(int layer) override {
+    if (layer != 0 || !split_embed()) return;
+    Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
+    mvt.before_read(w.opt2);
+    w.gembed_tr.before_read(w.opt2);
+    ex.adam_layer(w, hj, s, base, 0, live.at(0), step, nullptr, /*part=*/1);
+    w.gembed_tr.after_read(w.opt2);
+    mvt.after_read(w.opt2);
+    dense_done = true;
+  }
+
   void emit(int layer) {
     float* p = live.at(layer);
     cudaEvent_t done = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
@@ -672,8 +863,15 @@ struct StreamingSink : hy::GradSink {
         if (w.ring + e.off == p) e.done = done;
       }
     }
+    if (hj.host_layer[static_cast<size_t>(layer)]) {
+      if (layer == 0) w.gembed_tr.before_read(w.up);
+      ex.host_adam_layer(w, hj, s, layer, p, step, done);
+      if (layer == 0) w.gembed_tr.after_read(w.up);
+      host_layers.push_back(layer);
+      return;
+    }
     if (layer == 0) w.gembed_tr.before_read(w.opt);
-    ex.adam_layer(w, hj, s, base, layer, p, step, done);
+    ex.adam_layer(w, hj, s, base, layer, p, step, done, layer == 0 && dense_done ? 2 : 0);
     if (layer == 0) w.gembed_tr.after_read(w.opt);
   }
 };
@@ -775,14 +973,34 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   if (loaded) {
     const long base = hy_layer_offset(&hj.m, g.l0);
     pe->tr.before_write(w.down);
-    hj.params_tr[static_cast<size_t>(s)]->before_read(w.down);
+    param_read_begin(hj, s, w.down);
     check_cuda(xfer(pbase, hj.params + base, sizeof(float) * static_cast<size_t>(g.param_floats),
                     cudaMemcpyHostToDevice, w.down),
                "param h2d");
-    hj.params_tr[static_cast<size_t>(s)]->after_read(w.down);
+    param_read_end(hj, s, w.down);
     pe->tr.after_write(w.down);
     w.st.param_h2d_bytes += 4.0 * g.param_floats;
     w.st.h2d_bytes += 4.0 * g.param_floats;
+  } else if (!pe->dirty.empty()) {
+    // resident, but some layers were updated host-side: refresh just those
+    pe->tr.before_write(w.down);
+    param_read_begin(hj, s, w.down);
+    double bytes = 0;
+    for (int l : pe->dirty) {
+      const long off = hy_layer_offset(&hj.m, l);
+      const long n = hy_layer_floats(&hj.m, l);
+      check_cuda(xfer(pbase + (off - hy_layer_offset(&hj.m, g.l0)), hj.params + off, sizeof(float) * static_cast<size_t>(n),
+                      cudaMemcpyHostToDevice, w.down),
+                 "param refresh h2d");
+      bytes += 4.0 * n;
+    }
+    param_read_end(hj, s, w.down);
+    pe->tr.after_write(w.down);
+    pe->dirty.clear();
+    w.st.refresh_h2d_bytes += bytes;
+    w.st.param_h2d_bytes += bytes;
+    w.st.h2d_bytes += bytes;
+    w.st.elided_param_bytes += std::max(0.0, task.t.param_load_bytes - bytes);
   } else {
     w.st.elided_param_bytes += task.t.param_load_bytes;
   }
@@ -793,10 +1011,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     const Tag wt{j, -1, -2, hj.version[0]};
     if (!(w.gembed_tag == wt)) {
       w.gembed_tr.before_write(w.down);
-      hj.params_tr[0]->before_read(w.down);
+      param_read_begin(hj, 0, w.down);
       const size_t wb = sizeof(float) * static_cast<size_t>(hj.m.V) * static_cast<size_t>(hj.m.d);
       check_cuda(xfer(w.gembed, hj.params, wb, cudaMemcpyHostToDevice, w.down), "wte h2d");
-      hj.params_tr[0]->after_read(w.down);
+      param_read_end(hj, 0, w.down);
       w.gembed_tr.after_write(w.down);
       w.gembed_tag = wt;
       w.st.param_h2d_bytes += static_cast<double>(wb);
@@ -897,6 +1115,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   check_cuda(cudaEventRecord(tm.pr1, w.down), "pr1");
 
   // ---- Compute (comp) ---------------------------------------------------------------
+  std::vector<int> host_dirty;  // layers of this backward updated host-side
   hy::Scratch sc;
   int max_blocks = 0;
   for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
@@ -904,12 +1123,15 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   if (w.stg_alias) {
     for (int i = 0; i < kStaging; ++i) w.stg_tr[i].before_write(w.comp);  // scratch reused as staging
   }
+  {
+  HY_PROF(w.comp, fwd ? "wait_task_F" : "wait_task_B");
   pe->tr.before_read(w.comp);
   if (wte_ext) w.gembed_tr.before_read(w.comp);
   if (need_tokens) w.tok_tr[tok_i].before_read(w.comp);
   if (ain >= 0) w.abuf_tr[ain].before_read(w.comp);
   if (gin >= 0) w.gbd_tr[gin].before_read(w.comp);
   if (needs_z) w.z_tr.before_read(w.comp);
+  }
   check_cuda(cudaEventRecord(tm.c0, w.comp), "c0");
   int aout = -1, gout = -1;
   if (fwd) {
@@ -954,14 +1176,15 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     w.st.elided_compute_tasks += 1;
   } else {
     // Gradients stream into the optimizer layer by layer (StreamingSink -> adam_layer on
-    // the opt stream); host params / m / v of the shard are rewritten by the up stream.
+    // the opt stream, zero-copy: host params / m / v of the shard are rewritten by the
+    // optimizer kernels themselves; host-placed layers go through host_adam_layer).
     Tracked& ptr = *hj.params_tr[static_cast<size_t>(s)];
     Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
     mvt.before_read(w.opt);
     ptr.before_write(w.up);
     mvt.before_write(w.up);
     check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
-    StreamingSink sink(*this, w, hj, s, pbase, gmb + 1);
+    StreamingSink sink(*this, w, hj, s, pbase, gmb + 1, need_tokens ? w.tok[tok_i] : nullptr);
     sink.deferred = w.stg_alias;
     if (g_debug_skip == 2) {  // gradients "computed": only the optimizer/transfer pipeline runs
       if (g.has_embed) sink.acquire(0);
@@ -981,12 +1204,12 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // staging = scratch: after the backward
     }
     sink.flush();
+    host_dirty = sink.host_layers;
     mvt.after_read(w.opt);
     ptr.after_write(w.up);
     mvt.after_write(w.up);
-    pe->tr.after_write(w.opt);  // Adam rewrote the params in place
-    pe->tr.after_read(w.up);    // ... and the up stream wrote them back
-    w.opt_pending = true;
+    pe->tr.after_write(w.opt);  // Adam rewrote the params in place (opt waited for opt2)
+    pe->tr.after_read(w.up);    // ... and the up stream writes them back
     if (g.has_head && !g.has_embed) {
       w.z_tr.before_write(w.comp);
       check_cuda(cudaMemcpyAsync(w.zbuf, sc.z, act_bytes, cudaMemcpyDeviceToDevice, w.comp), "z save");
@@ -1063,6 +1286,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   if (!fwd) {
     hj.version[static_cast<size_t>(s)] += 1;
     pe->tag = Tag{j, -1, s, hj.version[static_cast<size_t>(s)]};
+    pe->dirty.insert(pe->dirty.end(), host_dirty.begin(), host_dirty.end());
   }
   w.prev_entry = pe;
   {
@@ -1085,13 +1309,15 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
         g_debug_skip = exec.debug_skip;
         check_cuda(cudaDeviceSynchronize(), "pre-pass sync");
         check_cuda(cudaEventRecord(w.t0, w.comp), "t0");
-        for (cudaStream_t s : {w.down, w.up, w.opt}) check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");
+        for (cudaStream_t s : {w.down, w.up, w.opt, w.opt2, w.hopt}) {
+          check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");
+        }
         const auto h0 = std::chrono::steady_clock::now();
         for (int t : w.tasks) enqueue_task(w, t, pass);
         w.enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         // join all streams into comp, then record the end
-        cudaStream_t others[3] = {w.down, w.up, w.opt};
-        for (int k = 0; k < 3; ++k) {
+        cudaStream_t others[5] = {w.down, w.up, w.opt, w.hopt, w.opt2};
+        for (int k = 0; k < 5; ++k) {
           check_cuda(cudaEventRecord(w.join[k], others[k]), "join");
           check_cuda(cudaStreamWaitEvent(w.comp, w.join[k], 0), "join wait");
         }
@@ -1216,6 +1442,9 @@ void Executor::run(int passes, bool timed) {
       a.act_h2d_bytes += b.act_h2d_bytes;
       a.act_d2h_bytes += b.act_d2h_bytes;
       a.elided_param_bytes += b.elided_param_bytes;
+      a.host_opt_params += b.host_opt_params;
+      a.host_grad_d2h_bytes += b.host_grad_d2h_bytes;
+      a.refresh_h2d_bytes += b.refresh_h2d_bytes;
       a.elided_act_bytes += b.elided_act_bytes;
       a.kernel_launches += b.kernel_launches;
     }

@@ -272,6 +272,21 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   const long n = static_cast<long>(s.M) * m.d;
   const int b0 = std::max(g.l0, 1);
   const int nb = g.n_blocks;
+  // 0) embedding shard without the head: the deferred tied-wte gradient first (logits
+  //    recomputed from the head's saved z), so the dense part of dwte is final before the
+  //    blocks and its rows can go to the optimizer while they back-propagate.
+  float* gembed = nullptr;
+  if (g.has_embed) gembed = sink.acquire(0);  // wte/wpe grads: head (k == 1) + embedding
+  if (g.has_embed && !g.has_head && io.z_in) {
+    if (io.z_in != s.z) {
+      check_cuda(cudaMemcpyAsync(s.z, io.z_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "z in");
+    }
+    float* saved_dz = s.dz;
+    s.dz = nullptr;  // only dwte is wanted
+    head_pass(st, m, nullptr, slot, nullptr, io.targets, s, true, gembed, /*z_ready=*/true);
+    s.dz = saved_dz;
+    sink.release_dense(0);
+  }
   // 1) recompute: stash[i] = input of block b0+i; stash[nb] = shard output.
   if (g.has_embed) {
     check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), s.stash),
@@ -287,8 +302,6 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   bool last_block_live = nb > 0 && !g.has_head;
   // 2) gradient wrt the shard output
   float* dh = s.tmp_h;
-  float* gembed = nullptr;
-  if (g.has_embed) gembed = sink.acquire(0);  // wte/wpe grads: head (k == 1) + embedding
   if (g.has_head) {
     const float* lnf = slot + lo(m, m.L + 1, g.l0);
     float* glnf = sink.acquire(m.L + 1);
@@ -296,6 +309,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     float* dwte = g.has_embed ? gembed : nullptr;  // otherwise deferred to shard 0 via z
     const float* hfin = s.stash + nb * n;
     head_pass(st, m, lnf, wte, hfin, io.targets, s, true, dwte);
+    if (dwte) sink.release_dense(0);
     check_cuda(layernorm_bwd(st, s.M, m.d, hfin, lnf, s.zmean, s.zrstd, s.dz, dh, false, glnf, glnf + hy_pad32(m.d),
                              s.ws),
                "ln_f bwd");
@@ -315,17 +329,8 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     block_backward(st, m, w, gw, s.stash + i * n, dh, s);
     sink.release(layer);
   }
-  // 4) embedding (+ deferred tied-wte gradient from the head's saved z)
+  // 4) embedding: token rows of wte and wpe
   if (g.has_embed) {
-    if (!g.has_head && io.z_in) {
-      if (io.z_in != s.z) {
-        check_cuda(cudaMemcpyAsync(s.z, io.z_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "z in");
-      }
-      float* saved_dz = s.dz;
-      s.dz = nullptr;  // only dwte is wanted
-      head_pass(st, m, nullptr, slot, nullptr, io.targets, s, true, gembed, /*z_ready=*/true);
-      s.dz = saved_dz;
-    }
     check_cuda(embed_bwd(st, s.M, m.T, m.d, io.tokens, dh, gembed, gembed + hy_pad32(static_cast<long>(m.V) * m.d),
                          nullptr),
                "embed bwd");

@@ -69,6 +69,10 @@ struct GradSink {
   virtual ~GradSink() = default;
   virtual float* acquire(int layer) = 0;
   virtual void release(int layer) = 0;
+  // Embedding only, before release(0): every wte row not indexed by this task's tokens is
+  // final (the tied head's dense dwte is in; the embedding scatter only touches token rows
+  // and wpe), so their optimizer update may start while the blocks back-propagate.
+  virtual void release_dense(int layer) {}
 };
 
 void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, GradSink& sink,

@@ -2,6 +2,7 @@
 // grid-stride float4 loops for elementwise work, two-stage deterministic column sums.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "launch_count.cuh"
@@ -346,6 +347,244 @@ __global__ void adam_bf16_kernel(long n4, float4* __restrict__ p, const float4* 
   }
 }
 
+// Zero-copy AdamW: the moments and the master-param mirror live in pinned host memory and
+// are read / written by the kernel itself over the host link (mapped pinned memory, UVA), so
+// the optimizer needs no HBM staging and no copy-engine round trip; p is updated in place in
+// the HBM slot. Each thread keeps kU independent host loads in flight to cover the PCIe
+// round-trip latency. Row filter: element e belongs to row e / row4 (float4 units) and is
+// processed iff flags[row] == want (flags == nullptr: every element).
+// 128 threads x <= 64 registers per CTA: small enough to co-reside with a persistent GEMM
+// CTA (256 threads x 191 registers) instead of evicting it from its SM for the whole transfer.
+template <bool kBf16>
+__global__ void __launch_bounds__(128, 8) adam_zc_kernel(long n4, long row4, const uint8_t* __restrict__ flags,
+                                                      int want, float4* __restrict__ p, const float4* __restrict__ g,
+                                                      void* __restrict__ mh, void* __restrict__ vh,
+                                                      float4* __restrict__ ph, AdamHyper h) {
+  constexpr int kU = 4;
+  const float c1 = 1.f - h.beta1, c2 = 1.f - h.beta2;
+  const long stride = static_cast<long>(gridDim.x) * blockDim.x;
+  for (long base = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; base < n4; base += stride * kU) {
+    float mk[kU][4], vk[kU][4];
+    bool on[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long i = base + u * stride;
+      on[u] = i < n4 && (flags == nullptr || flags[i / row4] == want);
+      if (!on[u]) continue;
+      if constexpr (kBf16) {
+        const uint2 mm = reinterpret_cast<const uint2*>(mh)[i], vv = reinterpret_cast<const uint2*>(vh)[i];
+        const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mm);
+        const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&vv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          mk[u][k] = __bfloat162float(mb[k]);
+          vk[u][k] = __bfloat162float(vb[k]);
+        }
+      } else {
+        const float4 mm = reinterpret_cast<const float4*>(mh)[i], vv = reinterpret_cast<const float4*>(vh)[i];
+        mk[u][0] = mm.x, mk[u][1] = mm.y, mk[u][2] = mm.z, mk[u][3] = mm.w;
+        vk[u][0] = vv.x, vk[u][1] = vv.y, vk[u][2] = vv.z, vk[u][3] = vv.w;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (!on[u]) continue;
+      const long i = base + u * stride;
+      float4 pp = p[i];
+      const float4 gg = g[i];
+      float* pe = &pp.x;
+      const float* ge = &gg.x;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        mk[u][k] = h.beta1 * mk[u][k] + c1 * ge[k];
+        vk[u][k] = h.beta2 * vk[u][k] + c2 * ge[k] * ge[k];
+        const float upd = (mk[u][k] / h.bc1) / (sqrtf(vk[u][k] / h.bc2) + h.eps);
+        pe[k] = pe[k] - h.lr * (upd + h.weight_decay * pe[k]);
+      }
+      p[i] = pp;
+      if (ph) ph[i] = pp;
+      if constexpr (kBf16) {
+        __nv_bfloat16 mb[4], vb[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          mb[k] = __float2bfloat16_rn(mk[u][k]);
+          vb[k] = __float2bfloat16_rn(vk[u][k]);
+        }
+        reinterpret_cast<uint2*>(mh)[i] = *reinterpret_cast<uint2*>(mb);
+        reinterpret_cast<uint2*>(vh)[i] = *reinterpret_cast<uint2*>(vb);
+      } else {
+        reinterpret_cast<float4*>(mh)[i] = make_float4(mk[u][0], mk[u][1], mk[u][2], mk[u][3]);
+        reinterpret_cast<float4*>(vh)[i] = make_float4(vk[u][0], vk[u][1], vk[u][2], vk[u][3]);
+      }
+    }
+  }
+}
+
+// ---- embedding optimizer split (token rows vs the rest) ------------------------------
+// idx[r] for the rows of layer 0 (wte rows 0..V-1, wpe rows V..V+T-1): the compact index of
+// the row if this minibatch's embedding scatter touches it (token rows, every wpe row), -1
+// otherwise; rows[c] = r inverts it; count[0] = number of such rows. Compact order is row order.
+__global__ void row_mark_kernel(int M, const int32_t* __restrict__ tok, int V, int T, int* __restrict__ idx) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < M) idx[tok[i]] = 0;
+  if (i < T) idx[V + i] = 0;
+}
+
+__global__ void __launch_bounds__(1024) row_compact_kernel(int n, int* __restrict__ idx, int* __restrict__ rows,
+                                                           int* __restrict__ count) {
+  __shared__ int warp_tot[32];
+  const int t = threadIdx.x, per = (n + 1023) / 1024;
+  const int lo = min(n, t * per), hi = min(n, lo + per);
+  int c = 0;
+  for (int r = lo; r < hi; ++r) c += idx[r] >= 0;
+  // block exclusive scan of c
+  int x = c;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if ((t & 31) >= o) x += y;
+  }
+  if ((t & 31) == 31) warp_tot[t >> 5] = x;
+  __syncthreads();
+  if (t < 32) {
+    int w = warp_tot[t];
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (t >= o) w += y;
+    }
+    warp_tot[t] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  int base = x - c + ((t >> 5) ? warp_tot[(t >> 5) - 1] : 0);
+  for (int r = lo; r < hi; ++r) {
+    if (idx[r] >= 0) {
+      idx[r] = base;
+      rows[base] = r;
+      ++base;
+    }
+  }
+  if (t == 1023) *count = base;
+}
+
+// Pass A over one staged chunk of layer 0 (elements [off, off + n) of the layer): AdamW on
+// every row not in the compact set; rows in the set are only copied (m, v) into the compact
+// buffers (cm, cv: [count][d]) for pass B. The chunk's p, m, v go back to the host afterwards
+// unchanged for those rows.
+template <bool kBf16>
+__global__ void adam_masked_kernel(long n4, long off, int d, const int* __restrict__ idx, float4* __restrict__ p,
+                                   const float4* __restrict__ g, void* __restrict__ m, void* __restrict__ v,
+                                   void* __restrict__ cm, void* __restrict__ cv, AdamHyper h) {
+  const float c1 = 1.f - h.beta1, c2 = 1.f - h.beta2;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n4;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long e = off + 4 * i;
+    const int c = idx[e / d];
+    const long col = e % d;
+    if (c >= 0) {  // token / wpe row: stash its state for pass B
+      if constexpr (kBf16) {
+        reinterpret_cast<uint2*>(cm)[(static_cast<long>(c) * d + col) / 4] = reinterpret_cast<const uint2*>(m)[i];
+        reinterpret_cast<uint2*>(cv)[(static_cast<long>(c) * d + col) / 4] = reinterpret_cast<const uint2*>(v)[i];
+      } else {
+        reinterpret_cast<float4*>(cm)[(static_cast<long>(c) * d + col) / 4] = reinterpret_cast<const float4*>(m)[i];
+        reinterpret_cast<float4*>(cv)[(static_cast<long>(c) * d + col) / 4] = reinterpret_cast<const float4*>(v)[i];
+      }
+      continue;
+    }
+    float4 pp = p[i];
+    const float4 gg = g[i];
+    float* pe = &pp.x;
+    const float* ge = &gg.x;
+    float mk[4], vk[4];
+    if constexpr (kBf16) {
+      const uint2 mm = reinterpret_cast<const uint2*>(m)[i], vv = reinterpret_cast<const uint2*>(v)[i];
+      const __nv_bfloat16* mb = reinterpret_cast<const __nv_bfloat16*>(&mm);
+      const __nv_bfloat16* vb = reinterpret_cast<const __nv_bfloat16*>(&vv);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mk[k] = __bfloat162float(mb[k]), vk[k] = __bfloat162float(vb[k]);
+    } else {
+      const float4 mm = reinterpret_cast<const float4*>(m)[i], vv = reinterpret_cast<const float4*>(v)[i];
+      mk[0] = mm.x, mk[1] = mm.y, mk[2] = mm.z, mk[3] = mm.w;
+      vk[0] = vv.x, vk[1] = vv.y, vk[2] = vv.z, vk[3] = vv.w;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mk[k] = h.beta1 * mk[k] + c1 * ge[k];
+      vk[k] = h.beta2 * vk[k] + c2 * ge[k] * ge[k];
+      const float upd = (mk[k] / h.bc1) / (sqrtf(vk[k] / h.bc2) + h.eps);
+      pe[k] = pe[k] - h.lr * (upd + h.weight_decay * pe[k]);
+    }
+    p[i] = pp;
+    if constexpr (kBf16) {
+      __nv_bfloat16 mb[4], vb[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mb[k] = __float2bfloat16_rn(mk[k]), vb[k] = __float2bfloat16_rn(vk[k]);
+      reinterpret_cast<uint2*>(m)[i] = *reinterpret_cast<uint2*>(mb);
+      reinterpret_cast<uint2*>(v)[i] = *reinterpret_cast<uint2*>(vb);
+    } else {
+      reinterpret_cast<float4*>(m)[i] = make_float4(mk[0], mk[1], mk[2], mk[3]);
+      reinterpret_cast<float4*>(v)[i] = make_float4(vk[0], vk[1], vk[2], vk[3]);
+    }
+  }
+}
+
+// Pass B1: AdamW on the compact rows (state from pass A's stash), p updated in the slot
+// (layer 0 base `p`) and copied into cp for the write-back.
+template <bool kBf16>
+__global__ void adam_rows_kernel(const int* __restrict__ count, const int* __restrict__ rows, int d, float* __restrict__ p,
+                                 const float* __restrict__ g, void* __restrict__ cm, void* __restrict__ cv,
+                                 float* __restrict__ cp, AdamHyper h) {
+  const float c1 = 1.f - h.beta1, c2 = 1.f - h.beta2;
+  const long n = static_cast<long>(*count) * d;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long c = i / d, col = i % d;
+    const long e = static_cast<long>(rows[c]) * d + col;
+    const float gi = g[e];
+    float mi, vi;
+    if constexpr (kBf16) {
+      mi = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(cm)[i]);
+      vi = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(cv)[i]);
+    } else {
+      mi = reinterpret_cast<const float*>(cm)[i];
+      vi = reinterpret_cast<const float*>(cv)[i];
+    }
+    mi = h.beta1 * mi + c1 * gi;
+    vi = h.beta2 * vi + c2 * gi * gi;
+    const float upd = (mi / h.bc1) / (sqrtf(vi / h.bc2) + h.eps);
+    const float pi = p[e] - h.lr * (upd + h.weight_decay * p[e]);
+    p[e] = pi;
+    cp[i] = pi;
+    if constexpr (kBf16) {
+      reinterpret_cast<__nv_bfloat16*>(cm)[i] = __float2bfloat16_rn(mi);
+      reinterpret_cast<__nv_bfloat16*>(cv)[i] = __float2bfloat16_rn(vi);
+    } else {
+      reinterpret_cast<float*>(cm)[i] = mi;
+      reinterpret_cast<float*>(cv)[i] = vi;
+    }
+  }
+}
+
+// Pass B2: the compact rows' p, m, v written straight into the host arrays (mapped pinned
+// memory, zero-copy stores; a few MB per minibatch).
+template <int kEs>
+__global__ void rows_to_host_kernel(const int* __restrict__ count, const int* __restrict__ rows, int d,
+                                    const float* __restrict__ cp, const void* __restrict__ cm,
+                                    const void* __restrict__ cv, float* __restrict__ hp, void* __restrict__ hm,
+                                    void* __restrict__ hv) {
+  const long n = static_cast<long>(*count) * d;
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long e = static_cast<long>(rows[i / d]) * d + i % d;
+    hp[e] = cp[i];
+    if constexpr (kEs == 2) {
+      reinterpret_cast<uint16_t*>(hm)[e] = reinterpret_cast<const uint16_t*>(cm)[i];
+      reinterpret_cast<uint16_t*>(hv)[e] = reinterpret_cast<const uint16_t*>(cv)[i];
+    } else {
+      reinterpret_cast<float*>(hm)[e] = reinterpret_cast<const float*>(cm)[i];
+      reinterpret_cast<float*>(hv)[e] = reinterpret_cast<const float*>(cv)[i];
+    }
+  }
+}
+
 int grid_for(long n, int block) {
   long g = (n + block - 1) / block;
   const long cap = static_cast<long>(sms()) * 8;
@@ -473,6 +712,79 @@ cudaError_t adam_update(cudaStream_t s, long n, float* p, const float* g, float*
   count_launch();
   adam_kernel<<<grid_for(n4, 256), 256, 0, s>>>(n4, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                                 reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), h);
+  return cudaGetLastError();
+}
+
+cudaError_t adam_zc(cudaStream_t s, long n, float* p, const float* g, void* m_host, void* v_host, float* p_host,
+                    bool bf16, const AdamHyper& h, const uint8_t* flags, int row_len, int want, int grid) {
+  if (n % 4 || (flags && (row_len <= 0 || row_len % 4))) return cudaErrorInvalidValue;
+  if (n == 0) return cudaSuccess;
+  const long n4 = n / 4;
+  const long row4 = flags ? row_len / 4 : 1;
+  const long need = (n4 + 128 * 4 - 1) / (128 * 4);
+  const int blocks = static_cast<int>(std::min<long>(need, grid > 0 ? grid : 96));
+  count_launch();
+  if (bf16) {
+    adam_zc_kernel<true><<<blocks, 128, 0, s>>>(n4, row4, flags, want, reinterpret_cast<float4*>(p),
+                                                reinterpret_cast<const float4*>(g), m_host, v_host,
+                                                reinterpret_cast<float4*>(p_host), h);
+  } else {
+    adam_zc_kernel<false><<<blocks, 128, 0, s>>>(n4, row4, flags, want, reinterpret_cast<float4*>(p),
+                                                 reinterpret_cast<const float4*>(g), m_host, v_host,
+                                                 reinterpret_cast<float4*>(p_host), h);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t embed_row_index(cudaStream_t s, int M, const int32_t* tokens, int V, int T, int* idx, int* rows,
+                            int* count) {
+  cudaError_t e = cudaMemsetAsync(idx, 0xff, sizeof(int) * (static_cast<size_t>(V) + T), s);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  row_mark_kernel<<<(std::max(M, T) + 255) / 256, 256, 0, s>>>(M, tokens, V, T, idx);
+  count_launch();
+  row_compact_kernel<<<1, 1024, 0, s>>>(V + T, idx, rows, count);
+  return cudaGetLastError();
+}
+
+cudaError_t adam_embed_dense(cudaStream_t s, long n, long off, int d, const int* idx, float* p, const float* g,
+                             void* m, void* v, void* cm, void* cv, bool bf16, const AdamHyper& h) {
+  if (n % 4 || off % 4 || d % 4) return cudaErrorInvalidValue;
+  const long n4 = n / 4;
+  count_launch();
+  if (bf16) {
+    adam_masked_kernel<true><<<grid_for(n4, 256), 256, 0, s>>>(n4, off, d, idx, reinterpret_cast<float4*>(p),
+                                                               reinterpret_cast<const float4*>(g), m, v, cm, cv, h);
+  } else {
+    adam_masked_kernel<false><<<grid_for(n4, 256), 256, 0, s>>>(n4, off, d, idx, reinterpret_cast<float4*>(p),
+                                                                reinterpret_cast<const float4*>(g), m, v, cm, cv, h);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t adam_embed_rows(cudaStream_t s, long max_rows, const int* count, const int* rows, int d, float* p,
+                            const float* g, void* cm, void* cv, float* cp, bool bf16, const AdamHyper& h) {
+  const long n = max_rows * d;
+  count_launch();
+  if (bf16) {
+    adam_rows_kernel<true><<<grid_for(n, 256), 256, 0, s>>>(count, rows, d, p, g, cm, cv, cp, h);
+  } else {
+    adam_rows_kernel<false><<<grid_for(n, 256), 256, 0, s>>>(count, rows, d, p, g, cm, cv, cp, h);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t embed_rows_to_host(cudaStream_t s, long max_rows, const int* count, const int* rows, int d,
+                               const float* cp, const void* cm, const void* cv, float* hp, void* hm, void* hv,
+                               bool bf16) {
+  count_launch();
+  // few CTAs: host-link bound, and small enough not to crowd the compute kernels
+  const int grid = static_cast<int>(std::min<long>(32, (max_rows * d + 255) / 256));
+  if (bf16) {
+    rows_to_host_kernel<2><<<grid, 256, 0, s>>>(count, rows, d, cp, cm, cv, hp, hm, hv);
+  } else {
+    rows_to_host_kernel<4><<<grid, 256, 0, s>>>(count, rows, d, cp, cm, cv, hp, hm, hv);
+  }
   return cudaGetLastError();
 }
 

@@ -38,6 +38,30 @@ cudaError_t adam_update(cudaStream_t s, long n, float* p, const float* g, float*
 cudaError_t adam_update_bf16(cudaStream_t s, long n, float* p, const float* g, uint16_t* m, uint16_t* v,
                              const AdamHyper& h);
 
+// Zero-copy AdamW (p in HBM; m, v and the p mirror p_host in mapped pinned host memory;
+// p_host may be null: the caller writes the params back itself).
+// flags != nullptr: only elements of rows r (row_len floats each) with flags[r] == want.
+// grid: CTAs (0 = default); the kernel is host-link bound, a few dozen CTAs saturate it.
+cudaError_t adam_zc(cudaStream_t s, long n, float* p, const float* g, void* m_host, void* v_host, float* p_host,
+                    bool bf16, const AdamHyper& h, const uint8_t* flags = nullptr, int row_len = 0, int want = 0,
+                    int grid = 0);
+// Embedding optimizer split. Rows of layer 0 (wte 0..V-1, wpe V..V+T-1) touched by this
+// minibatch's embedding scatter (token rows, all wpe rows) get compact indices:
+// idx[V+T] (-1 = untouched), rows[<= M+T] (inverse), count[1].
+cudaError_t embed_row_index(cudaStream_t s, int M, const int32_t* tokens, int V, int T, int* idx, int* rows,
+                            int* count);
+// Pass A on a staged chunk (layer-0 elements [off, off+n)): AdamW for untouched rows; touched
+// rows' m, v copied to the compact buffers cm, cv ([rows][d]).
+cudaError_t adam_embed_dense(cudaStream_t s, long n, long off, int d, const int* idx, float* p, const float* g,
+                             void* m, void* v, void* cm, void* cv, bool bf16, const AdamHyper& h);
+// Pass B1: AdamW on the compact rows; p (layer-0 base in HBM) updated in place, cp = new p.
+cudaError_t adam_embed_rows(cudaStream_t s, long max_rows, const int* count, const int* rows, int d, float* p,
+                            const float* g, void* cm, void* cv, float* cp, bool bf16, const AdamHyper& h);
+// Pass B2: compact rows' p, m, v -> host arrays (layer-0 base pointers), zero-copy stores.
+cudaError_t embed_rows_to_host(cudaStream_t s, long max_rows, const int* count, const int* rows, int d,
+                               const float* cp, const void* cm, const void* cv, float* hp, void* hm, void* hv,
+                               bool bf16);
+
 // Tensor-core attention (attention_tc.cu). `work` holds score matrices: forward needs
 // T*T floats per (batch, head) processed at once, backward 2*T*T; chunks are sized to fit.
 cudaError_t attention_fwd_tc(cudaStream_t s, int B, int T, int H, const float* qkv, float* out, float* work,

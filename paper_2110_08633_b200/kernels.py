@@ -127,3 +127,11 @@ def bias_grad(dy, out=None, accumulate=False):
 
 def adam(p, g, m, v, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0):
     check(lib().hy_adam(_s(), p.numel(), _p(p), _p(g), _p(m), _p(v), lr, beta1, beta2, eps, weight_decay, step))
+
+
+def adam_host_state(p, g, m_host, v_host, p_host, lr, step, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0,
+                    grid=0):
+    """Zero-copy AdamW: p, g on the GPU; m, v, p_host pinned host tensors (fp32, or bf16 moments)."""
+    bf16 = int(m_host.dtype == torch.bfloat16)
+    check(lib().hy_adam_host_state(_s(), p.numel(), _p(p), _p(g), _p(m_host), _p(v_host), _p(p_host), lr, beta1,
+                                   beta2, eps, weight_decay, step, bf16, grid))

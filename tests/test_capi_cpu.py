@@ -60,3 +60,32 @@ def test_plan_json_matches_reference(case, hash_g1):
     assert [p["shard_starts"] for p in r["partitions"]] == [p["shard_starts"] for p in gold["partitions"]]
     assert [[d[0], d[1]] for d in r["dispatch"]] == [[d[0], d[1]] for d in gold["dispatch"]]
     assert abs(r["makespan_s"] - float(gold["makespan"])) == 0.0
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_host_adam_matches_oracle(bf16):
+    """Host-side AdamW (the executor's host_opt_fraction path) against the
+    CPU oracle's update over 3 steps; bf16 moments round RNE like the oracle's emulation."""
+    import numpy as np
+    from oracle import oracle as O
+
+    rng = np.random.default_rng(7)
+    n = 100_003  # ragged: not a multiple of the vector width or the thread split
+    p0 = rng.standard_normal(n).astype(np.float32) * 0.02
+    po, mo, vo = p0.copy(), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    ph = p0.copy()
+    mh = np.zeros(n, np.uint16 if bf16 else np.float32)
+    vh = np.zeros_like(mh)
+    for step in (1, 2, 3):
+        g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+        g[::97] = 0.0
+        O.adam(po, g, mo, vo, 3e-4, step, wd=0.01, bf16_state=bf16)
+        rc = P.lib().hy_host_adam(n, ph.ctypes.data, g.ctypes.data, mh.ctypes.data, vh.ctypes.data, 3e-4, 0.9,
+                                  0.999, 1e-8, 0.01, step, int(bf16), 3)
+        assert rc == 0
+    as_f = (lambda a: (a.astype(np.uint32) << 16).view(np.float32)) if bf16 else (lambda a: a)
+    # identical formula; only FMA contraction may differ -> a few ulp
+    np.testing.assert_allclose(ph, po, rtol=2e-6, atol=1e-9)
+    np.testing.assert_allclose(as_f(mh), mo, rtol=1e-2 if bf16 else 2e-6, atol=1e-9)
+    np.testing.assert_allclose(as_f(vh), vo, rtol=1e-2 if bf16 else 2e-6, atol=1e-12)
+    assert P.lib().hy_host_adam(-1, 0, 0, 0, 0, 1e-3, 0.9, 0.999, 1e-8, 0.0, 1, 0, 1) == -1

