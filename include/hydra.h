@@ -105,6 +105,12 @@ int hy_attention_fwd(void* stream, int B, int T, int H, int hd, const float* qkv
                      long work_floats);
 int hy_attention_bwd(void* stream, int B, int T, int H, int hd, const float* qkv, const float* dout, float* dqkv,
                      float* work, long work_floats);
+/* Fused (flash-style) causal attention on tcgen05, kind::tf32, head dim 64 — the TF32 path of
+ * the shard runner. lse2 [B*H*T]: per-query log2-domain logsumexp of S/8 written by the
+ * forward, read by the backward; Di [B*H*T] backward scratch. dqkv overwritten. */
+int hy_flash_attention_fwd(void* stream, int B, int T, int H, const float* qkv, float* out, float* lse2);
+int hy_flash_attention_bwd(void* stream, int B, int T, int H, const float* qkv, const float* out, const float* dout,
+                           const float* lse2, float* dqkv, float* Di);
 int hy_embed_fwd(void* stream, int rows, int T, int d, const int32_t* tokens, const float* wte, const float* wpe,
                  float* h);
 int hy_embed_bwd(void* stream, int rows, int T, int d, int V, const int32_t* tokens, const float* dh, float* dwte,

@@ -46,6 +46,8 @@ _SIGS = {
                 + [ctypes.c_float] * 5 + [ctypes.c_int]),
     "hy_adam_host_state": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_long] + [ctypes.c_void_p] * 5
                            + [ctypes.c_float] * 5 + [ctypes.c_int] * 3),
+    "hy_flash_attention_fwd": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3),
+    "hy_flash_attention_bwd": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p] * 6),
     "hy_host_adam": (ctypes.c_int, [ctypes.c_long] + [ctypes.c_void_p] * 4 + [ctypes.c_float] * 5
                      + [ctypes.c_int] * 3),
 }

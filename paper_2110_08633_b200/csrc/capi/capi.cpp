@@ -203,6 +203,17 @@ int hy_attention_bwd(void* stream, int B, int T, int H, int hd, const float* qkv
       "hy_attention_bwd");
 }
 
+int hy_flash_attention_fwd(void* stream, int B, int T, int H, const float* qkv, float* out, float* lse2) {
+  return cuda_status(hy::attention_fwd_fa(static_cast<cudaStream_t>(stream), B, T, H, qkv, out, lse2),
+                     "hy_flash_attention_fwd");
+}
+
+int hy_flash_attention_bwd(void* stream, int B, int T, int H, const float* qkv, const float* out, const float* dout,
+                           const float* lse2, float* dqkv, float* Di) {
+  return cuda_status(hy::attention_bwd_fa(static_cast<cudaStream_t>(stream), B, T, H, qkv, out, dout, lse2, dqkv, Di),
+                     "hy_flash_attention_bwd");
+}
+
 int hy_embed_fwd(void* stream, int rows, int T, int d, const int32_t* tokens, const float* wte, const float* wpe,
                  float* h) {
   return cuda_status(hy::embed_fwd(static_cast<cudaStream_t>(stream), rows, T, d, tokens, wte, wpe, h), "hy_embed_fwd");

@@ -70,7 +70,13 @@ void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const floa
   }
   // scores live in the (not yet written) MLP buffers fc+act: 8*M*d floats, contiguous
   { HY_PROF(st, "attn_fwd");
-  check_cuda(attention_fwd_tc(st, m.B, m.T, m.H, s.qkv, s.att, s.fc, s.act + 4L * M * d - s.fc), "attn_fwd");
+  // TF32: fused flash-style kernel (lse kept for the backward); 3xTF32 "fp32" precision:
+  // score matrices in the MLP buffers fc+act (8*M*d floats) through the batched GEMMs
+  if (gemm_precision_fp32()) {
+    check_cuda(attention_fwd_tc(st, m.B, m.T, m.H, s.qkv, s.att, s.fc, s.act + 4L * M * d - s.fc), "attn_fwd");
+  } else {
+    check_cuda(attention_fwd_fa(st, m.B, m.T, m.H, s.qkv, s.att, s.lse), "attn_fwd");
+  }
   }
   { HY_PROF(st, "o_proj");
   gemm(st, M, d, d, s.att, d, false, bt(w, d, HY_WO), d, false, s.hmid, d, bt(w, d, HY_BO), h_in, d);
@@ -133,7 +139,11 @@ void block_backward(cudaStream_t st, const hy_dims& m, const float* w, float* gw
   float* dqkv = s.fc;
   float* work = s.fc + 3L * M * d;
   { HY_PROF(st, "attn_bwd");
-  check_cuda(attention_bwd_tc(st, m.B, m.T, m.H, s.qkv, datt, dqkv, work, s.act + 4L * M * d - work), "attn bwd");
+  if (gemm_precision_fp32()) {
+    check_cuda(attention_bwd_tc(st, m.B, m.T, m.H, s.qkv, datt, dqkv, work, s.act + 4L * M * d - work), "attn bwd");
+  } else {
+    check_cuda(attention_bwd_fa(st, m.B, m.T, m.H, s.qkv, s.att, datt, s.lse, dqkv, s.attn_ws), "attn bwd");
+  }
   }
   { HY_PROF(st, "bwd_dW_qkv");
   gemm(st, 3 * d, d, M, dqkv, 3 * d, true, s.ln1, d, true, btw(gw, d, HY_WQKV), d, nullptr, nullptr, 0, 1.f);

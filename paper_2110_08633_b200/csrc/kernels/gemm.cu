@@ -575,6 +575,7 @@ cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const float* A, long 
 }  // namespace
 
 void gemm_set_precision_fp32(bool three_pass) { t_prec3 = three_pass; }
+bool gemm_precision_fp32() { return t_prec3; }
 
 cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
                       const float* B, long ldb, bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch) {

@@ -56,5 +56,6 @@ void gemm_set_splitk_workspace(float* ws, long floats);
 // Per host thread: true = "fp32" precision (3xTF32 split on the tensor cores, ~fp32
 // accuracy at 3x the MMA work), false = plain TF32 (default).
 void gemm_set_precision_fp32(bool three_pass);
+bool gemm_precision_fp32();
 
 }  // namespace hy

@@ -62,6 +62,13 @@ cudaError_t embed_rows_to_host(cudaStream_t s, long max_rows, const int* count, 
                                const float* cp, const void* cm, const void* cv, float* hp, void* hm, void* hv,
                                bool bf16);
 
+// Fused causal attention (attention_fa.cu), kind::tf32, head dim 64. qkv [B*T, 3*H*64];
+// out [B*T, H*64]; lse2 [B*H*T] = per-row log2-domain logsumexp of S/8 (for the backward).
+cudaError_t attention_fwd_fa(cudaStream_t s, int B, int T, int H, const float* qkv, float* out, float* lse2);
+// dqkv overwritten; Di: [B*H*T] scratch.
+cudaError_t attention_bwd_fa(cudaStream_t s, int B, int T, int H, const float* qkv, const float* out,
+                             const float* dout, const float* lse2, float* dqkv, float* Di);
+
 // Tensor-core attention (attention_tc.cu). `work` holds score matrices: forward needs
 // T*T floats per (batch, head) processed at once, backward 2*T*T; chunks are sized to fit.
 cudaError_t attention_fwd_tc(cudaStream_t s, int B, int T, int H, const float* qkv, float* out, float* work,

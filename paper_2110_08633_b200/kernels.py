@@ -91,6 +91,20 @@ def attention_bwd(qkv, dout, B, T, H, work_floats=None):
     return dqkv
 
 
+def flash_attention_fwd(qkv, B, T, H):
+    out = torch.empty(B * T, H * 64, device=qkv.device)
+    lse = torch.empty(B * H * T, device=qkv.device)
+    check(lib().hy_flash_attention_fwd(_s(), B, T, H, _p(qkv), _p(out), _p(lse)))
+    return out, lse
+
+
+def flash_attention_bwd(qkv, out, dout, lse, B, T, H):
+    dqkv = torch.empty_like(qkv)
+    di = torch.empty(B * H * T, device=qkv.device)
+    check(lib().hy_flash_attention_bwd(_s(), B, T, H, _p(qkv), _p(out), _p(dout), _p(lse), _p(dqkv), _p(di)))
+    return dqkv
+
+
 def embed_fwd(tokens, wte, wpe, T):
     rows = tokens.numel()
     d = wte.shape[1]

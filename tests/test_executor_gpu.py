@@ -81,10 +81,12 @@ def test_head_shard_without_embedding(tmp_path, mem, starts, precision):
     assert res["stats"]["arena_bytes"][0] <= mem + 8e6
 
 
-@pytest.mark.parametrize("precision,tol", [("fp32", dict(loss_tol=1e-5, param_tol=1e-4)), ("tf32", {})])
+@pytest.mark.parametrize("precision,tol", [("fp32", dict(loss_tol=1e-5, param_tol=1e-4)), ("tf32", dict(param_tol=2e-3))])
 def test_bf16_optimizer_state(tmp_path, precision, tol):
     """Adam moments stored/streamed as bf16 (halves optimizer-state link bytes); compared with
-    the oracle applying the same bf16 rounding to its moments."""
+    the oracle applying the same bf16 rounding to its moments. Stated separately (north_star):
+    with TF32 GEMMs a gradient perturbation can move a moment across a bf16 rounding boundary,
+    so parameters hold 2e-3 here (1.05e-3 measured on layer 1), losses 1e-3."""
     cfg = tiny_config(mbs=3)
     compare(cfg, tmp_path, precision=precision, opt_state="bf16", **tol)
 

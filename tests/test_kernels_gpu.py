@@ -176,6 +176,30 @@ def test_attention(B, T, H, chunk):
     assert rel(dqkv, qr.grad) < 3e-3
 
 
+@pytest.mark.parametrize("B,T,H", [(2, 32, 1), (2, 100, 3), (1, 512, 2), (4, 128, 12), (8, 512, 12), (2, 384, 4),
+                                   (3, 200, 5), (1, 1024, 2)])
+def test_flash_attention(B, T, H):
+    """Fused tcgen05 attention (the TF32 path): forward, lse, and the dK/dV + dQ backward
+    against PyTorch fp32 autograd; ragged T (not a multiple of the 128 / 64 tiles)."""
+    torch.manual_seed(7 * T + H)
+    qkv = torch.randn(B * T, 3 * H * 64, device=dev)
+    out, lse = K.flash_attention_fwd(qkv, B, T, H)
+    qr = qkv.clone().requires_grad_(True)
+    ref = ref_attention(qr, B, T, H)
+    assert rel(out, ref) < 3e-3
+    q, k, _ = qkv.view(B, T, 3, H, 64).permute(2, 0, 3, 1, 4)
+    s = (q @ k.transpose(-1, -2)) / 8.0
+    s = s.masked_fill(~torch.ones(T, T, device=dev, dtype=torch.bool).tril(), float("-inf"))
+    lse_ref = torch.logsumexp(s, -1).reshape(-1) / math.log(2.0)
+    assert (lse - lse_ref).abs().max().item() < 2e-2
+    dout = torch.randn_like(out)
+    ref.backward(dout)
+    dqkv = K.flash_attention_bwd(qkv, out, dout, lse, B, T, H)
+    assert rel(dqkv, qr.grad) < 3e-3
+    # deterministic (no atomics): bit-identical on a rerun
+    assert torch.equal(dqkv, K.flash_attention_bwd(qkv, out, dout, lse, B, T, H))
+
+
 def test_embedding():
     V, d, B, T = 1000, 128, 3, 40
     tok = torch.randint(0, V, (B * T,), device=dev, dtype=torch.int32)

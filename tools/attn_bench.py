@@ -19,3 +19,9 @@ for wf_mult, name in ((8, "fwd work=8Md (C2 runner)"), (32, "fwd work=32Md")):
     print(name, "%.1f us" % timeit(lambda: K.attention_fwd(qkv, B, T, H, work_floats=wf_mult * Md)))
 for wf_mult, name in ((5, "bwd work=5Md (C2 runner)"), (9, "bwd work=9Md"), (16, "bwd work=16Md (1 chunk)")):
     print(name, "%.1f us" % timeit(lambda: K.attention_bwd(qkv, dout, B, T, H, work_floats=wf_mult * Md)))
+out, lse = K.flash_attention_fwd(qkv, B, T, H)
+fl_fwd = 4.0 * B * H * T * T * 64 / 2  # causal: QK^T + PV over the lower triangle
+t = timeit(lambda: K.flash_attention_fwd(qkv, B, T, H))
+print("flash fwd %.1f us  %.0f TFLOP/s (causal-useful)" % (t, fl_fwd / t / 1e6))
+t = timeit(lambda: K.flash_attention_bwd(qkv, out, dout, lse, B, T, H))
+print("flash bwd %.1f us  %.0f TFLOP/s (causal-useful, 2.5x fwd)" % (t, 2.5 * fl_fwd / t / 1e6))
