@@ -46,6 +46,11 @@ struct ExecOptions {
   // are reloaded anyway, head side first); 0 = all on the GPU.
   double host_opt_fraction = 0;
   int host_opt_threads = 0;        // OpenMP threads of the host optimizer (0: cores - 4)
+  // Parameter cache policy. Default: write-back — a job whose tasks all run on one GPU
+  // (SHARP with double buffering) keeps its updated params in the GPU's cache and copies them
+  // to the host only on eviction and at the end of each pass. write_through: every backward
+  // writes its params back immediately (always the case for jobs spread over GPUs).
+  bool write_through = false;
 };
 
 struct ExecStats {
@@ -56,6 +61,7 @@ struct ExecStats {
   double elided_param_bytes = 0, elided_act_bytes = 0;
   double host_opt_params = 0;       // parameter updates done host-side
   double host_grad_d2h_bytes = 0, refresh_h2d_bytes = 0;  // their GradOffload / resident-slot refresh
+  double writeback_d2h_bytes = 0;   // params written back by the cache (eviction / pass end)
   std::vector<double> arena_bytes;  // per executed device: HBM reserved (<= mem_bytes)
   std::vector<double> device_busy_s;
   std::vector<double> enqueue_s;    // host time to enqueue a pass (per executed GPU)

@@ -90,6 +90,7 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   ex.host_opt_fraction = req.value("host_opt_fraction", 0.0);
   if (ex.host_opt_fraction < 0 || ex.host_opt_fraction > 1) throw InvalidArgument("host_opt_fraction must be in [0, 1]");
   ex.host_opt_threads = req.value("host_opt_threads", 0);
+  ex.write_through = req.value("write_through", false);
   const std::string prec = req.value("precision", std::string("tf32"));
   if (prec != "tf32" && prec != "fp32") throw InvalidArgument("precision must be 'tf32' or 'fp32'");
   ex.precision_fp32 = prec == "fp32";
@@ -161,6 +162,7 @@ ojson session_result(Session& S, bool with_trace) {
   st["host_opt_params_per_pass"] = r.stats.host_opt_params / np;
   st["host_grad_d2h_bytes_per_pass"] = r.stats.host_grad_d2h_bytes / np;
   st["refresh_h2d_bytes_per_pass"] = r.stats.refresh_h2d_bytes / np;
+  st["writeback_d2h_bytes_per_pass"] = r.stats.writeback_d2h_bytes / np;
   st["arena_bytes"] = r.stats.arena_bytes;
   st["pinned_bytes"] = r.stats.pinned_bytes;
   st["device_busy_s_last_pass"] = r.stats.device_busy_s.empty() ? 0.0 : r.stats.device_busy_s.back();

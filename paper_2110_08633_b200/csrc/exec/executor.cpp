@@ -142,6 +142,9 @@ struct HostJob {
   float* hgrad = nullptr;                            // pinned gradients of host layers
   std::vector<std::unique_ptr<Tracked>> hgrad_tr;    // per layer
   std::vector<std::unique_ptr<Tracked>> hparams_tr;  // per shard: host-side writes of params
+  // every task of the job on one GPU (SHARP with double buffering): its updated params may
+  // stay in that GPU's parameter cache and reach the host only on eviction / at pass end
+  bool write_back = false;
 };
 
 struct TaskTiming {
@@ -173,7 +176,8 @@ struct Worker {
     long off = 0, len = 0;
     long last_use = -1;
     Tracked tr;
-    std::vector<int> dirty;  // layers updated host-side since the slot was filled
+    std::vector<int> dirty;      // layers updated host-side since the slot was filled (refresh)
+    std::vector<int> gpu_dirty;  // layers updated in the slot, host copy stale (write back)
   };
   float* pool = nullptr;
   long pool_floats = 0;
@@ -221,7 +225,7 @@ struct Worker {
   int* rowidx = nullptr;   // [V + T]
   int* rowlist = nullptr;  // [M + T]
   int* rowcount = nullptr;
-  float* cbuf = nullptr;   // compact p | m | v of those rows
+  float* cbuf = nullptr;   // compact m | v (| p for write-through jobs) of those rows
   long crow_max = 0;
   Tracked rowidx_tr, cbuf_tr;
   float* scratch = nullptr;
@@ -274,6 +278,7 @@ struct ExecutorImpl {
   void param_read_begin(HostJob& hj, int s, cudaStream_t st);
   void param_read_end(HostJob& hj, int s, cudaStream_t st);
   Worker::PoolEntry* acquire_params(Worker& w, HostJob& hj, int j, int s, bool* loaded);
+  void write_back(Worker& w, Worker::PoolEntry& e);
   void collect(int pass, ExecResult& res);
 };
 
@@ -426,6 +431,15 @@ void ExecutorImpl::setup_worker(Worker& w) {
   check_cuda(cudaStreamCreateWithFlags(&w.hopt, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.opt2, cudaStreamNonBlocking), "stream");
   // Size the arena from the tasks this GPU will run.
+  bool all_write_back = true;
+  long model_f = 0;  // the largest job's parameters (all shards): what the cache can usefully hold
+  for (int t : w.tasks) {
+    const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
+    all_write_back = all_write_back && hj.write_back;
+    long sum = 0;
+    for (const ShardGeom& sg : hj.geom) sum += hy_pad32(sg.param_floats);
+    model_f = std::max(model_f, sum + 256L * static_cast<long>(hj.geom.size()));
+  }
   long slot_f = 0, embed_f = 0, layer_f = 0, act_f = 0, scratch_f = 0, tok_n = 0, idx_n = 0, list_n = 0, crow = 0;
   for (int t : w.tasks) {
     const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
@@ -447,14 +461,15 @@ void ExecutorImpl::setup_worker(Worker& w) {
   const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(embed_f) + 5 * hy_pad32(act_f) +
                            2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
                            hy_pad32(2 * static_cast<long>(w.tasks.size()) + 2) + hy_pad32(idx_n > 0 ? 32 + idx_n + list_n : 0) +
-                           hy_pad32(3 * crow);
+                           hy_pad32((all_write_back ? 2 : 3) * crow);
   const DeviceSpec& dev = cluster.devices[static_cast<size_t>(w.plan_dev)];
   const double cap = dev.mem_bytes + exec.hbm_slack_bytes;
   long budget_floats = static_cast<long>(cap / 4) - base_floats - 2048;
   // gradient ring: at least two of the largest non-embedding layers
   long ring_f = 2 * hy_pad32(layer_f) + 64;
   budget_floats -= ring_f;
-  // split-K partials (<= 16 MB) from what the cap leaves, then the Adam staging ring
+  // split-K partials (<= 16 MB) from what the cap leaves, the Adam staging ring, then the
+  // parameter cache beyond its two slots
   long splitk_f = std::min(4L << 20, std::max(0L, budget_floats / 4)) / 1024 * 1024;
   if (splitk_f < (256L << 10)) splitk_f = 0;
   budget_floats -= splitk_f;
@@ -476,9 +491,18 @@ void ExecutorImpl::setup_worker(Worker& w) {
     budget_floats -= std::max(0L, shard_f - ring_f);
     ring_f = std::max(ring_f, shard_f);
   }
+  // The parameter cache (LRU over shard entries) grows toward the whole of the largest job:
+  // shards that stay resident skip their ParamLoad (and, with write-back, their write-back)
+  // — physical traffic only, the plan is unchanged.
+  long pool_f = 2 * hy_pad32(slot_f);
+  if (budget_floats > 0 && model_f > pool_f) {
+    const long ext = std::min(budget_floats, model_f - pool_f) / 32 * 32;
+    pool_f += ext;
+    budget_floats -= ext;
+  }
   // spare budget deepens the gradient ring (up to 4 layers)
   if (budget_floats > 0) ring_f += std::min(budget_floats, 2 * hy_pad32(layer_f)) / 32 * 32;
-  const long floats = base_floats + ring_f + splitk_f + kStaging * 2 * hy_pad32(chunk);
+  const long floats = base_floats + ring_f + splitk_f + kStaging * 2 * hy_pad32(chunk) + (pool_f - 2 * hy_pad32(slot_f));
   w.arena_bytes = floats * 4 + 4096;
   if (static_cast<double>(w.arena_bytes) > cap) {
     throw InfeasibleOOM("sharp-executor", "(all jobs on this device)", dev.device_id,
@@ -491,8 +515,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
     p += hy_pad32(n);
     return r;
   };
-  w.pool = take(2 * hy_pad32(slot_f));
-  w.pool_floats = 2 * hy_pad32(slot_f);
+  w.pool = take(pool_f);
+  w.pool_floats = pool_f;
   w.gembed = embed_f > 0 ? take(embed_f) : nullptr;
   w.ring = take(ring_f);
   w.ring_floats = ring_f;
@@ -533,7 +557,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
     w.rowidx = ip + 32;
     w.rowlist = w.rowidx + idx_n;
     w.crow_max = crow;
-    w.cbuf = take(3 * crow);
+    w.cbuf = take((all_write_back ? 2 : 3) * crow);
   }
   w.loss_dev = reinterpret_cast<double*>(take(2 * static_cast<long>(w.tasks.size()) + 2));
   check_cuda(cudaMemset(w.arena, 0, static_cast<size_t>(w.arena_bytes)), "arena memset");
@@ -586,6 +610,16 @@ void ExecutorImpl::setup(ExecResult& res) {
     }
     workers.push_back(std::move(w));
   }
+  for (auto& kv : jobs) {
+    int dev = -1;
+    bool one = true;
+    for (size_t t = 0; t < tasks.size(); ++t) {
+      if (tasks[t].t.job != kv.first) continue;
+      if (dev < 0) dev = task_device[t];
+      one = one && task_device[t] == dev;
+    }
+    kv.second.write_back = one && !exec.write_through;
+  }
   for (auto& w : workers) setup_worker(*w);
   host_loss = static_cast<double*>(pinned(sizeof(double) * tasks.size()));
   host_threads = exec.host_opt_threads > 0 ? exec.host_opt_threads
@@ -631,14 +665,15 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
   char* hm = reinterpret_cast<char*>(hj.mom);
   char* hv = reinterpret_cast<char*>(hj.var);
   const int d = hj.m.d;
-  float* cp = w.cbuf;
-  char* cm = reinterpret_cast<char*>(w.cbuf + w.crow_max);
-  char* cv = cm + es * static_cast<size_t>(w.crow_max);
+  char* cm = reinterpret_cast<char*>(w.cbuf);
+  char* cv = cm + 4 * static_cast<size_t>(w.crow_max);
+  float* cp = w.cbuf + 2 * w.crow_max;
   if (part == 2) {
     check_cuda(cudaStreamWaitEvent(w.opt, w.dense_done, 0), "dense wait");
     w.cbuf_tr.before_write(w.opt);
     w.rowidx_tr.before_read(w.opt);
-    check_cuda(hy::adam_embed_rows(w.opt, hj.M + hj.m.T, w.rowcount, w.rowlist, d, base + slot_off, grads, cm, cv, cp,
+    check_cuda(hy::adam_embed_rows(w.opt, hj.M + hj.m.T, w.rowcount, w.rowlist, d, base + slot_off, grads, cm, cv,
+                                   hj.write_back ? nullptr : cp,
                                    bf16, h),
                "adam rows");
     ++w.st.kernel_launches;
@@ -647,7 +682,8 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
     if (done) check_cuda(cudaEventRecord(done, w.opt), "adam done");
     w.cbuf_tr.before_read(w.up);
     w.rowidx_tr.before_read(w.up);
-    check_cuda(hy::embed_rows_to_host(w.up, hj.M + hj.m.T, w.rowcount, w.rowlist, d, cp, cm, cv, hj.params + host_off,
+    check_cuda(hy::embed_rows_to_host(w.up, hj.M + hj.m.T, w.rowcount, w.rowlist, d, cp, cm, cv,
+                                      hj.write_back ? nullptr : hj.params + host_off,
                                       hm + es * host_off, hv + es * host_off, bf16),
                "rows to host");
     ++w.st.kernel_launches;
@@ -690,12 +726,16 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
     ++w.st.kernel_launches;
     stg.after_write(os);
     stg.before_read(w.up);
-    check_cuda(xfer(hj.params + host_off + off, base + slot_off + off, bytes, cudaMemcpyDeviceToHost, w.up), "p d2h");
+    if (!hj.write_back) {  // write-through (jobs spread over GPUs); else the cache writes back
+      check_cuda(xfer(hj.params + host_off + off, base + slot_off + off, bytes, cudaMemcpyDeviceToHost, w.up),
+                 "p d2h");
+      w.st.d2h_bytes += static_cast<double>(bytes);
+    }
     check_cuda(xfer(hm + hoff, sm, sbytes, cudaMemcpyDeviceToHost, w.up), "m d2h");
     check_cuda(xfer(hv + hoff, sv, sbytes, cudaMemcpyDeviceToHost, w.up), "v d2h");
     stg.after_read(w.up);
     w.st.opt_d2h_bytes += 2.0 * sbytes;
-    w.st.d2h_bytes += static_cast<double>(bytes) + 2.0 * sbytes;
+    w.st.d2h_bytes += 2.0 * sbytes;
   }
   if (part == 1) {
     w.rowidx_tr.after_read(w.opt2);
@@ -913,6 +953,7 @@ Worker::PoolEntry* ExecutorImpl::acquire_params(Worker& w, HostJob& hj, int j, i
       for (auto it = w.live.begin(); it != w.live.end(); ++it) victim = it;
     }
     if (victim == w.live.end()) throw InvalidArgument("parameter pool smaller than a shard");
+    write_back(w, **victim);
     w.retired.splice(w.retired.end(), w.live, victim);
     off = find_gap();
   }
@@ -937,6 +978,30 @@ Worker::PoolEntry* ExecutorImpl::acquire_params(Worker& w, HostJob& hj, int j, i
   *loaded = true;
   w.live.push_back(std::move(ent));
   return w.live.back().get();
+}
+
+// Write-back cache: the slot's GPU-updated layers -> host master params (up stream), before
+// the slot is reused or the host copy is read.
+void ExecutorImpl::write_back(Worker& w, Worker::PoolEntry& e) {
+  if (e.gpu_dirty.empty()) return;
+  HostJob& hj = jobs.at(e.tag.job);
+  const int s = e.tag.idx;
+  const long base = hy_layer_offset(&hj.m, hj.geom[static_cast<size_t>(s)].l0);
+  Tracked& ptr = *hj.params_tr[static_cast<size_t>(s)];
+  e.tr.before_read(w.up);
+  ptr.before_write(w.up);
+  for (int l : e.gpu_dirty) {
+    const long off = hy_layer_offset(&hj.m, l);
+    const long n = hy_layer_floats(&hj.m, l);
+    check_cuda(xfer(hj.params + off, w.pool + e.off + (off - base), sizeof(float) * static_cast<size_t>(n),
+                    cudaMemcpyDeviceToHost, w.up),
+               "param write-back");
+    w.st.d2h_bytes += 4.0 * n;
+    w.st.writeback_d2h_bytes += 4.0 * n;
+  }
+  ptr.after_write(w.up);
+  e.tr.after_read(w.up);
+  e.gpu_dirty.clear();
 }
 
 void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
@@ -1010,6 +1075,9 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   if (g.wte_offset >= 0) {
     const Tag wt{j, -1, -2, hj.version[0]};
     if (!(w.gembed_tag == wt)) {
+      for (auto& e : w.live) {
+        if (e->tag.job == j && e->tag.idx == 0) write_back(w, *e);
+      }
       w.gembed_tr.before_write(w.down);
       param_read_begin(hj, 0, w.down);
       const size_t wb = sizeof(float) * static_cast<size_t>(hj.m.V) * static_cast<size_t>(hj.m.d);
@@ -1205,6 +1273,14 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     }
     sink.flush();
     host_dirty = sink.host_layers;
+    if (hj.write_back) {
+      for (int l = g.l0; l < g.l1; ++l) {
+        if (!hj.host_layer[static_cast<size_t>(l)] &&
+            std::find(pe->gpu_dirty.begin(), pe->gpu_dirty.end(), l) == pe->gpu_dirty.end()) {
+          pe->gpu_dirty.push_back(l);
+        }
+      }
+    }
     mvt.after_read(w.opt);
     ptr.after_write(w.up);
     mvt.after_write(w.up);
@@ -1314,6 +1390,8 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
         }
         const auto h0 = std::chrono::steady_clock::now();
         for (int t : w.tasks) enqueue_task(w, t, pass);
+        // end of pass: the cache's updated params reach the host (they stay cached)
+        for (auto& e : w.live) write_back(w, *e);
         w.enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         // join all streams into comp, then record the end
         cudaStream_t others[5] = {w.down, w.up, w.opt, w.hopt, w.opt2};
@@ -1445,6 +1523,7 @@ void Executor::run(int passes, bool timed) {
       a.host_opt_params += b.host_opt_params;
       a.host_grad_d2h_bytes += b.host_grad_d2h_bytes;
       a.refresh_h2d_bytes += b.refresh_h2d_bytes;
+      a.writeback_d2h_bytes += b.writeback_d2h_bytes;
       a.elided_act_bytes += b.elided_act_bytes;
       a.kernel_launches += b.kernel_launches;
     }

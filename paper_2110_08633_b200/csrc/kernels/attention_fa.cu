@@ -77,13 +77,20 @@ __device__ __forceinline__ uint64_t desc_mn(const uint8_t* base, int kk) {
   return smem_desc_sw128_b32(smem_u32(base) + (kk >> 2) * 8192 + (kk & 3) * 1024, 4096, 512);
 }
 
-// Row r (of a K-major 128B-swizzled operand with k-block stride kb_bytes) <- 64 floats.
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// Row r (of a K-major 128B-swizzled operand with k-block stride kb_bytes) <- 64 floats,
+// rounded to TF32 (nearest, ties away) — the tensor core would otherwise truncate them.
 __device__ __forceinline__ void store_row64(uint8_t* base, int r, int kb_bytes, const float (&x)[64]) {
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
     const int kb = c >> 3, chunk = c & 7;
     float4* dst = reinterpret_cast<float4*>(base + kb * kb_bytes + r * 128 + ((chunk ^ (r & 7)) << 4));
-    *dst = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+    *dst = make_float4(tf32_rna(x[4 * c]), tf32_rna(x[4 * c + 1]), tf32_rna(x[4 * c + 2]), tf32_rna(x[4 * c + 3]));
   }
 }
 

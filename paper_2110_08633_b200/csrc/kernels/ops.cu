@@ -552,7 +552,7 @@ __global__ void adam_rows_kernel(const int* __restrict__ count, const int* __res
     const float upd = (mi / h.bc1) / (sqrtf(vi / h.bc2) + h.eps);
     const float pi = p[e] - h.lr * (upd + h.weight_decay * p[e]);
     p[e] = pi;
-    cp[i] = pi;
+    if (cp) cp[i] = pi;
     if constexpr (kBf16) {
       reinterpret_cast<__nv_bfloat16*>(cm)[i] = __float2bfloat16_rn(mi);
       reinterpret_cast<__nv_bfloat16*>(cv)[i] = __float2bfloat16_rn(vi);
@@ -574,7 +574,7 @@ __global__ void rows_to_host_kernel(const int* __restrict__ count, const int* __
   for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<long>(gridDim.x) * blockDim.x) {
     const long e = static_cast<long>(rows[i / d]) * d + i % d;
-    hp[e] = cp[i];
+    if (hp) hp[e] = cp[i];
     if constexpr (kEs == 2) {
       reinterpret_cast<uint16_t*>(hm)[e] = reinterpret_cast<const uint16_t*>(cm)[i];
       reinterpret_cast<uint16_t*>(hv)[e] = reinterpret_cast<const uint16_t*>(cv)[i];
