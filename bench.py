@@ -232,10 +232,10 @@ def run_hydra(args, cfg):
     else:
         h2d, d2h = st["h2d_bytes_per_pass"], st["d2h_bytes_per_pass"]
     if rank != 0:
+        ex.close()
         if dist:
             dist.barrier()
             dist.destroy_process_group()
-        ex.close()
         return None
     value = samples / dev_time
     out = {
@@ -287,6 +287,23 @@ def run_hydra(args, cfg):
         out["roofline"] = live_gemm_roofline(torch, cfg)
     except Exception as e:  # pragma: no cover
         out["roofline"] = {"error": str(e)}
+    ex.close()
+    if not args.no_variants and world == 1:
+        # same workload, Adam moments stored / streamed as bf16 (fp32 master params, TF32 GEMMs):
+        # parity stated separately (tests/test_executor_gpu.py::test_bf16_optimizer_state)
+        vreq = dict(req, opt_state="bf16" if args.opt_state == "fp32" else "fp32")
+        vex = P.Executor(cfg, **vreq)
+        vex.run(args.warmup, timed=False)
+        torch.cuda.synchronize()
+        vres = vex.run(args.steps, timed=True)
+        vt = sum(vres["pass_seconds"])
+        out["variants"] = {f"opt_state_{vreq['opt_state']}": {
+            "value": round(vres["samples_per_pass"] * args.steps / vt, 3), "unit": "samples/s",
+            "ms_per_step": round(vt / args.steps * 1e3, 3),
+            "shard_roofline_frac": round(virt / (vt / args.steps), 4),
+            "h2d_bytes_per_step": int(vres["stats"]["h2d_bytes_per_pass"]),
+            "d2h_bytes_per_step": int(vres["stats"]["d2h_bytes_per_pass"])}}
+        vex.close()
     if not args.no_cpu_baseline:
         try:
             secs, cores, _ = cpu_sample(cfg, starts=res["shard_starts"][0])
@@ -299,7 +316,6 @@ def run_hydra(args, cfg):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
-    ex.close()
     return out
 
 
@@ -358,8 +374,9 @@ def main():
     # optimizer placement (the reference keeps optimizer state host-side): the
     # fraction of each job's params updated by the host; the rest stream their fp32 moments
     # through HBM and are updated on the GPU
-    ap.add_argument("--host-opt-fraction", type=float, default=0.3)
+    ap.add_argument("--host-opt-fraction", type=float, default=0.0)
     ap.add_argument("--opt-state", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--no-variants", action="store_true", help="skip the other opt-state measurement")
     args = ap.parse_args()
     cfg = load_config(args.config)
     if args.impl == "reference":

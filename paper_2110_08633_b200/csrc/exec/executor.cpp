@@ -164,7 +164,7 @@ struct Worker {
   ExecutorImpl* ex = nullptr;
   int plan_dev = 0, cuda_dev = 0;
   std::vector<int> tasks;  // plan order
-  cudaStream_t comp{}, down{}, up{}, opt{}, opt2{}, hopt{};
+  cudaStream_t comp{}, down{}, up{}, opt{}, opt2{}, hopt{}, optin{};
   cudaEvent_t dense_done = nullptr;  // opt2: the embedding's early (non-token rows) update
   char* arena = nullptr;
   long arena_bytes = 0;
@@ -237,7 +237,7 @@ struct Worker {
   double enqueue_s = 0;
   std::vector<TaskTiming> timing;  // per local task index
   cudaEvent_t t0 = nullptr, t_end = nullptr;
-  cudaEvent_t join[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t join[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   ExecStats st;  // per pass accumulation (bytes)
 };
 
@@ -307,11 +307,12 @@ ExecutorImpl::~ExecutorImpl() {
     for (auto& e : w.retired) e->tr.destroy();
     w.gembed_tr.destroy();
     w.z_tr.destroy();
-    for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2], w.join[3], w.join[4], w.dense_done}) {
+    for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2], w.join[3], w.join[4], w.join[5],
+                          w.dense_done}) {
       if (e) cudaEventDestroy(e);
     }
     if (w.arena) cudaFree(w.arena);
-    for (cudaStream_t s : {w.comp, w.down, w.up, w.opt, w.opt2, w.hopt}) {
+    for (cudaStream_t s : {w.comp, w.down, w.up, w.opt, w.opt2, w.hopt, w.optin}) {
       if (s) cudaStreamDestroy(s);
     }
   }
@@ -430,6 +431,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
   check_cuda(cudaStreamCreateWithFlags(&w.opt, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.hopt, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.opt2, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithFlags(&w.optin, cudaStreamNonBlocking), "stream");
   // Size the arena from the tasks this GPU will run.
   bool all_write_back = true;
   long model_f = 0;  // the largest job's parameters (all shards): what the cache can usefully hold
@@ -656,6 +658,9 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
   h.bc1 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta1), step));
   h.bc2 = static_cast<float>(1.0 - std::pow(static_cast<double>(spec.beta2), step));
   cudaStream_t os = part == 1 ? w.opt2 : w.opt;
+  // m, v of a whole-layer update are prefetched on their own stream (optin) as soon as a
+  // staging chunk frees up — ahead of the gradient; only the Adam kernels wait for it
+  cudaStream_t is = part == 0 ? w.optin : os;
   // the layer's gradient is final and its params are no longer read by the compute stream
   cudaEvent_t ready = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
   check_cuda(cudaEventRecord(ready, w.comp), "layer ready");
@@ -705,9 +710,14 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
     char* sv = sm + es * static_cast<size_t>(chunk);
     Tracked& stg = w.stg_tr[si];
     const size_t hoff = es * static_cast<size_t>(host_off + off);
-    stg.before_write(os);
-    check_cuda(xfer(sm, hm + hoff, sbytes, cudaMemcpyHostToDevice, os), "m h2d");
-    check_cuda(xfer(sv, hv + hoff, sbytes, cudaMemcpyHostToDevice, os), "v h2d");
+    stg.before_write(is);
+    check_cuda(xfer(sm, hm + hoff, sbytes, cudaMemcpyHostToDevice, is), "m h2d");
+    check_cuda(xfer(sv, hv + hoff, sbytes, cudaMemcpyHostToDevice, is), "v h2d");
+    if (is != os) {
+      cudaEvent_t in = w.ev_pool[w.ev_next++ % w.ev_pool.size()];
+      check_cuda(cudaEventRecord(in, is), "mv in");
+      check_cuda(cudaStreamWaitEvent(os, in, 0), "mv in wait");
+    }
     w.st.opt_h2d_bytes += 2.0 * sbytes;
     w.st.h2d_bytes += 2.0 * sbytes;
     if (part == 1) {
@@ -1249,6 +1259,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     Tracked& ptr = *hj.params_tr[static_cast<size_t>(s)];
     Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
     mvt.before_read(w.opt);
+    mvt.before_read(w.optin);
     ptr.before_write(w.up);
     mvt.before_write(w.up);
     check_cuda(cudaEventRecord(tm.d0, w.up), "d0");
@@ -1282,6 +1293,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       }
     }
     mvt.after_read(w.opt);
+    mvt.after_read(w.optin);
     ptr.after_write(w.up);
     mvt.after_write(w.up);
     pe->tr.after_write(w.opt);  // Adam rewrote the params in place (opt waited for opt2)
@@ -1385,7 +1397,7 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
         g_debug_skip = exec.debug_skip;
         check_cuda(cudaDeviceSynchronize(), "pre-pass sync");
         check_cuda(cudaEventRecord(w.t0, w.comp), "t0");
-        for (cudaStream_t s : {w.down, w.up, w.opt, w.opt2, w.hopt}) {
+        for (cudaStream_t s : {w.down, w.up, w.opt, w.opt2, w.hopt, w.optin}) {
           check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");
         }
         const auto h0 = std::chrono::steady_clock::now();
@@ -1394,8 +1406,8 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
         for (auto& e : w.live) write_back(w, *e);
         w.enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         // join all streams into comp, then record the end
-        cudaStream_t others[5] = {w.down, w.up, w.opt, w.hopt, w.opt2};
-        for (int k = 0; k < 5; ++k) {
+        cudaStream_t others[6] = {w.down, w.up, w.opt, w.hopt, w.opt2, w.optin};
+        for (int k = 0; k < 6; ++k) {
           check_cuda(cudaEventRecord(w.join[k], others[k]), "join");
           check_cuda(cudaStreamWaitEvent(w.comp, w.join[k], 0), "join wait");
         }
