@@ -129,8 +129,10 @@ def cpu_sample(cfg, rows=1, starts=None):
 
 # ------------------------------------------------------------------------- GPU leg
 def live_gemm_roofline(torch, cfg):
-    """Dominant kernel (tcgen05 TF32 GEMM) at the workload's MLP shape, CUDA-event timed on
-    its launching stream, against a live cuBLAS TF32 peak."""
+    """Dominant kernel: the tcgen05 TF32 GEMM, measured at the workload's QKV projection
+    (X[M,d] W^T[d,3d] + bias, the first GEMM of every block forward), CUDA-event timed on its
+    launching stream, against a live cuBLAS TF32 peak (MEASURED_PEAKS.json carries bf16 only).
+    `traffic` = DRAM bytes of that launch from the committed ncu --set full capture."""
     from paper_2110_08633_b200 import kernels as K
 
     g = cfg["models"][0]["generator"]
@@ -138,21 +140,22 @@ def live_gemm_roofline(torch, cfg):
     M = g["batch_size"] * g["seq_len"]
     dev = torch.device("cuda")
     A = torch.randn(M, d, device=dev)
-    B = torch.randn(4 * d, d, device=dev)
-    C = torch.empty(M, 4 * d, device=dev)
+    B = torch.randn(3 * d, d, device=dev)
+    bias = torch.randn(3 * d, device=dev)
+    C = torch.empty(M, 3 * d, device=dev)
     for _ in range(5):
-        K.gemm(A, B, C=C)
+        K.gemm(A, B, C=C, bias=bias)
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     reps = 50
     torch.cuda.synchronize()
     e0.record(s)
     for _ in range(reps):
-        K.gemm(A, B, C=C)
+        K.gemm(A, B, C=C, bias=bias)
     e1.record(s)
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / 1e3 / reps
-    flops = 2.0 * M * 4 * d * d
+    flops = 2.0 * M * 3 * d * d
     torch.backends.cuda.matmul.allow_tf32 = True
     X = torch.randn(8192, 8192, device=dev)
     Y = torch.randn(8192, 8192, device=dev)
@@ -170,10 +173,21 @@ def live_gemm_roofline(torch, cfg):
     torch.backends.cuda.matmul.allow_tf32 = False
     del X, Y
     ach = flops / t / 1e12
-    return {"bound": "tensor", "kernel": f"gemm_tf32_kernel fc [{M}x{4*d}x{d}] (tcgen05 kind::tf32)",
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            tr = json.load(f)
+        if tr.get("shape") == [M, 3 * d, d]:
+            traffic = tr["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
+    return {"bound": "tensor", "kernel": f"gemm_tf32_kernel qkv [{M}x{3*d}x{d}] +bias (tcgen05 kind::tf32)",
             "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-            "peak_source": "live cuBLAS TF32 8192^3 (MEASURED_PEAKS.json has no TF32 figure)",
-            "traffic": None, "launch_us": round(t * 1e6, 2)}
+            "peak_source": "live cuBLAS TF32 8192^3 in this run (MEASURED_PEAKS.json has no TF32 figure; "
+                           "nominal dense TF32 1100)",
+            "frac_of_nominal_tf32": round(ach / 1100.0, 4),
+            "traffic": traffic, "algorithmic_bytes": int(4 * (M * d + 3 * d * d + 3 * d + M * 3 * d)),
+            "launch_us": round(t * 1e6, 2)}
 
 
 def shard_roofline(res, per_rank_time, link_GBps):
