@@ -60,7 +60,10 @@ void gemm(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a
   check_cuda(gemm_tf32(st, M, N, K, A, lda, amn, B, ldb, bmn, e), "gemm");
 }
 
-void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const float* h_in, float* h_out, Scratch& s) {
+// keep_h: also store the MLP pre-activation (s.fc), which only the backward's GELU' needs; the
+// forward tasks and the backward's stash recompute skip that M x 4d write.
+void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const float* h_in, float* h_out, Scratch& s,
+                   bool keep_h) {
   const int M = s.M, d = m.d;
   { HY_PROF(st, "ln1");
   check_cuda(layernorm_fwd(st, M, d, h_in, bt(w, d, HY_LN1_G), bt(w, d, HY_LN1_B), s.ln1, s.mean1, s.rstd1), "ln1");
@@ -86,7 +89,7 @@ void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const floa
   }
   { HY_PROF(st, "fc");
   gemm(st, M, 4 * d, d, s.ln2, d, false, bt(w, d, HY_WFC), d, false, s.act, 4 * d, bt(w, d, HY_BFC), nullptr, 0, 0.f,
-       kEpiGelu, s.fc, nullptr, 4 * d);
+       kEpiGelu, keep_h ? s.fc : nullptr, nullptr, 4 * d);
   }
   { HY_PROF(st, "mlp_proj");
   gemm(st, M, d, 4 * d, s.act, 4 * d, false, bt(w, d, HY_WPR), 4 * d, false, h_out, d, bt(w, d, HY_BPR), s.hmid, d);
@@ -266,7 +269,7 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
   for (int l = b0; l < b1; ++l) {
     float* dst = (cur == s.tmp_h) ? s.stash : s.tmp_h;
     if (write_out && l == b1 - 1) dst = io.act_out;
-    block_forward(st, m, slot + lo(m, l, g.l0), cur, dst, s);
+    block_forward(st, m, slot + lo(m, l, g.l0), cur, dst, s, false);
     cur = dst;
   }
   if (g.has_head) {
@@ -304,12 +307,13 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   } else {
     check_cuda(cudaMemcpyAsync(s.stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
   }
-  for (int i = 0; i < nb; ++i) {
-    block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, s.stash + (i + 1) * n, s);
-  }
   // The last block's intermediates survive in scratch unless the head pass (whose logits
   // alias the MLP buffers) runs in between: then its recompute can be skipped.
   bool last_block_live = nb > 0 && !g.has_head;
+  for (int i = 0; i < nb; ++i) {
+    block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, s.stash + (i + 1) * n, s,
+                  last_block_live && i == nb - 1);
+  }
   // 2) gradient wrt the shard output
   float* dh = s.tmp_h;
   if (g.has_head) {
@@ -333,7 +337,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     const int layer = b0 + i;
     const float* w = slot + lo(m, layer, g.l0);
     if (!(last_block_live && i == nb - 1)) {
-      block_forward(st, m, w, s.stash + i * n, s.stash + (i + 1) * n, s);  // block output is scratch here
+      block_forward(st, m, w, s.stash + i * n, s.stash + (i + 1) * n, s, true);  // block output is scratch here
     }
     float* gw = sink.acquire(layer);
     block_backward(st, m, w, gw, s.stash + i * n, dh, s);

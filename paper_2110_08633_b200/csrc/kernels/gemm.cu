@@ -382,7 +382,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
               xe[e] = y;
             }
             const long grow = row0 + r;
-            if (epi.mode == kEpiGelu) *reinterpret_cast<float4*>(epi.Hout + grow * epi.ldho + col) = h;
+            if (epi.mode == kEpiGelu && epi.Hout) *reinterpret_cast<float4*>(epi.Hout + grow * epi.ldho + col) = h;
             *reinterpret_cast<float4*>(Cb + grow * epi.ldc + col) = x[it];
           }
         } else {
@@ -398,7 +398,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
               } else {
                 y += bias_v;
                 if (epi.mode == kEpiGelu) {
-                  epi.Hout[grow * epi.ldho + colx] = y;
+                  if (epi.Hout) epi.Hout[grow * epi.ldho + colx] = y;
                   y = gelu_tanh(y);
                 } else {
                   if (epi.R) y += epi.R[grow * epi.ldr + colx];

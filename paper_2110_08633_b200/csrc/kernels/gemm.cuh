@@ -7,7 +7,7 @@ namespace hy {
 
 enum EpiMode : int {
   kEpiStore = 0,    // C = beta*C + acc (+bias) (+R)
-  kEpiGelu = 1,     // Hout = acc + bias ; C = gelu(Hout)
+  kEpiGelu = 1,     // Hout = acc + bias (skipped when Hout is null) ; C = gelu(acc + bias)
   kEpiGeluBwd = 2,  // C = (acc) * gelu'(Hin)
 };
 

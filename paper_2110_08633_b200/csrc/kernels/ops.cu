@@ -281,6 +281,97 @@ __global__ void xent_kernel(int V, float* __restrict__ logits, long ldl, const i
   if (tid == 0) row_loss[row] = logf(gs) + gm - zt;
 }
 
+// Register-resident variant (V <= 512 * 4 * kV4): the row is read from HBM once into
+// registers as float4 (rows are 16-byte aligned: ldl = HY_VOCAB_PAD), reduced for max and
+// sum, and written once — 2 x V x 4 bytes of traffic instead of 3 passes.
+template <int kV4>
+__global__ void __launch_bounds__(512) xent_reg_kernel(int V, float* __restrict__ logits, long ldl,
+                                                       const int32_t* __restrict__ targets, float grad_scale,
+                                                       float* __restrict__ row_loss) {
+  __shared__ float red[32];
+  __shared__ float bcast;
+  const int row = blockIdx.x;
+  float* lr = logits + static_cast<long>(row) * ldl;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n4 = V >> 2;  // full float4s; V & 3 tail elements handled by thread 0
+  float4 z[kV4];
+  float m = -FLT_MAX;
+#pragma unroll
+  for (int k = 0; k < kV4; ++k) {
+    const int i4 = tid + k * 512;
+    if (i4 < n4) {
+      z[k] = reinterpret_cast<const float4*>(lr)[i4];
+      m = fmaxf(m, fmaxf(fmaxf(z[k].x, z[k].y), fmaxf(z[k].z, z[k].w)));
+    }
+  }
+  float tail[3] = {-FLT_MAX, -FLT_MAX, -FLT_MAX};
+  if (tid == 0) {
+    for (int t = 0; t < (V & 3); ++t) {
+      tail[t] = lr[4 * n4 + t];
+      m = fmaxf(m, tail[t]);
+    }
+  }
+  m = warp_max(m);
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  if (warp == 0) {
+    float x = lane < 16 ? red[lane] : -FLT_MAX;
+    x = warp_max(x);
+    if (lane == 0) bcast = x;
+  }
+  __syncthreads();
+  const float gm = bcast;
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < kV4; ++k) {
+    const int i4 = tid + k * 512;
+    if (i4 < n4) {
+      z[k].x = __expf(z[k].x - gm);
+      z[k].y = __expf(z[k].y - gm);
+      z[k].z = __expf(z[k].z - gm);
+      z[k].w = __expf(z[k].w - gm);
+      s += (z[k].x + z[k].y) + (z[k].z + z[k].w);
+    }
+  }
+  if (tid == 0) {
+    for (int t = 0; t < (V & 3); ++t) {
+      tail[t] = __expf(tail[t] - gm);
+      s += tail[t];
+    }
+  }
+  s = warp_sum(s);
+  __syncthreads();
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  if (warp == 0) {
+    float x = lane < 16 ? red[lane] : 0.f;
+    x = warp_sum(x);
+    if (lane == 0) bcast = x;
+  }
+  __syncthreads();
+  const float gs = bcast;
+  const int tgt = targets[row];
+  const float zt = lr[tgt];  // read before this thread block overwrites the row
+  __syncthreads();
+  const float sc = grad_scale / gs;
+#pragma unroll
+  for (int k = 0; k < kV4; ++k) {
+    const int i4 = tid + k * 512;
+    if (i4 < n4) {
+      float4 o = make_float4(z[k].x * sc, z[k].y * sc, z[k].z * sc, z[k].w * sc);
+      if ((tgt >> 2) == i4) (&o.x)[tgt & 3] -= grad_scale;
+      reinterpret_cast<float4*>(lr)[i4] = o;
+    }
+  }
+  if (tid == 0) {
+    for (int t = 0; t < (V & 3); ++t) {
+      const int i = 4 * n4 + t;
+      lr[i] = tail[t] * sc - (i == tgt ? grad_scale : 0.f);
+    }
+    row_loss[row] = logf(gs) + gm - zt;
+  }
+}
+
 __global__ void sum_double_kernel(int n, const float* __restrict__ x, double* __restrict__ out, int accumulate) {
   __shared__ double sh[256];
   double s = 0.0;
@@ -685,7 +776,11 @@ cudaError_t softmax_xent(cudaStream_t s, int rows, int V, float* logits, long ld
                          float grad_scale, float* row_loss) {
   if (rows <= 0) return cudaSuccess;
   count_launch();
-  xent_kernel<<<rows, 512, 0, s>>>(V, logits, ldl, targets, grad_scale, row_loss);
+  if (V <= 512 * 4 * 25 && (ldl & 3) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
+    xent_reg_kernel<25><<<rows, 512, 0, s>>>(V, logits, ldl, targets, grad_scale, row_loss);
+  } else {
+    xent_kernel<<<rows, 512, 0, s>>>(V, logits, ldl, targets, grad_scale, row_loss);
+  }
   return cudaGetLastError();
 }
 

@@ -216,8 +216,11 @@ def test_embedding():
     assert rel(dwpe, dh.view(B, T, d).sum(0)) < 1e-5
 
 
-def test_softmax_xent():
-    rows, V, Vp = 77, 50257, 50304
+@pytest.mark.parametrize("V,Vp", [(50257, 50304), (1000, 1003), (30001, 30004)])
+def test_softmax_xent(V, Vp):
+    """Register-resident path (16-byte aligned rows, V & 3 tail), and the 3-pass fallback
+    (unaligned row stride)."""
+    rows = 77
     logits = torch.randn(rows, Vp, device=dev) * 3
     tgt = torch.randint(0, V, (rows,), device=dev, dtype=torch.int32)
     lr = logits[:, :V].clone().requires_grad_(True)
