@@ -127,6 +127,36 @@ def cpu_sample(cfg, rows=1, starts=None):
     return time.perf_counter() - t0, O.lib().oracle_threads(), starts
 
 
+# ------------------------------------------------------------------------- rank shares
+def plan_share(cfg, n, rank):
+    """What rank `rank` of an N-GPU run executes: the tasks the SHARP plan (G=n, the
+    reference's dispatch order, sim.cpp:524-527) puts on device `rank`. With double
+    buffering a job never spans two devices, so shares are disjoint job sets
+    and ranks exchange nothing but the timing reduce."""
+    import paper_2110_08633_b200 as P
+
+    plan = P.plan(cfg, gpus=n)
+    tasks = plan["tasks"]
+    mine = [t for t, dev, _ in plan["dispatch"] if dev == rank]
+    jobs = sorted({tasks[t]["job"] for t in mine})
+    samples = sum(cfg["jobs"][j]["batch_size"] for t in mine for j in [tasks[t]["job"]]
+                  if tasks[t]["shard"] == 0 and tasks[t]["dir"] in (0, "F", "fwd"))
+    return {"tasks": mine, "jobs": jobs, "samples": samples, "dispatch_hash": plan["dispatch_hash"],
+            "virtual_makespan_s": plan["makespan_s"]}
+
+
+def reduce_over_ranks(dist, device, dev_time, wall, samples, h2d, d2h, launches):
+    """Max of the per-rank times, sum of the per-rank work (the N>1 contract: value = units
+    all ranks processed / max-over-ranks time)."""
+    import torch
+
+    t = torch.tensor([dev_time, wall], device=device, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot = torch.tensor([samples, h2d, d2h, launches], device=device, dtype=torch.float64)
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    return t.tolist() + tot.tolist()
+
+
 # ------------------------------------------------------------------------- GPU leg
 def live_gemm_roofline(torch, cfg):
     """Dominant kernel: the tcgen05 TF32 GEMM, measured at the workload's QKV projection
@@ -236,13 +266,8 @@ def run_hydra(args, cfg):
     samples = res["samples_per_pass"] * args.steps
     st = res["stats"]
     if dist:
-        t = torch.tensor([dev_time, wall], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_time, wall = t.tolist()
-        tot = torch.tensor([samples, st["h2d_bytes_per_pass"], st["d2h_bytes_per_pass"], launches_t],
-                           device="cuda", dtype=torch.float64)
-        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
-        samples, h2d, d2h, launches_t = tot.tolist()
+        dev_time, wall, samples, h2d, d2h, launches_t = reduce_over_ranks(
+            dist, "cuda", dev_time, wall, samples, st["h2d_bytes_per_pass"], st["d2h_bytes_per_pass"], launches_t)
     else:
         h2d, d2h = st["h2d_bytes_per_pass"], st["d2h_bytes_per_pass"]
     if rank != 0:
