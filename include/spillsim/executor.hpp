@@ -51,6 +51,10 @@ struct ExecOptions {
   // to the host only on eviction and at the end of each pass. write_through: every backward
   // writes its params back immediately (always the case for jobs spread over GPUs).
   bool write_through = false;
+  // Optimizer-state cache: HBM left under the cap after every other region keeps whole
+  // layers' moments resident across the owning job's minibatches (write-back jobs only).
+  bool mv_cache = true;
+  double mv_cache_max_bytes = -1;  // < 0: no limit beyond the cap (tests use a small limit)
 };
 
 struct ExecStats {
@@ -62,6 +66,9 @@ struct ExecStats {
   double host_opt_params = 0;       // parameter updates done host-side
   double host_grad_d2h_bytes = 0, refresh_h2d_bytes = 0;  // their GradOffload / resident-slot refresh
   double writeback_d2h_bytes = 0;   // params written back by the cache (eviction / pass end)
+  double mv_load_h2d_bytes = 0, mv_writeback_d2h_bytes = 0;  // moment cache fills / write-backs
+  double mv_resident_updates = 0;   // parameter updates whose moments were HBM-resident
+  std::vector<double> mv_cache_bytes;  // per executed device: HBM given to the moment cache
   std::vector<double> arena_bytes;  // per executed device: HBM reserved (<= mem_bytes)
   std::vector<double> device_busy_s;
   std::vector<double> enqueue_s;    // host time to enqueue a pass (per executed GPU)

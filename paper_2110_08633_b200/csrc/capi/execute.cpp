@@ -91,6 +91,8 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   if (ex.host_opt_fraction < 0 || ex.host_opt_fraction > 1) throw InvalidArgument("host_opt_fraction must be in [0, 1]");
   ex.host_opt_threads = req.value("host_opt_threads", 0);
   ex.write_through = req.value("write_through", false);
+  ex.mv_cache = req.value("mv_cache", true);
+  ex.mv_cache_max_bytes = req.value("mv_cache_max_bytes", -1.0);
   const std::string prec = req.value("precision", std::string("tf32"));
   if (prec != "tf32" && prec != "fp32") throw InvalidArgument("precision must be 'tf32' or 'fp32'");
   ex.precision_fp32 = prec == "fp32";
@@ -163,6 +165,10 @@ ojson session_result(Session& S, bool with_trace) {
   st["host_grad_d2h_bytes_per_pass"] = r.stats.host_grad_d2h_bytes / np;
   st["refresh_h2d_bytes_per_pass"] = r.stats.refresh_h2d_bytes / np;
   st["writeback_d2h_bytes_per_pass"] = r.stats.writeback_d2h_bytes / np;
+  st["mv_load_h2d_bytes_per_pass"] = r.stats.mv_load_h2d_bytes / np;
+  st["mv_writeback_d2h_bytes_per_pass"] = r.stats.mv_writeback_d2h_bytes / np;
+  st["mv_resident_updates_per_pass"] = r.stats.mv_resident_updates / np;
+  st["mv_cache_bytes"] = r.stats.mv_cache_bytes;
   st["arena_bytes"] = r.stats.arena_bytes;
   st["pinned_bytes"] = r.stats.pinned_bytes;
   st["device_busy_s_last_pass"] = r.stats.device_busy_s.empty() ? 0.0 : r.stats.device_busy_s.back();

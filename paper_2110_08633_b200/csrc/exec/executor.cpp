@@ -127,6 +127,7 @@ struct Tag {
 
 struct HostJob {
   const ExecJob* spec = nullptr;
+  int job = -1;
   hy_dims m{};
   long M = 0, n_act = 0, total = 0;
   std::vector<ShardGeom> geom;
@@ -228,6 +229,26 @@ struct Worker {
   float* cbuf = nullptr;   // compact m | v (| p for write-through jobs) of those rows
   long crow_max = 0;
   Tracked rowidx_tr, cbuf_tr;
+  // Optimizer-state cache: the HBM the cap leaves after every other region keeps whole
+  // layers' Adam moments resident across the minibatches of the job that owns it (write-back:
+  // the host copy is refreshed when ownership passes to the next job on this GPU and at the
+  // end of each pass). Layers that do not fit stream through the staging ring as before.
+  struct MvEntry {
+    int layer = -1;
+    long off = 0, bytes = 0;  // m at off, v at off + bytes / 2
+    bool valid = false, dirty = false;
+    Tracked tr;
+  };
+  char* mvpool = nullptr;
+  long mvpool_bytes = 0, mvpool_used = 0;
+  int mv_owner = -1;                         // job whose moments the pool holds
+  int mv_owner_pass = -1;                    // last pass in which the owner used the pool
+  std::map<int, std::unique_ptr<MvEntry>> mv_live;  // layer -> entry (owner's)
+  std::vector<std::unique_ptr<MvEntry>> mv_retired;
+  cudaEvent_t mv_free = nullptr;             // up: previous owner's write-back done
+  bool mv_free_pending = false;
+  std::map<int, int> last_local_of_job;      // job -> its last local task index on this GPU
+  int cur_local = -1, cur_pass = -1;
   float* scratch = nullptr;
   double* loss_dev = nullptr;  // per task slot
   int last_slot = -1;
@@ -278,6 +299,8 @@ struct ExecutorImpl {
   void param_read_begin(HostJob& hj, int s, cudaStream_t st);
   void param_read_end(HostJob& hj, int s, cudaStream_t st);
   Worker::PoolEntry* acquire_params(Worker& w, HostJob& hj, int j, int s, bool* loaded);
+  Worker::MvEntry* acquire_moments(Worker& w, HostJob& hj, int layer, long bytes);
+  void release_moments(Worker& w, bool keep);
   void write_back(Worker& w, Worker::PoolEntry& e);
   void collect(int pass, ExecResult& res);
 };
@@ -305,6 +328,9 @@ ExecutorImpl::~ExecutorImpl() {
     if (w.gembed_free) cudaEventDestroy(w.gembed_free);
     for (auto& e : w.live) e->tr.destroy();
     for (auto& e : w.retired) e->tr.destroy();
+    for (auto& kv : w.mv_live) kv.second->tr.destroy();
+    for (auto& e : w.mv_retired) e->tr.destroy();
+    if (w.mv_free) cudaEventDestroy(w.mv_free);
     w.gembed_tr.destroy();
     w.z_tr.destroy();
     for (cudaEvent_t e : {w.t0, w.t_end, w.join[0], w.join[1], w.join[2], w.join[3], w.join[4], w.join[5],
@@ -352,6 +378,7 @@ void ExecutorImpl::setup_host_job(int j) {
   HostJob& hj = jobs[j];
   const ExecJob& spec = exec.jobs.at(static_cast<size_t>(j));
   hj.spec = &spec;
+  hj.job = j;
   hj.m = spec.dims;
   hj.M = static_cast<long>(hj.m.B) * hj.m.T;
   hj.n_act = hj.M * hj.m.d;
@@ -477,7 +504,9 @@ void ExecutorImpl::setup_worker(Worker& w) {
   budget_floats -= splitk_f;
   long chunk = std::min(exec.opt_chunk_floats, budget_floats / (2 * kStaging));
   chunk = chunk / 1024 * 1024;
-  w.stg_alias = chunk < (1L << 20);
+  // alias the staging ring onto the scratch only when the cap leaves no room for the
+  // requested chunks (or for 1M-element chunks, whichever is smaller)
+  w.stg_alias = chunk < std::min(exec.opt_chunk_floats / 1024 * 1024, 1L << 20);
   if (w.stg_alias) chunk = 0;
   budget_floats -= kStaging * 2 * hy_pad32(chunk);
   if (w.stg_alias) {
@@ -503,8 +532,27 @@ void ExecutorImpl::setup_worker(Worker& w) {
     budget_floats -= ext;
   }
   // spare budget deepens the gradient ring (up to 4 layers)
-  if (budget_floats > 0) ring_f += std::min(budget_floats, 2 * hy_pad32(layer_f)) / 32 * 32;
-  const long floats = base_floats + ring_f + splitk_f + kStaging * 2 * hy_pad32(chunk) + (pool_f - 2 * hy_pad32(slot_f));
+  if (budget_floats > 0) {
+    const long deep = std::min(budget_floats, 2 * hy_pad32(layer_f)) / 32 * 32;
+    ring_f += deep;
+    budget_floats -= deep;
+  }
+  // ... and what is still left keeps optimizer moments resident (write-back jobs only)
+  long mv_f = 0;
+  if (exec.mv_cache && all_write_back && !w.stg_alias && budget_floats > (2L << 20)) {
+    long job_mv_f = 0;  // the largest job's moments: what the cache can usefully hold
+    const long es = exec.opt_state_bf16 ? 2 : 4;
+    for (int t : w.tasks) {
+      const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
+      job_mv_f = std::max(job_mv_f, (2 * es * hj.total) / 4 + 64L * (hj.m.L + 2));
+    }
+    mv_f = std::min(budget_floats - (1L << 20), job_mv_f);
+    if (exec.mv_cache_max_bytes >= 0) mv_f = std::min(mv_f, static_cast<long>(exec.mv_cache_max_bytes / 4));
+    mv_f = mv_f / 256 * 256;
+    budget_floats -= mv_f;
+  }
+  const long floats = base_floats + ring_f + splitk_f + kStaging * 2 * hy_pad32(chunk) + (pool_f - 2 * hy_pad32(slot_f)) +
+                      mv_f;
   w.arena_bytes = floats * 4 + 4096;
   if (static_cast<double>(w.arena_bytes) > cap) {
     throw InfeasibleOOM("sharp-executor", "(all jobs on this device)", dev.device_id,
@@ -562,6 +610,14 @@ void ExecutorImpl::setup_worker(Worker& w) {
     w.cbuf = take((all_write_back ? 2 : 3) * crow);
   }
   w.loss_dev = reinterpret_cast<double*>(take(2 * static_cast<long>(w.tasks.size()) + 2));
+  if (mv_f > 0) {
+    w.mvpool = reinterpret_cast<char*>(take(mv_f));
+    w.mvpool_bytes = 4 * mv_f;
+  }
+  for (size_t i = 0; i < w.tasks.size(); ++i) {
+    w.last_local_of_job[tasks[static_cast<size_t>(w.tasks[i])].t.job] = static_cast<int>(i);
+  }
+  w.mv_free = new_event(false);
   check_cuda(cudaMemset(w.arena, 0, static_cast<size_t>(w.arena_bytes)), "arena memset");
   w.timing.resize(w.tasks.size());
   for (TaskTiming& tm : w.timing) {
@@ -696,6 +752,45 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
     w.cbuf_tr.after_read(w.up);
     return;
   }
+  if (part == 0) {
+    const long half = (static_cast<long>(es) * nfl + 511) / 512 * 512;
+    if (Worker::MvEntry* e = acquire_moments(w, hj, layer, 2 * half)) {
+      char* dm = w.mvpool + e->off;
+      char* dv = dm + half;
+      const size_t sbytes = es * static_cast<size_t>(nfl);
+      const size_t hoff = es * static_cast<size_t>(host_off);
+      if (!e->valid) {  // first update of this layer since the job took the cache: load once
+        if (w.mv_free_pending) {
+          check_cuda(cudaStreamWaitEvent(w.optin, w.mv_free, 0), "mv free wait");
+          w.mv_free_pending = false;
+        }
+        e->tr.before_write(w.optin);
+        check_cuda(xfer(dm, hm + hoff, sbytes, cudaMemcpyHostToDevice, w.optin), "m load");
+        check_cuda(xfer(dv, hv + hoff, sbytes, cudaMemcpyHostToDevice, w.optin), "v load");
+        e->tr.after_write(w.optin);
+        e->valid = true;
+        w.st.opt_h2d_bytes += 2.0 * sbytes;
+        w.st.h2d_bytes += 2.0 * sbytes;
+        w.st.mv_load_h2d_bytes += 2.0 * sbytes;
+      }
+      e->tr.before_write(os);
+      if (bf16) {
+        check_cuda(hy::adam_update_bf16(os, nfl, base + slot_off, grads, reinterpret_cast<uint16_t*>(dm),
+                                        reinterpret_cast<uint16_t*>(dv), h),
+                   "adam bf16 (resident moments)");
+      } else {
+        check_cuda(hy::adam_update(os, nfl, base + slot_off, grads, reinterpret_cast<float*>(dm),
+                                   reinterpret_cast<float*>(dv), h),
+                   "adam (resident moments)");
+      }
+      ++w.st.kernel_launches;
+      e->tr.after_write(os);
+      e->dirty = true;
+      w.st.mv_resident_updates += static_cast<double>(nfl);
+      if (done) check_cuda(cudaEventRecord(done, os), "adam done");
+      return;
+    }
+  }
   if (part == 1) {
     w.cbuf_tr.before_write(w.opt2);
     w.rowidx_tr.before_read(w.opt2);
@@ -754,6 +849,75 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
     return;
   }
   if (done) check_cuda(cudaEventRecord(done, w.opt), "adam done");
+}
+
+// Moment-cache entry of `layer` for the job `hj` (nullptr: stream it through the staging ring).
+// The pool belongs to one job at a time; ownership passes to the next job only once the owner
+// has no task left on this GPU in this pass (SHARP runs a GPU's jobs one after another), so
+// entries are never thrashed between interleaved jobs.
+Worker::MvEntry* ExecutorImpl::acquire_moments(Worker& w, HostJob& hj, int layer, long bytes) {
+  if (!w.mvpool || !hj.write_back) return nullptr;
+  if (w.mv_owner != hj.job) {
+    if (w.mv_owner >= 0) {
+      // the owner still has tasks ahead of it on this GPU in this pass: stream instead
+      auto it = w.last_local_of_job.find(w.mv_owner);
+      if (w.mv_owner_pass == w.cur_pass && it != w.last_local_of_job.end() && it->second > w.cur_local) return nullptr;
+      release_moments(w, false);
+    }
+    w.mv_owner = hj.job;
+  }
+  w.mv_owner_pass = w.cur_pass;
+  auto it = w.mv_live.find(layer);
+  if (it != w.mv_live.end()) return it->second.get();
+  if (w.mvpool_used + bytes > w.mvpool_bytes) return nullptr;
+  auto e = std::make_unique<Worker::MvEntry>();
+  e->layer = layer;
+  e->off = w.mvpool_used;
+  e->bytes = bytes;
+  w.mvpool_used += bytes;
+  Worker::MvEntry* r = e.get();
+  w.mv_live[layer] = std::move(e);
+  return r;
+}
+
+// Write the owner's updated moments back to its host state (up stream). keep = true (end of
+// a pass): entries stay resident and valid for the owner's next pass; false: the pool is
+// handed over — `mv_free` (up) marks when the next owner may overwrite it.
+void ExecutorImpl::release_moments(Worker& w, bool keep) {
+  if (w.mv_owner < 0) return;
+  HostJob& hj = jobs.at(w.mv_owner);
+  const size_t es = exec.opt_state_bf16 ? 2 : 4;
+  char* hm = reinterpret_cast<char*>(hj.mom);
+  char* hv = reinterpret_cast<char*>(hj.var);
+  for (auto& kv : w.mv_live) {
+    Worker::MvEntry& e = *kv.second;
+    e.tr.before_read(w.up);
+    if (e.dirty) {
+      int s = 0;
+      while (s + 1 < static_cast<int>(hj.geom.size()) && hj.geom[static_cast<size_t>(s) + 1].l0 <= e.layer) ++s;
+      Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
+      const long nfl = hy_layer_floats(&hj.m, e.layer);
+      const size_t sbytes = es * static_cast<size_t>(nfl);
+      const size_t hoff = es * static_cast<size_t>(hy_layer_offset(&hj.m, e.layer));
+      const long half = e.bytes / 2;
+      mvt.before_write(w.up);
+      check_cuda(xfer(hm + hoff, w.mvpool + e.off, sbytes, cudaMemcpyDeviceToHost, w.up), "m write-back");
+      check_cuda(xfer(hv + hoff, w.mvpool + e.off + half, sbytes, cudaMemcpyDeviceToHost, w.up), "v write-back");
+      mvt.after_write(w.up);
+      w.st.opt_d2h_bytes += 2.0 * sbytes;
+      w.st.d2h_bytes += 2.0 * sbytes;
+      w.st.mv_writeback_d2h_bytes += 2.0 * sbytes;
+      e.dirty = false;
+    }
+    e.tr.after_read(w.up);
+  }
+  if (keep) return;
+  check_cuda(cudaEventRecord(w.mv_free, w.up), "mv free");
+  w.mv_free_pending = true;
+  for (auto& kv : w.mv_live) w.mv_retired.push_back(std::move(kv.second));
+  w.mv_live.clear();
+  w.mvpool_used = 0;
+  w.mv_owner = -1;
 }
 
 // Host-placed layer: GradOffload of the layer's gradient (up), then AdamW on the host
@@ -1024,6 +1188,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   const int gmb = pass * job_mb[static_cast<size_t>(j)] + task.t.minibatch;
   const bool fwd = task.t.direction == Direction::kForward;
   const int local = task_local[static_cast<size_t>(t)];
+  w.cur_local = local;
+  w.cur_pass = pass;
   TaskTiming& tm = w.timing[static_cast<size_t>(local)];
   const size_t act_bytes = sizeof(float) * static_cast<size_t>(hj.n_act);
 
@@ -1404,6 +1570,7 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
         for (int t : w.tasks) enqueue_task(w, t, pass);
         // end of pass: the cache's updated params reach the host (they stay cached)
         for (auto& e : w.live) write_back(w, *e);
+        release_moments(w, true);
         w.enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         // join all streams into comp, then record the end
         cudaStream_t others[6] = {w.down, w.up, w.opt, w.hopt, w.opt2, w.optin};
@@ -1536,6 +1703,9 @@ void Executor::run(int passes, bool timed) {
       a.host_grad_d2h_bytes += b.host_grad_d2h_bytes;
       a.refresh_h2d_bytes += b.refresh_h2d_bytes;
       a.writeback_d2h_bytes += b.writeback_d2h_bytes;
+      a.mv_load_h2d_bytes += b.mv_load_h2d_bytes;
+      a.mv_writeback_d2h_bytes += b.mv_writeback_d2h_bytes;
+      a.mv_resident_updates += b.mv_resident_updates;
       a.elided_act_bytes += b.elided_act_bytes;
       a.kernel_launches += b.kernel_launches;
     }
@@ -1544,7 +1714,11 @@ void Executor::run(int passes, bool timed) {
   for (double x : res_.pass_seconds) total += x;
   res_.stats.makespan_s = res_.pass_seconds.empty() ? 0 : total / static_cast<double>(res_.pass_seconds.size());
   res_.stats.arena_bytes.clear();
-  for (auto& w : impl_->workers) res_.stats.arena_bytes.push_back(static_cast<double>(w->arena_bytes));
+  res_.stats.mv_cache_bytes.clear();
+  for (auto& w : impl_->workers) {
+    res_.stats.arena_bytes.push_back(static_cast<double>(w->arena_bytes));
+    res_.stats.mv_cache_bytes.push_back(static_cast<double>(w->mvpool_bytes));
+  }
 }
 
 void Executor::dump_params(const std::string& dir) const {

@@ -138,3 +138,35 @@ def test_host_optimizer_placement(tmp_path, fraction, state):
     if fraction == 1.0:
         assert st["opt_h2d_bytes_per_pass"] == 0
         assert st["refresh_h2d_bytes_per_pass"] > 0
+
+
+@pytest.mark.parametrize("limit", [-1, 5e5])
+def test_moment_cache_bit_identical(tmp_path, limit):
+    """The optimizer-state cache (moments resident in spare HBM, written back when the next
+    job takes the pool and at each pass end) changes only where m, v live: two jobs sharing
+    one GPU (ownership switch), 3 minibatches, 2 passes — params and losses bit-identical to
+    streaming every layer's moments through the staging ring. limit=5e5 B: only some layers
+    fit (the rest stream)."""
+    cfg = tiny_config(mbs=3)
+    runs = {}
+    for on in (False, True):
+        d = tmp_path / f"mv{int(on)}"
+        d.mkdir()
+        runs[on] = P.execute(cfg, params_out_dir=str(d), passes=2, mv_cache=on, mv_cache_max_bytes=limit,
+                             opt_chunk_floats=65536, hbm_slack_bytes=60e6)
+    st0, st1 = runs[False]["stats"], runs[True]["stats"]
+    assert st0["mv_resident_updates_per_pass"] == 0
+    assert st1["mv_resident_updates_per_pass"] > 0
+    assert st1["opt_h2d_bytes_per_pass"] < st0["opt_h2d_bytes_per_pass"]
+    assert runs[True]["losses"] == runs[False]["losses"]
+    for j in range(2):
+        a = np.fromfile(tmp_path / "mv0" / f"job{j}.f32", dtype=np.float32)
+        b = np.fromfile(tmp_path / "mv1" / f"job{j}.f32", dtype=np.float32)
+        assert np.array_equal(a, b), j
+
+
+def test_moment_cache_matches_oracle(tmp_path):
+    cfg = tiny_config(mbs=3)
+    res = compare(cfg, tmp_path, precision="fp32", loss_tol=1e-5, param_tol=1e-4, hbm_slack_bytes=60e6,
+                  opt_chunk_floats=65536)
+    assert res["stats"]["mv_resident_updates_per_pass"] > 0

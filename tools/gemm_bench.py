@@ -40,13 +40,42 @@ def run(bn):
     return out
 
 
+def run_cublas():
+    """cuBLAS TF32 at the same shapes (torch.matmul, allow_tf32): the library yardstick."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = True
+    dev = torch.device("cuda")
+    out = {}
+    for name, (M, N, Kd, amn, bmn) in SHAPES.items():
+        A = torch.randn(Kd, M, device=dev).t() if amn else torch.randn(M, Kd, device=dev)
+        B = torch.randn(Kd, N, device=dev) if bmn else torch.randn(N, Kd, device=dev).t()
+        C = torch.empty(M, N, device=dev)
+        f = lambda: torch.matmul(A, B, out=C)
+        for _ in range(3):
+            f()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(20):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 20 / 1e3
+        out[name] = round(2.0 * M * N * Kd / t / 1e12, 1)
+    return out
+
+
 if __name__ == "__main__":
-    if len(sys.argv) > 1:
+    if len(sys.argv) > 1 and sys.argv[1] == "cublas":
+        print(json.dumps(run_cublas()))
+    elif len(sys.argv) > 1:
         print(json.dumps(run(int(sys.argv[1]))))
     else:
         res = {}
-        for bn in ("128", "192", "256", "0"):
-            env = dict(os.environ, HY_GEMM_BN=bn)
-            r = subprocess.run([sys.executable, __file__, bn], env=env, capture_output=True, text=True)
-            res[bn] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-500:]
+        for bn in ("0", "nopair", "cublas"):
+            env = dict(os.environ, HY_GEMM_BN=bn, HY_GEMM_PAIR="0" if bn == "nopair" else "1")
+            bn = "0" if bn == "nopair" else bn
+            r = subprocess.run([sys.executable, __file__, bn], env=env, capture_output=True, text=True, timeout=180)
+            key = env["HY_GEMM_BN"]
+            res[key] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-500:]
         print(json.dumps(res, indent=1))
