@@ -1,712 +1,24 @@
-// Persistent warp-specialised tcgen05 GEMM for sm_100a (kind::tf32, fp32 in HBM).
-//
-//   warp 0      TMA producer (one elected lane): A/B tiles -> 4-stage smem ring (128B swizzle)
-//   warp 1      MMA issuer  (one elected lane): tcgen05.mma 128xBNx8 into TMEM, commit -> mbarriers
-//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
-//   warps 4..7  epilogue: tcgen05.ld 32x32b -> bias / residual / GELU / GELU' -> st.global
-//
-// Operands may be K-major or MN-major in global memory (the UMMA descriptor major bit),
-// so forward (X W^T), data-grad (dY W) and weight-grad (dY^T X) GEMMs all read their
-// inputs in place with no transposes.
+// Host entry of the tcgen05 TF32 GEMM: split-K planning and the per-mode dispatch. The
+// kernels live in gemm_kernels.cuh, instantiated per epilogue mode in gemm_m{0,1,2}.cu.
 #include <cuda.h>
-#include <cudaTypedefs.h>
 
-#include <cstdio>
 #include <algorithm>
-#include <cstdlib>
-#include <mutex>
 
 #include "gemm.cuh"
 #include "launch_count.cuh"
-#include "ptx.cuh"
 
 namespace hy {
+cudaError_t gemm_dispatch_m0(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+                           long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
+cudaError_t gemm_dispatch_m1(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+                           long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
+cudaError_t gemm_dispatch_m2(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+                           long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
+
 namespace {
 
-constexpr int BM = 128;
-constexpr int BK = 32;  // one 128-byte swizzle atom of fp32
-constexpr int kStages = 4;
-constexpr int kThreads = 256;
-
-// P3 (3xTF32, "fp32" precision): every stage also holds the low parts A_lo, B_lo
-// (x = hi + lo, hi = tf32_rna(x)); D += A_lo B_hi + A_hi B_lo + A_hi B_hi.
-template <int BN, bool P3 = false>
-struct Smem {
-  static constexpr int kStagesN = P3 ? 3 : kStages;
-  static constexpr int kABytes = BM * BK * 4;
-  static constexpr int kBBytes = BN * BK * 4;
-  static constexpr int kOpBytes = kABytes + kBBytes;
-  static constexpr int kStageBytes = P3 ? 2 * kOpBytes : kOpBytes;
-  static constexpr int kRing = kStagesN * kStageBytes;
-  static constexpr int kEpi = 4 * 32 * 36 * 4;  // per epilogue warp: 32x32 transpose tile, row stride 36
-  static constexpr int kTotal = kRing + kEpi + 1024 /*align slack*/ + 256 /*barriers*/;
-};
-
-__device__ __forceinline__ uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-
-__device__ __forceinline__ float gelu_tanh(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
-}
-__device__ __forceinline__ float gelu_tanh_grad(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float u = k0 * (x + k1 * x * x * x);
-  const float t = tanhf(u);
-  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
-}
-
-struct TileInfo {
-  int m0, n0, z1, z2;
-  int kb0, nkb;  // first k-block, number of k-blocks
-  bool skip;     // tile not computed (causal upper)
-};
-
-template <int BN>
-__device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n, int M, int N, int K, int nb2,
-                                              int causal, int nb1 = 1) {
-  TileInfo t;
-  const int per_batch = tiles_m * tiles_n;
-  const int z = tile / per_batch;
-  const int r = tile - z * per_batch;
-  t.z1 = z / nb2;
-  t.z2 = z - t.z1 * nb2;
-  t.m0 = (r % tiles_m) * BM;
-  t.n0 = (r / tiles_m) * BN;
-  const int kb_all = (K + BK - 1) / BK;
-  t.kb0 = 0;
-  t.nkb = kb_all;
-  t.skip = false;
-  if (causal == kCausalSkipUpper) {
-    t.skip = t.n0 >= t.m0 + BM;
-  } else if (causal == kCausalKLower) {
-    const int kend = min(K, t.m0 + BM);
-    t.nkb = (kend + BK - 1) / BK;
-  } else if (causal == kCausalKUpper) {
-    t.kb0 = t.m0 / BK;
-    t.nkb = max(0, kb_all - t.kb0);
-  } else if (causal == kSplitK) {
-    // z1 indexes the K slice; the operands themselves are not batched (TMA z = 0)
-    const int per = (kb_all + nb1 - 1) / nb1;
-    t.kb0 = t.z1 * per;
-    t.nkb = max(0, min(per, kb_all - t.kb0));
-  }
-  (void)M;
-  (void)N;
-  return t;
-}
-
-__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
-  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
-               : "memory");
-  return v;
-}
-__device__ __forceinline__ void tmem_ld_x32_issue(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-
-// Epilogue of one accumulator tile, run by epilogue warp q (TMEM lane quarter q), specialised
-// per mode at compile time (no per-element mode branches): TMEM -> registers (thread = row,
-// the next 32-column chunk's tcgen05.ld in flight while this one is processed) -> smem
-// transpose -> each lane takes 4 consecutive columns of a row (8 lanes per 32-column row, 4
-// rows per instruction), so bias / residual / GELU operands and the stores move as coalesced
-// 128-bit accesses.
-struct EpiCtx {
-  uint32_t lane, st_base;
-  float* stile;
-  int row0, nrows, sub_r, sub_c;
-  float* Cb;
-  const float* src;
-  long lds;
-  bool use_beta;
-  const float* bias;
-};
-
-// One 32-column chunk (v: this thread's row, 32 accumulator columns).
-template <int MODE>
-__device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t (&v)[32], int col0,
-                                               const GemmEpilogue& epi, int N) {
-  const uint32_t lane = x0.lane;
-  if (x0.nrows <= 0 || col0 >= N) return;  // warp-uniform
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    sts128(x0.st_base + (lane * 36 + 4 * k) * 4,
-           make_float4(__uint_as_float(v[4 * k]), __uint_as_float(v[4 * k + 1]), __uint_as_float(v[4 * k + 2]),
-                       __uint_as_float(v[4 * k + 3])));
-  }
-  __syncwarp();
-  const float alpha = epi.alpha;
-  const int col = col0 + x0.sub_c;
-  if (col0 + 32 <= N) {
-    const bool full_rows = x0.nrows == 32;
-    float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (x0.bias) bv = *reinterpret_cast<const float4*>(x0.bias + col);
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int r = it * 4 + x0.sub_r;
-      if (!full_rows && r >= x0.nrows) continue;
-      const long grow = x0.row0 + r;
-      float4 x = lds128(x0.st_base + (r * 36 + x0.sub_c) * 4);
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (x0.src) a = *reinterpret_cast<const float4*>(x0.src + grow * x0.lds + col);
-      float* xe = &x.x;
-      const float* ae = &a.x;
-      const float* be = &bv.x;
-      if constexpr (MODE == kEpiGeluBwd) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) xe[e] = xe[e] * alpha * gelu_tanh_grad(ae[e]);
-      } else if constexpr (MODE == kEpiGelu) {
-        float4 h;
-        float* he = &h.x;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          he[e] = xe[e] * alpha + be[e];
-          xe[e] = gelu_tanh(he[e]);
-        }
-        if (epi.Hout) *reinterpret_cast<float4*>(epi.Hout + grow * epi.ldho + col) = h;
-      } else {
-        float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (x0.use_beta) p = *reinterpret_cast<const float4*>(x0.Cb + grow * epi.ldc + col);
-        const float* pe = &p.x;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float y = xe[e] * alpha + be[e];
-          if (x0.src) y += ae[e];
-          if (x0.use_beta) y += epi.beta * pe[e];
-          xe[e] = y;
-        }
-      }
-      *reinterpret_cast<float4*>(x0.Cb + grow * epi.ldc + col) = x;
-    }
-  } else {
-    // ragged last chunk (N not a multiple of 32): scalar path, lanes over columns
-    const int colx = col0 + static_cast<int>(lane);
-    if (colx < N) {
-      const float bias_v = x0.bias ? x0.bias[colx] : 0.f;
-      for (int r = 0; r < x0.nrows; ++r) {
-        const long grow = x0.row0 + r;
-        float y = x0.stile[r * 36 + lane] * alpha;
-        if constexpr (MODE == kEpiGeluBwd) {
-          y *= gelu_tanh_grad(epi.Hin[grow * epi.ldhi + colx]);
-        } else if constexpr (MODE == kEpiGelu) {
-          y += bias_v;
-          if (epi.Hout) epi.Hout[grow * epi.ldho + colx] = y;
-          y = gelu_tanh(y);
-        } else {
-          y += bias_v;
-          if (epi.R) y += epi.R[grow * epi.ldr + colx];
-          if (epi.beta != 0.f) y += epi.beta * x0.Cb[grow * epi.ldc + colx];
-        }
-        x0.Cb[grow * epi.ldc + colx] = y;
-      }
-    }
-  }
-  __syncwarp();
-}
-
-// Epilogue of one accumulator tile, run by epilogue warp q (TMEM lane quarter q), specialised
-// per mode at compile time (no per-element mode branches): TMEM -> registers (thread = row,
-// the next 32-column chunk's tcgen05.ld in flight while this one is processed) -> smem
-// transpose -> each lane takes 4 consecutive columns of a row (8 lanes per 32-column row, 4
-// rows per instruction), so bias / residual / GELU operands and the stores move as coalesced
-// 128-bit accesses.
-template <int BN, int MODE>
-__device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uint32_t q, uint32_t tmem_base,
-                                                float* epi_smem, const GemmEpilogue& epi, const GemmBatch& bat,
-                                                int M, int N) {
-  static_assert((BN / 32) % 2 == 0, "chunk pairs");
-  EpiCtx x;
-  x.lane = lane_id();
-  x.stile = epi_smem + q * (32 * 36);
-  x.st_base = smem_u32(x.stile);
-  x.row0 = ti.m0 + static_cast<int>(q * 32);
-  x.nrows = min(32, M - x.row0);
-  x.Cb = epi.C + ti.z1 * bat.c_s1 + ti.z2 * bat.c_s2;
-  x.sub_r = static_cast<int>(x.lane >> 3);
-  x.sub_c = static_cast<int>(x.lane & 7) * 4;
-  x.src = MODE == kEpiGeluBwd ? epi.Hin : (MODE == kEpiStore ? epi.R : nullptr);
-  x.lds = MODE == kEpiGeluBwd ? epi.ldhi : epi.ldr;
-  x.use_beta = MODE == kEpiStore && epi.beta != 0.f;
-  x.bias = MODE == kEpiGeluBwd ? nullptr : epi.bias;
-  const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
-  uint32_t b0[32], b1[32];
-  if (ti.nkb > 0) {
-    tmem_ld_x32_issue(tbase, b0);
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; c += 2) {
-      tmem_ld_wait();
-      tmem_ld_x32_issue(tbase + (c + 1) * 32, b1);
-      epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
-      tmem_ld_wait();
-      if (c + 2 < BN / 32) tmem_ld_x32_issue(tbase + (c + 2) * 32, b0);
-      epilogue_chunk<MODE>(x, b1, ti.n0 + (c + 1) * 32, epi, N);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 32; ++i) b0[i] = 0u;
-#pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
-  }
-}
-
-template <int BN>
-__device__ __forceinline__ void epilogue_tile(const TileInfo& ti, int acc, uint32_t q, uint32_t tmem_base,
-                                              float* epi_smem, const GemmEpilogue& epi, const GemmBatch& bat, int M,
-                                              int N) {
-  if (epi.mode == kEpiGelu) {
-    epilogue_tile_m<BN, kEpiGelu>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N);
-  } else if (epi.mode == kEpiGeluBwd) {
-    epilogue_tile_m<BN, kEpiGeluBwd>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N);
-  } else {
-    epilogue_tile_m<BN, kEpiStore>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N);
-  }
-}
-
-template <int BN, bool A_MN, bool B_MN, bool P3>
-__global__ void __launch_bounds__(kThreads, 1)
-gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
-                 int N, int K, GemmEpilogue epi, GemmBatch bat) {
-  using L = Smem<BN, P3>;
-  constexpr int kStages = L::kStagesN;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* epi_smem = reinterpret_cast<float*>(smem + L::kRing);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kRing + L::kEpi);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* conv = tempty + 2;  // P3: hi/lo split of the stage done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + kStages);
-
-  const uint32_t warp = warp_id();
-  const int tiles_m = (M + BM - 1) / BM;
-  const int tiles_n = (N + BN - 1) / BN;
-  const int n_tiles = tiles_m * tiles_n * bat.nb1 * bat.nb2;
-
-  if (warp == 0 && elect_one()) {
-    tma_prefetch_desc(&map_a);
-    tma_prefetch_desc(&map_b);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-      mbar_init(&conv[s], 64);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 128);
-    }
-    fence_barrier_init();
-  }
-  constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  if (warp == 2) tmem_alloc<kTmemCols>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-        if (ti.skip) continue;
-        if (bat.causal == kSplitK) ti.z1 = ti.z2 = 0;  // K slices read the same operands
-        for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * L::kStageBytes;
-          uint8_t* sb = sa + L::kABytes;
-          mbar_expect_tx(&full[stage], L::kOpBytes);
-          const int k0 = kb * BK;
-          if constexpr (A_MN) {
-#pragma unroll
-            for (int j = 0; j < BM / 32; ++j) {
-              if (bat.a_perm) tma_load_4d(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, k0, ti.z2, ti.z1);
-            }
-          } else {
-            if (bat.a_perm) tma_load_4d(sa, &map_a, &full[stage], k0, ti.z2, ti.m0, ti.z1);
-            else tma_load_4d(sa, &map_a, &full[stage], k0, ti.m0, ti.z2, ti.z1);
-          }
-          if constexpr (B_MN) {
-#pragma unroll
-            for (int j = 0; j < BN / 32; ++j) {
-              if (bat.b_perm) tma_load_4d(sb + j * (32 * BK * 4), &map_b, &full[stage], ti.n0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d(sb + j * (32 * BK * 4), &map_b, &full[stage], ti.n0 + 32 * j, k0, ti.z2, ti.z1);
-            }
-          } else {
-            if (bat.b_perm) tma_load_4d(sb, &map_b, &full[stage], k0, ti.z2, ti.n0, ti.z1);
-            else tma_load_4d(sb, &map_b, &full[stage], k0, ti.n0, ti.z2, ti.z1);
-          }
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
-    int stage = 0;
-    uint32_t phase = 0;
-    int local = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-      if (ti.skip) continue;
-      const int acc = local & 1;
-      const uint32_t acc_phase = (local >> 1) & 1;
-      ++local;
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
-      if (ti.nkb == 0) {
-        if (elect_one()) mbar_arrive(&tfull[acc]);
-        __syncwarp();
-        continue;
-      }
-      for (int kb = 0; kb < ti.nkb; ++kb) {
-        if constexpr (P3) {
-          mbar_wait(&conv[stage], phase);
-        } else {
-          mbar_wait(&full[stage], phase);
-        }
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
-          const uint32_t sb = sa + L::kABytes;
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            if constexpr (P3) {
-              const uint32_t la = sa + L::kOpBytes, lb = sb + L::kOpBytes;
-              const uint64_t dah = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
-                                        : smem_desc_sw128(sa + kk * 32, 16, 1024);
-              const uint64_t dbh = B_MN ? smem_desc_sw128_b32(sb + kk * 1024, BK * 128, 512)
-                                        : smem_desc_sw128(sb + kk * 32, 16, 1024);
-              const uint64_t dal = A_MN ? smem_desc_sw128_b32(la + kk * 1024, BK * 128, 512)
-                                        : smem_desc_sw128(la + kk * 32, 16, 1024);
-              const uint64_t dbl = B_MN ? smem_desc_sw128_b32(lb + kk * 1024, BK * 128, 512)
-                                        : smem_desc_sw128(lb + kk * 32, 16, 1024);
-              mma_tf32(d_tmem, dal, dbh, idesc, (kb | kk) != 0 ? 1u : 0u);
-              mma_tf32(d_tmem, dah, dbl, idesc, 1u);
-              mma_tf32(d_tmem, dah, dbh, idesc, 1u);
-              continue;
-            }
-            // K-major: advance 8 fp32 = 32 B inside the swizzled row; SBO = 8 rows * 128 B.
-            // MN-major: advance 8 k-rows = 1024 B; LBO = one 32-element MN column (BK rows * 128 B),
-            // SBO = 4 k-rows (512 B) of the 32-byte-atom swizzle.
-            const uint64_t da = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
-                                     : smem_desc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t db = B_MN ? smem_desc_sw128_b32(sb + kk * 1024, BK * 128, 512)
-                                     : smem_desc_sw128(sb + kk * 32, 16, 1024);
-            mma_tf32(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
-          }
-          mma_commit(&empty[stage]);
-          if (kb == ti.nkb - 1) mma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else if (P3 && (warp == 2 || warp == 3)) {
-    // Split each landed stage into tf32 hi (in place) + lo (second half of the stage).
-    const int tid = static_cast<int>(threadIdx.x) - 64;
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-      if (ti.skip) continue;
-      for (int kb = 0; kb < ti.nkb; ++kb) {
-        mbar_wait(&full[stage], phase);
-        float4* hi = reinterpret_cast<float4*>(smem + stage * L::kStageBytes);
-        float4* lo = reinterpret_cast<float4*>(smem + stage * L::kStageBytes + L::kOpBytes);
-        for (int i = tid; i < L::kOpBytes / 16; i += 64) {
-          float4 x = hi[i];
-          float4 h, l;
-          h.x = __uint_as_float(tf32_rna(x.x));
-          h.y = __uint_as_float(tf32_rna(x.y));
-          h.z = __uint_as_float(tf32_rna(x.z));
-          h.w = __uint_as_float(tf32_rna(x.w));
-          l.x = x.x - h.x;
-          l.y = x.y - h.y;
-          l.z = x.z - h.z;
-          l.w = x.w - h.w;
-          hi[i] = h;
-          lo[i] = l;
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&conv[stage]);
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
-  } else if (warp >= 4) {
-    const uint32_t q = warp - 4;  // TMEM lane quarter this warp may access
-    int local = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-      if (ti.skip) continue;
-      const int acc = local & 1;
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ++local;
-      tc_fence_after();
-      epilogue_tile<BN>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N);
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<kTmemCols>(tmem_base);
-  }
-}
-
-// ---- CTA-pair variant (cta_group::2) ------------------------------------------------
-// A cluster of two CTAs on one TPC computes a 256 x BN tile: each CTA stages its own 128
-// rows of A and half (BN/2 rows) of B, the even CTA issues tcgen05.mma.cta_group::2 with
-// M = 256 over both CTAs' shared memory, and each CTA's TMEM receives its 128 rows of the
-// accumulator. Per SM, a 128 x BN x 32 stage now moves 16 KB of A + BN/2 x 128 B of B from
-// L2 (vs BN x 128 B of B alone before): the shared-memory / L2 operand traffic per MMA
-// flop drops by a third at BN = 256, the bound that held the 1-CTA kernel near 0.6 of the
-// library GEMM on the workload's short-K shapes.
-template <int BN>
-struct SmemPair {
-  static constexpr int kABytes = BM * BK * 4;
-  static constexpr int kBBytes = (BN / 2) * BK * 4;
-  static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesN = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
-  static constexpr int kRing = kStagesN * kStageBytes;
-  static constexpr int kEpi = 4 * 32 * 36 * 4;
-  static constexpr int kTotal = kRing + kEpi + 1024 + 256;
-};
-
-template <int BN, bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
-gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
-                      int N, int K, GemmEpilogue epi, GemmBatch bat) {
-  using L = SmemPair<BN>;
-  constexpr int kStages = L::kStagesN;
-  constexpr int BM2 = 2 * BM;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* epi_smem = reinterpret_cast<float*>(smem + L::kRing);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kRing + L::kEpi);
-  uint64_t* empty = full + kStages;
-  uint64_t* tfull = empty + kStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
-  const uint32_t warp = warp_id();
-  const uint32_t rank = cluster_ctarank();
-  const bool leader = rank == 0;
-  const int tiles_m = (M + BM2 - 1) / BM2;
-  const int tiles_n = (N + BN - 1) / BN;
-  const int n_tiles = tiles_m * tiles_n * bat.nb1 * bat.nb2;
-  const int pair = static_cast<int>(cluster_id_x());
-  const int n_pairs = static_cast<int>(nclusters_x());
-
-  if (warp == 0 && elect_one()) {
-    tma_prefetch_desc(&map_a);
-    tma_prefetch_desc(&map_b);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
-    for (int a = 0; a < 2; ++a) {
-      mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
-    }
-    fence_barrier_init();
-  }
-  constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  if (warp == 2) tmem_alloc_pair<kTmemCols>(tmem_slot);
-  tc_fence_before();
-  cluster_sync();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-
-  if (warp == 0) {
-    if (elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-        // tile_info counts 128-row tiles; rescale to this CTA's half of the 256-row pair tile
-        ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
-        if (bat.causal == kSplitK) ti.z1 = ti.z2 = 0;
-        const int nb0 = ti.n0 + static_cast<int>(rank) * (BN / 2);
-        for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * L::kStageBytes;
-          uint8_t* sb = sa + L::kABytes;
-          if (leader) mbar_expect_tx(&full[stage], 2 * L::kStageBytes);
-          const int k0 = kb * BK;
-          if constexpr (A_MN) {
-#pragma unroll
-            for (int j = 0; j < BM / 32; ++j) {
-              if (bat.a_perm) tma_load_4d_pair(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d_pair(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, k0, ti.z2, ti.z1);
-            }
-          } else {
-            if (bat.a_perm) tma_load_4d_pair(sa, &map_a, &full[stage], k0, ti.z2, ti.m0, ti.z1);
-            else tma_load_4d_pair(sa, &map_a, &full[stage], k0, ti.m0, ti.z2, ti.z1);
-          }
-          if constexpr (B_MN) {
-#pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
-              if (bat.b_perm) tma_load_4d_pair(sb + j * (32 * BK * 4), &map_b, &full[stage], nb0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d_pair(sb + j * (32 * BK * 4), &map_b, &full[stage], nb0 + 32 * j, k0, ti.z2, ti.z1);
-            }
-          } else {
-            if (bat.b_perm) tma_load_4d_pair(sb, &map_b, &full[stage], k0, ti.z2, nb0, ti.z1);
-            else tma_load_4d_pair(sb, &map_b, &full[stage], k0, nb0, ti.z2, ti.z1);
-          }
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (leader) {
-      constexpr uint32_t idesc = idesc_tf32(BM2, BN, A_MN, B_MN);
-      int stage = 0;
-      uint32_t phase = 0;
-      int local = 0;
-      for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-        const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-        const int acc = local & 1;
-        const uint32_t acc_phase = (local >> 1) & 1;
-        ++local;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
-        if (ti.nkb == 0) {
-          if (elect_one()) {
-            mbar_arrive_cluster(&tfull[acc], 0);
-            mbar_arrive_cluster(&tfull[acc], 1);
-          }
-          __syncwarp();
-          continue;
-        }
-        for (int kb = 0; kb < ti.nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          if (elect_one()) {
-            const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
-            const uint32_t sb = sa + L::kABytes;
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t da = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
-                                       : smem_desc_sw128(sa + kk * 32, 16, 1024);
-              const uint64_t db = B_MN ? smem_desc_sw128_b32(sb + kk * 1024, BK * 128, 512)
-                                       : smem_desc_sw128(sb + kk * 32, 16, 1024);
-              mma_tf32_pair(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
-            }
-            mma_commit_pair(&empty[stage], 0x3);
-            if (kb == ti.nkb - 1) mma_commit_pair(&tfull[acc], 0x3);
-          }
-          __syncwarp();
-          if (++stage == kStages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
-    }
-  } else if (warp >= 4) {
-    const uint32_t q = warp - 4;
-    int local = 0;
-    for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-      TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-      ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
-      const int acc = local & 1;
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ++local;
-      tc_fence_after();
-      epilogue_tile<BN>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N);
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) {
-        if (leader) mbar_arrive(&tempty[acc]);
-        else mbar_arrive_cluster(&tempty[acc], 0);
-      }
-    }
-  }
-
-  tc_fence_before();
-  cluster_sync();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc_pair<kTmemCols>(tmem_base);
-  }
-}
-
-// ---- host side -------------------------------------------------------------------
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess) {
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-  });
-  return fn;
-}
-
-// 4-D fp32 tensor map over {inner, outer, b2, b1}: row stride ld, batch strides s2, s1
-// (elements). Dimensions are ordered by increasing stride: {inner, outer, b2, b1}, or
-// {inner, b2, outer, b1} when b2's stride is below the row stride (*perm = 1).
-bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long ld, int box_inner, int box_outer,
-              bool mn_major, long nb2 = 1, long s2 = 0, long nb1 = 1, long s1 = 0, int* perm = nullptr) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  const long st2 = s2 > 0 ? s2 : ld * outer;
-  const long st1 = s1 > 0 ? s1 : st2 * nb2;
-  const bool swap = nb2 > 1 && st2 < ld;
-  if (perm) *perm = swap ? 1 : 0;
-  cuuint64_t dims[4] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(swap ? nb2 : outer),
-                        static_cast<cuuint64_t>(swap ? outer : nb2), static_cast<cuuint64_t>(nb1)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(swap ? st2 : ld) * 4, static_cast<cuuint64_t>(swap ? ld : st2) * 4,
-                           static_cast<cuuint64_t>(st1) * 4};
-  cuuint32_t box[4] = {static_cast<cuuint32_t>(box_inner), swap ? 1u : static_cast<cuuint32_t>(box_outer),
-                       swap ? static_cast<cuuint32_t>(box_outer) : 1u, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
+constexpr int BM = 128;  // must match gemm_kernels.cuh
+constexpr int BK = 32;
 
 thread_local float* t_splitk_ws = nullptr;
 thread_local bool t_prec3 = false;
@@ -726,7 +38,7 @@ __global__ void splitk_reduce_kernel(int M, int N, int S, const float* __restric
   }
 }
 
-int sm_count() {
+int sm_count_host() {
   static int n = 0;
   if (n == 0) {
     int dev = 0;
@@ -736,156 +48,14 @@ int sm_count() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool P3>
-cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
-                   const GemmEpilogue& epi, const GemmBatch& bat) {
-  CUtensorMap ma, mb;
-  GemmBatch b = bat;
-  const long mb1 = b.causal == kSplitK ? 1 : b.nb1;  // K slices share the (unbatched) operands
-  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm)
-                         : make_map(&ma, A, K, M, lda, BK, BM, false, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm);
-  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm)
-                         : make_map(&mb, B, K, N, ldb, BK, BN, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
-  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, P3>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN, P3>::kTotal);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
-  const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
-  count_launch();
-  kern<<<grid, kThreads, Smem<BN, P3>::kTotal, stream>>>(ma, mb, M, N, K, epi, b);
-  return cudaGetLastError();
-}
-
-template <int BN, bool A_MN, bool B_MN>
-cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
-                        const GemmEpilogue& epi, const GemmBatch& bat) {
-  CUtensorMap ma, mb;
-  GemmBatch b = bat;
-  const long mb1 = b.causal == kSplitK ? 1 : b.nb1;
-  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm)
-                         : make_map(&ma, A, K, M, lda, BK, BM, false, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm);
-  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm)
-                         : make_map(&mb, B, K, N, ldb, BK, BN / 2, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
-  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-  auto kern = gemm_tf32_pair_kernel<BN, A_MN, B_MN>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemPair<BN>::kTotal);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const long tiles = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
-  const long pairs = std::min<long>(tiles, sm_count() / 2);
-  count_launch();
-  kern<<<static_cast<int>(2 * pairs), kThreads, SmemPair<BN>::kTotal, stream>>>(ma, mb, M, N, K, epi, b);
-  return cudaGetLastError();
-}
-
-template <int BN>
-cudaError_t dispatch_pair(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
-                          long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
-  if (!a_mn && !b_mn) return launch_pair<BN, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (!a_mn && b_mn) return launch_pair<BN, false, true>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (a_mn && !b_mn) return launch_pair<BN, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  return launch_pair<BN, true, true>(st, M, N, K, A, lda, B, ldb, e, bat);
-}
-
-// CTA-pair tile width (256 x BN pair tiles): the widest tile whose wave count is not worse.
-int pick_bn_pair(int M, int N, long batches) {
-  static const int forced = [] {
-    const char* e = std::getenv("HY_GEMM_BN");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced == 128 || forced == 192 || forced == 256) return forced;
-  static const int kBN[3] = {128, 192, 256};
-  static const double kCost[3] = {128 / 0.62, 192 / 0.70, 256 / 0.76};
-  const long tm = (M + 2 * BM - 1) / (2 * BM);
-  const long pairs = sm_count() / 2;
-  int best = 128;
-  double best_t = 1e300;
-  for (int i = 0; i < 3; ++i) {
-    if (kBN[i] > 128 && N <= 128) break;
-    const long tiles = tm * ((N + kBN[i] - 1) / kBN[i]) * batches;
-    const double t = static_cast<double>((tiles + pairs - 1) / pairs) * kCost[i];
-    if (t < best_t - 1e-9) {
-      best_t = t;
-      best = kBN[i];
-    }
-  }
-  return best;
-}
-
-bool use_pairs() {
-  static const bool on = [] {
-    const char* e = std::getenv("HY_GEMM_PAIR");  // experiments: 0 = one-CTA tiles only
-    return !e || std::atoi(e) != 0;
-  }();
-  return on;
-}
-
-template <int BN>
-cudaError_t dispatch_bn(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
-                        long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
-  if (!a_mn && !b_mn) return launch<BN, false, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (!a_mn && b_mn) return launch<BN, false, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (a_mn && !b_mn) return launch<BN, true, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  return launch<BN, true, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-}
-
-// Output tile width: wider tiles cut the shared-memory traffic per MMA (the TF32 pipe is
-// smem-bound at BN=128), but fewer tiles can leave SMs idle in the last wave. Pick the
-// width minimising waves x relative per-tile cost.
-int pick_bn(int M, int N, long batches) {
-  static const int forced = [] {
-    const char* e = std::getenv("HY_GEMM_BN");  // experiments only
-    return e ? std::atoi(e) : 0;
-  }();
-  if (forced == 128 || forced == 192 || forced == 256) return forced;
-  static const int kBN[3] = {128, 192, 256};
-  static const double kCost[3] = {128 / 0.50, 192 / 0.60, 256 / 0.66};  // relative time per tile
-  const long tm = (M + BM - 1) / BM;
-  int best = 128;
-  double best_t = 1e300;
-  for (int i = 0; i < 3; ++i) {
-    if (kBN[i] > 128 && N <= 128) break;
-    const long tiles = tm * ((N + kBN[i] - 1) / kBN[i]) * batches;
-    const double t = static_cast<double>((tiles + sm_count() - 1) / sm_count()) * kCost[i];
-    if (t < best_t - 1e-9) {
-      best_t = t;
-      best = kBN[i];
-    }
-  }
-  return best;
-}
-
+// The epilogue mode is a kernel template parameter: each instantiation carries only its own
+// epilogue code (the 3-mode kernel's instruction footprint stalled the epilogue warps on
+// instruction fetch).
 cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
                      long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
-  if (!t_prec3 && (bat.causal == kCausalNone || bat.causal == kSplitK) && M > BM && use_pairs()) {
-    const int bn = pick_bn_pair(M, N, static_cast<long>(bat.nb1) * bat.nb2);
-    if (bn == 256) return dispatch_pair<256>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-    if (bn == 192) return dispatch_pair<192>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-    return dispatch_pair<128>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-  }
-  if (!t_prec3 && bat.causal == kCausalNone) {
-    const int bn = pick_bn(M, N, static_cast<long>(bat.nb1) * bat.nb2);
-    if (bn == 256) return dispatch_bn<256>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-    if (bn == 192) return dispatch_bn<192>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-  }
-  if (t_prec3) {
-    if (!a_mn && !b_mn) return launch<128, false, false, true>(st, M, N, K, A, lda, B, ldb, e, bat);
-    if (!a_mn && b_mn) return launch<128, false, true, true>(st, M, N, K, A, lda, B, ldb, e, bat);
-    if (a_mn && !b_mn) return launch<128, true, false, true>(st, M, N, K, A, lda, B, ldb, e, bat);
-    return launch<128, true, true, true>(st, M, N, K, A, lda, B, ldb, e, bat);
-  }
-  if (!a_mn && !b_mn) return launch<128, false, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (!a_mn && b_mn) return launch<128, false, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (a_mn && !b_mn) return launch<128, true, false, false>(st, M, N, K, A, lda, B, ldb, e, bat);
-  return launch<128, true, true, false>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (e.mode == kEpiGelu) return gemm_dispatch_m1(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
+  if (e.mode == kEpiGeluBwd) return gemm_dispatch_m2(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
+  return gemm_dispatch_m0(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
 }
 
 }  // namespace
@@ -907,8 +77,8 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + 127) / 128);
   const int kb_all = (K + BK - 1) / BK;
   const bool plain = !batch && e.mode == kEpiStore && !e.bias && !e.R;
-  if (plain && t_splitk_ws && tiles * 2 <= sm_count() && kb_all >= 32) {
-    split = static_cast<int>(std::min<long>(sm_count() / tiles, kb_all / 16));
+  if (plain && t_splitk_ws && tiles * 2 <= sm_count_host() && kb_all >= 32) {
+    split = static_cast<int>(std::min<long>(sm_count_host() / tiles, kb_all / 16));
     split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
   if (split >= 2) {
@@ -921,7 +91,7 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
     const cudaError_t r = dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, pe, bat);
     if (r != cudaSuccess) return r;
     const long total = static_cast<long>(M) * N;
-    const int grid = static_cast<int>(std::min<long>((total + 255) / 256, sm_count() * 8L));
+    const int grid = static_cast<int>(std::min<long>((total + 255) / 256, sm_count_host() * 8L));
     count_launch();
     splitk_reduce_kernel<<<grid, 256, 0, stream>>>(M, N, split, t_splitk_ws, e.C, e.ldc, e.alpha, e.beta);
     return cudaGetLastError();
