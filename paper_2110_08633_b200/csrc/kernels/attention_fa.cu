@@ -77,6 +77,14 @@ __device__ __forceinline__ uint64_t desc_mn(const uint8_t* base, int kk) {
   return smem_desc_sw128_b32(smem_u32(base) + (kk >> 2) * 8192 + (kk & 3) * 1024, 4096, 512);
 }
 
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp; the TF32 path's probabilities are rounded to TF32
+// afterwards anyway); exp2f's range fix-ups cost more than the exponential itself here.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
@@ -107,7 +115,43 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&x)[64]) {
 
 __device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr int kFwdSmem = 32768 + 16384 + 16384 + 32768 + 256 + 1024;
+// TMEM <- registers: 32 lanes x 32 columns (thread t of the warp writes its lane's 32 values).
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem: 128 lanes x 8 fp32 columns] * B[smem]^T, kind::tf32 (A K-major).
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// Forward, software-pipelined over 64-key tiles j (S, K, V double-buffered; P in TMEM):
+//   S(j+1) = Q K(j+1)^T is issued as soon as S(j) lands, so it runs under softmax(j);
+//   P(j) goes registers -> TMEM (tcgen05.st, TF32-rounded) and PV(j) = P(j) V(j) reads it as
+//   the MMA's A operand, running under the next tile's softmax; O lives in registers and
+//   takes PV(j-1) one iteration late (O = O * alpha(j-1) + PV(j-1)).
+// smem: Q 32 KB + K 2 x 16 KB + V 2 x 16 KB (two CTAs per SM); TMEM: S 2 x 64, P 64, PV 64.
+constexpr int kFwdSmem = 32768 + 2 * 16384 + 2 * 16384 + 256 + 1024;
 
 __global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ CUtensorMap mq,
                                                        const __grid_constant__ CUtensorMap mk,
@@ -115,10 +159,10 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ C
                                                        float* __restrict__ out, float* __restrict__ lse2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sQ = align1024(smem_raw);
-  uint8_t* sK = sQ + 32768;
-  uint8_t* sV = sK + 16384;
-  uint8_t* sP = sV + 16384;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 32768);  // q, k, v, s, pv
+  uint8_t* sK0 = sQ + 32768;
+  uint8_t* sV0 = sK0 + 2 * 16384;
+  // barriers: 0 q, 1-2 k[2], 3-4 v[2], 5-6 s[2], 7 pv
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV0 + 2 * 16384);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 8);
   const int tid = threadIdx.x;
   const int nqt = (T + 127) / 128;
@@ -131,91 +175,131 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ C
     tma_prefetch_desc(&mq);
     tma_prefetch_desc(&mk);
     tma_prefetch_desc(&mv);
-    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
-  if (tid < 32) tmem_alloc<128>(tslot);
+  if (tid < 32) tmem_alloc<256>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tS = *tslot, tPV = *tslot + 64;
+  const uint32_t tbase = *tslot;
+  const uint32_t tP = tbase + 128, tPV = tbase + 192;
   const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
+  auto load_k = [&](int j) {
+    uint8_t* dst = sK0 + (j & 1) * 16384;
+    mbar_expect_tx(&bar[1 + (j & 1)], 16384);
+    tma_load_2d(dst, &mk, &bar[1 + (j & 1)], D + h * HD, row0 + j * 64);
+    tma_load_2d(dst + 8192, &mk, &bar[1 + (j & 1)], D + h * HD + 32, row0 + j * 64);
+  };
+  auto load_v = [&](int j) {
+    uint8_t* dst = sV0 + (j & 1) * 16384;
+    mbar_expect_tx(&bar[3 + (j & 1)], 16384);
+    for (int kb = 0; kb < 2; ++kb)
+      for (int jn = 0; jn < 2; ++jn)
+        tma_load_2d(dst + kb * 8192 + jn * 4096, &mv, &bar[3 + (j & 1)], 2 * D + h * HD + 32 * jn, row0 + j * 64 + 32 * kb);
+  };
+  constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
+  constexpr uint32_t idPV = idesc_tf32(128, 64, false, true);
+  auto issue_s = [&](int j) {  // tid 0
+    mbar_wait(&bar[1 + (j & 1)], (j >> 1) & 1);
+    tc_fence_after();
+    const uint32_t tS = tbase + (j & 1) * 64;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sK0 + (j & 1) * 16384, kk, 8192), idS, kk > 0);
+    mma_commit(&bar[5 + (j & 1)]);
+  };
   if (tid == 0) {
     mbar_expect_tx(&bar[0], 32768);
     tma_load_2d(sQ, &mq, &bar[0], h * HD, row0 + q0);
     tma_load_2d(sQ + 16384, &mq, &bar[0], h * HD + 32, row0 + q0);
-    mbar_expect_tx(&bar[1], 16384);
-    tma_load_2d(sK, &mk, &bar[1], D + h * HD, row0);
-    tma_load_2d(sK + 8192, &mk, &bar[1], D + h * HD + 32, row0);
-    mbar_expect_tx(&bar[2], 16384);
-    for (int kb = 0; kb < 2; ++kb)
-      for (int jn = 0; jn < 2; ++jn) tma_load_2d(sV + kb * 8192 + jn * 4096, &mv, &bar[2], 2 * D + h * HD + 32 * jn, row0 + 32 * kb);
+    load_k(0);
+    load_v(0);
+    if (nkt > 1) {
+      load_k(1);
+      load_v(1);
+    }
+    mbar_wait(&bar[0], 0);
+    issue_s(0);
   }
-  constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
-  constexpr uint32_t idPV = idesc_tf32(128, 64, false, true);
   float o[64];
 #pragma unroll
   for (int i = 0; i < 64; ++i) o[i] = 0.f;
-  float m_run = -FLT_MAX, l_run = 0.f;
+  float m_run = -FLT_MAX, l_run = 0.f, alpha_prev = 1.f;
   const int q = q0 + tid;
-  uint32_t ph = 0;
-  for (int j = 0; j < nkt; ++j, ph ^= 1) {
+  for (int j = 0; j < nkt; ++j) {
     const int k0 = j * 64;
-    if (tid == 0) {
-      if (j == 0) mbar_wait(&bar[0], 0);
-      mbar_wait(&bar[1], ph);
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sK, kk, 8192), idS, kk > 0);
-      mma_commit(&bar[3]);
-    }
-    mbar_wait(&bar[3], ph);
+    mbar_wait(&bar[5 + (j & 1)], (j >> 1) & 1);  // S(j) landed (K(j) consumed)
     tc_fence_after();
-    if (tid == 0 && j + 1 < nkt) {  // S consumed K: fetch the next key tile
-      mbar_expect_tx(&bar[1], 16384);
-      tma_load_2d(sK, &mk, &bar[1], D + h * HD, row0 + k0 + 64);
-      tma_load_2d(sK + 8192, &mk, &bar[1], D + h * HD + 32, row0 + k0 + 64);
+    if (tid == 0) {
+      if (j + 2 < nkt) load_k(j + 2);  // into the buffer S(j) just released
+      if (j + 1 < nkt) issue_s(j + 1);
     }
     float s[64];
-    tmem_ld64(tS + lane_off, s);
+    tmem_ld64(tbase + (j & 1) * 64 + lane_off, s);
     float mx = m_run;
+    const bool full = k0 + 63 <= q0;  // every key of the tile visible to every row (CTA-uniform)
+    if (full) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      s[i] = (k0 + i <= q) ? s[i] * kScaleLog2 : -FLT_MAX;
-      mx = fmaxf(mx, s[i]);
+      for (int i = 0; i < 64; ++i) {
+        s[i] *= kScaleLog2;
+        mx = fmaxf(mx, s[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        s[i] = (k0 + i <= q) ? s[i] * kScaleLog2 : -FLT_MAX;
+        mx = fmaxf(mx, s[i]);
+      }
     }
-    const float alpha = exp2f(m_run - mx);
+    const float alpha = fast_exp2(m_run - mx);
     float sum = 0.f;
+    if (full) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
-      s[i] = (k0 + i <= q) ? exp2f(s[i] - mx) : 0.f;
-      sum += s[i];
+      for (int i = 0; i < 64; ++i) {
+        s[i] = fast_exp2(s[i] - mx);
+        sum += s[i];
+        s[i] = tf32_rna(s[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        s[i] = (k0 + i <= q) ? fast_exp2(s[i] - mx) : 0.f;
+        sum += s[i];
+        s[i] = tf32_rna(s[i]);
+      }
     }
     l_run = l_run * alpha + sum;
     m_run = mx;
-    store_row64(sP, tid, 16384, s);
-    proxy_fence();
+    if (j > 0) {  // PV(j-1) done: fold it into O, its P and V(j-1) buffers are free
+      mbar_wait(&bar[7], (j - 1) & 1);
+      tc_fence_after();
+      if (tid == 0 && j + 1 < nkt) load_v(j + 1);
+      float pv[64];
+      tmem_ld64(tPV + lane_off, pv);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) o[i] = o[i] * alpha_prev + pv[i];
+    }
+    tmem_st_x32(tP + lane_off, s);
+    tmem_st_x32(tP + lane_off + 32, s + 32);
+    tmem_st_wait();
     tc_fence_before();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
-      mbar_wait(&bar[2], ph);
+      mbar_wait(&bar[3 + (j & 1)], (j >> 1) & 1);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tPV, desc_k(sP, kk, 16384), desc_mn(sV, kk), idPV, kk > 0);
-      mma_commit(&bar[4]);
+      for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tPV, tP + kk * 8, desc_mn(sV0 + (j & 1) * 16384, kk), idPV, kk > 0);
+      mma_commit(&bar[7]);
     }
-    mbar_wait(&bar[4], ph);
-    tc_fence_after();
-    if (tid == 0 && j + 1 < nkt) {  // PV consumed V
-      mbar_expect_tx(&bar[2], 16384);
-      for (int kb = 0; kb < 2; ++kb)
-        for (int jn = 0; jn < 2; ++jn)
-          tma_load_2d(sV + kb * 8192 + jn * 4096, &mv, &bar[2], 2 * D + h * HD + 32 * jn, row0 + k0 + 64 + 32 * kb);
-    }
+    alpha_prev = alpha;
+  }
+  mbar_wait(&bar[7], (nkt - 1) & 1);
+  tc_fence_after();
+  {
     float pv[64];
     tmem_ld64(tPV + lane_off, pv);
 #pragma unroll
-    for (int i = 0; i < 64; ++i) o[i] = o[i] * alpha + pv[i];
+    for (int i = 0; i < 64; ++i) o[i] = o[i] * alpha_prev + pv[i];
   }
   if (q < T) {
     const float inv = 1.f / l_run;
@@ -228,7 +312,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ C
   __syncthreads();
   if (tid < 32) {
     tc_fence_after();
-    tmem_dealloc<128>(*tslot);
+    tmem_dealloc<256>(*tslot);
   }
 }
 
@@ -252,10 +336,16 @@ __global__ void attn_di_kernel(long n, int T, int H, const float* __restrict__ o
   }
 }
 
-// dK, dV of one (batch, head, 128-key tile); thread t owns key row k0 + t.
-constexpr int kDkvSmem = 32768 * 2 + 16384 * 4 + 32768 * 2 + 256 + 1024;
+// dK, dV of one (batch, head, 128-key tile), warp-specialised and pipelined over 64-query
+// tiles i (from the diagonal): warp 4 (one lane) streams Q / dO tiles (double-buffered, both
+// majors) and issues S^T(i) = K Q(i)^T, dP^T(i) = V dO(i)^T into double-buffered TMEM as soon
+// as they land, then dV += P^T(i) dO(i) and dK += dS^T(i) Q(i) with P^T, dS^T read from TMEM;
+// warps 0-3 (thread = key row) compute P^T = exp2(S^T c - lse2) and dS^T = P^T (dP^T - Di) / 8.
+// smem: K, V 32 KB each + 2 stages x (Q k, Q mn, dO k, dO mn) 64 KB = 192 KB;
+// TMEM: S^T 2 x 64, dP^T 2 x 64, P^T 64, dS^T 64, dV 64, dK 64 columns.
+constexpr int kDkvSmem = 32768 * 2 + 2 * 65536 + 256 + 1024 + 1024;  // + lse / Di staging
 
-__global__ void __launch_bounds__(128) attn_dkdv_kernel(
+__global__ void __launch_bounds__(160) attn_dkdv_kernel(
     const __grid_constant__ CUtensorMap mkv128, const __grid_constant__ CUtensorMap mq64,
     const __grid_constant__ CUtensorMap mqmn, const __grid_constant__ CUtensorMap mdo64,
     const __grid_constant__ CUtensorMap mdomn, int T, int H, const float* __restrict__ lse2,
@@ -263,15 +353,12 @@ __global__ void __launch_bounds__(128) attn_dkdv_kernel(
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sK = align1024(smem_raw);
   uint8_t* sV = sK + 32768;
-  uint8_t* sQk = sV + 32768;   // Q tile, K-major B (S^T = K Q^T)
-  uint8_t* sQm = sQk + 16384;  // Q tile, MN-major B (dK += dS^T Q)
-  uint8_t* sGk = sQm + 16384;  // dO tile, K-major B (dP^T = V dO^T)
-  uint8_t* sGm = sGk + 16384;  // dO tile, MN-major B (dV += P^T dO)
-  uint8_t* sP = sGm + 16384;   // P^T  [128 keys x 64 q], K-major A
-  uint8_t* sS = sP + 32768;    // dS^T [128 keys x 64 q], K-major A
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 32768);  // kv, q, mma1, mma2
+  uint8_t* sQG = sV + 32768;  // stage s: Q k at +0, Q mn at +16K, dO k at +32K, dO mn at +48K
+  // barriers: 0 k/v, 1-2 qg[2], 3-4 sp[2], 5 pds (P^T, dS^T written), 6-7 g[2] (dV, dK MMAs done)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sQG + 2 * 65536);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 8);
   const int tid = threadIdx.x;
+  const int warp = tid >> 5;
   const int nkt = (T + 127) / 128;
   const int bh = blockIdx.x / nkt;
   const int kt = blockIdx.x % nkt;  // tiles near the start see the most queries: schedule them first
@@ -284,120 +371,167 @@ __global__ void __launch_bounds__(128) attn_dkdv_kernel(
     tma_prefetch_desc(&mqmn);
     tma_prefetch_desc(&mdo64);
     tma_prefetch_desc(&mdomn);
-    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], i == 5 ? 4 : 1);
     fence_barrier_init();
   }
-  if (tid < 32) tmem_alloc<256>(tslot);
+  if (warp == 0) tmem_alloc<512>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tS = *tslot, tP = *tslot + 64, tdV = *tslot + 128, tdK = *tslot + 192;
-  const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
-  auto load_q = [&](int q0) {
-    mbar_expect_tx(&bar[1], 4 * 16384);
-    for (int kb = 0; kb < 2; ++kb) {
-      tma_load_2d(sQk + kb * 8192, &mq64, &bar[1], h * HD + 32 * kb, row0 + q0);
-      tma_load_2d(sGk + kb * 8192, &mdo64, &bar[1], h * HD + 32 * kb, row0 + q0);
-      for (int jn = 0; jn < 2; ++jn) {
-        tma_load_2d(sQm + kb * 8192 + jn * 4096, &mqmn, &bar[1], h * HD + 32 * jn, row0 + q0 + 32 * kb);
-        tma_load_2d(sGm + kb * 8192 + jn * 4096, &mdomn, &bar[1], h * HD + 32 * jn, row0 + q0 + 32 * kb);
+  // S^T: tb + 64s, dP^T: tb + 128 + 64s, P^T: tb + 256, dS^T: tb + 320, dV: tb + 384, dK: tb + 448
+  const uint32_t tb = *tslot;
+  const uint32_t tPT = tb + 256, tDST = tb + 320, tdV = tb + 384, tdK = tb + 448;
+  if (warp == 4) {
+    if (lane_id() == 0) {
+      auto load_q = [&](int i) {
+        uint8_t* st = sQG + (i & 1) * 65536;
+        uint64_t* bb = &bar[1 + (i & 1)];
+        const int q0 = k0 + 64 * i;
+        mbar_expect_tx(bb, 4 * 16384);
+        for (int kb = 0; kb < 2; ++kb) {
+          tma_load_2d(st + kb * 8192, &mq64, bb, h * HD + 32 * kb, row0 + q0);
+          tma_load_2d(st + 32768 + kb * 8192, &mdo64, bb, h * HD + 32 * kb, row0 + q0);
+          for (int jn = 0; jn < 2; ++jn) {
+            tma_load_2d(st + 16384 + kb * 8192 + jn * 4096, &mqmn, bb, h * HD + 32 * jn, row0 + q0 + 32 * kb);
+            tma_load_2d(st + 49152 + kb * 8192 + jn * 4096, &mdomn, bb, h * HD + 32 * jn, row0 + q0 + 32 * kb);
+          }
+        }
+      };
+      constexpr uint32_t idT = idesc_tf32(128, 64, false, false);  // S^T, dP^T
+      constexpr uint32_t idG = idesc_tf32(128, 64, false, true);   // dV, dK (B MN-major)
+      auto issue_sp = [&](int i) {
+        uint8_t* st = sQG + (i & 1) * 65536;
+        mbar_wait(&bar[1 + (i & 1)], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tS = tb + (i & 1) * 64, tP = tb + 128 + (i & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sK, kk, 16384), desc_k(st, kk, 8192), idT, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sV, kk, 16384), desc_k(st + 32768, kk, 8192), idT, kk > 0);
+        mma_commit(&bar[3 + (i & 1)]);
+      };
+      mbar_expect_tx(&bar[0], 65536);
+      for (int kb = 0; kb < 2; ++kb) {
+        tma_load_2d(sK + kb * 16384, &mkv128, &bar[0], D + h * HD + 32 * kb, row0 + k0);
+        tma_load_2d(sV + kb * 16384, &mkv128, &bar[0], 2 * D + h * HD + 32 * kb, row0 + k0);
+      }
+      load_q(0);
+      if (nq > 1) load_q(1);
+      mbar_wait(&bar[0], 0);
+      issue_sp(0);
+      for (int i = 0; i < nq; ++i) {
+        // S^T/dP^T(i+1) overwrite the buffers of tile i-1, released with its P^T, dS^T (waited
+        // for in the previous iteration; bar[5] must not be re-waited on an old phase)
+        if (i + 1 < nq) issue_sp(i + 1);
+        mbar_wait(&bar[5], i & 1);  // P^T(i), dS^T(i) in TMEM
+        tc_fence_after();
+        uint8_t* st = sQG + (i & 1) * 65536;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdV, tPT + kk * 8, desc_mn(st + 49152, kk), idG, (i | kk) > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdK, tDST + kk * 8, desc_mn(st + 16384, kk), idG, (i | kk) > 0);
+        mma_commit(&bar[6 + (i & 1)]);
+        if (i + 2 < nq) {  // stage i&1 is free once dV/dK(i) have read it
+          mbar_wait(&bar[6 + (i & 1)], (i >> 1) & 1);
+          load_q(i + 2);
+        }
       }
     }
-  };
-  if (tid == 0) {
-    mbar_expect_tx(&bar[0], 65536);
-    for (int kb = 0; kb < 2; ++kb) {
-      tma_load_2d(sK + kb * 16384, &mkv128, &bar[0], D + h * HD + 32 * kb, row0 + k0);
-      tma_load_2d(sV + kb * 16384, &mkv128, &bar[0], 2 * D + h * HD + 32 * kb, row0 + k0);
-    }
-    load_q(k0);
-  }
-  constexpr uint32_t idT = idesc_tf32(128, 64, false, false);   // S^T, dP^T
-  constexpr uint32_t idG = idesc_tf32(128, 64, false, true);    // dV, dK (B MN-major)
-  const int key = k0 + tid;
-  const float* lse_bh = lse2 + static_cast<long>(bh) * T;
-  const float* di_bh = Di + static_cast<long>(bh) * T;
-  uint32_t ph = 0;
-  for (int i = 0; i < nq; ++i, ph ^= 1) {
-    const int q0 = k0 + 64 * i;
-    if (tid == 0) {
-      if (i == 0) mbar_wait(&bar[0], 0);
-      mbar_wait(&bar[1], ph);
+    __syncwarp();
+  } else {
+    const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
+    const int key = k0 + tid;
+    const float* lse_bh = lse2 + static_cast<long>(bh) * T;
+    const float* di_bh = Di + static_cast<long>(bh) * T;
+    float* sLD = reinterpret_cast<float*>(bar + 10);  // [2][lse 64 | Di 64] per query tile
+    for (int i = 0; i < nq; ++i) {
+      const int q0 = k0 + 64 * i;
+      // the tile's 64 lse / Di values, one per compute thread, staged for broadcast reads
+      float* ld = sLD + (i & 1) * 128;
+      {
+        const int q = q0 + (tid & 63);
+        ld[tid] = q < T ? (tid < 64 ? lse_bh[q] : di_bh[q]) : 0.f;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(&bar[3 + (i & 1)], (i >> 1) & 1);
       tc_fence_after();
+      float s[64], dp[64];
+      tmem_ld64(tb + (i & 1) * 64 + lane_off, s);
+      tmem_ld64(tb + 128 + (i & 1) * 64 + lane_off, dp);
+      const bool full = q0 >= k0 + 127 && q0 + 63 < T;  // no masked (query, key) pair in the tile
+      if (full) {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sK, kk, 16384), desc_k(sQk, kk, 8192), idT, kk > 0);
+        for (int c = 0; c < 64; ++c) {
+          const float p = fast_exp2(fmaf(s[c], kScaleLog2, -ld[c]));
+          s[c] = tf32_rna(p);
+          dp[c] = tf32_rna(p * (dp[c] - ld[64 + c]) * 0.125f);
+        }
+      } else {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sV, kk, 16384), desc_k(sGk, kk, 8192), idT, kk > 0);
-      mma_commit(&bar[2]);
+        for (int c = 0; c < 64; ++c) {
+          const int q = q0 + c;
+          const bool valid = q >= key && q < T;
+          const float p = valid ? fast_exp2(fmaf(s[c], kScaleLog2, -ld[c])) : 0.f;
+          s[c] = tf32_rna(p);
+          dp[c] = valid ? tf32_rna(p * (dp[c] - ld[64 + c]) * 0.125f) : 0.f;
+        }
+      }
+      if (i >= 1) mbar_wait(&bar[6 + ((i - 1) & 1)], ((i - 1) >> 1) & 1);  // P^T, dS^T(i-1) consumed
+      tmem_st_x32(tPT + lane_off, s);
+      tmem_st_x32(tPT + lane_off + 32, s + 32);
+      tmem_st_x32(tDST + lane_off, dp);
+      tmem_st_x32(tDST + lane_off + 32, dp + 32);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&bar[5]);
     }
-    mbar_wait(&bar[2], ph);
+    mbar_wait(&bar[6 + ((nq - 1) & 1)], ((nq - 1) >> 1) & 1);
     tc_fence_after();
-    float s[64], dp[64];
-    tmem_ld64(tS + lane_off, s);
-    tmem_ld64(tP + lane_off, dp);
+    float dv[64], dk[64];
+    tmem_ld64(tdV + lane_off, dv);
+    tmem_ld64(tdK + lane_off, dk);
+    if (key < T) {
+      float4* gk = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + D + h * HD);
+      float4* gv = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + 2 * D + h * HD);
 #pragma unroll
-    for (int c = 0; c < 64; ++c) {
-      const int q = q0 + c;
-      const bool valid = q >= key && q < T;
-      const float p = valid ? exp2f(s[c] * kScaleLog2 - lse_bh[q]) : 0.f;
-      s[c] = p;
-      dp[c] = valid ? p * (dp[c] - di_bh[q]) * 0.125f : 0.f;
-    }
-    store_row64(sP, tid, 16384, s);
-    store_row64(sS, tid, 16384, dp);
-    proxy_fence();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tdV, desc_k(sP, kk, 16384), desc_mn(sGm, kk), idG, (i | kk) > 0);
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tdK, desc_k(sS, kk, 16384), desc_mn(sQm, kk), idG, (i | kk) > 0);
-      mma_commit(&bar[3]);
-      mbar_wait(&bar[3], ph);  // operands free: fetch the next query tile
-      if (i + 1 < nq) load_q(q0 + 64);
-    }
-    mbar_wait(&bar[3], ph);
-    tc_fence_after();
-  }
-  float dv[64], dk[64];
-  tmem_ld64(tdV + lane_off, dv);
-  tmem_ld64(tdK + lane_off, dk);
-  if (key < T) {
-    float4* gk = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + D + h * HD);
-    float4* gv = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + 2 * D + h * HD);
-#pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      gk[c] = make_float4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
-      gv[c] = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
+      for (int c = 0; c < 16; ++c) {
+        gk[c] = make_float4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
+        gv[c] = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
+      }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (tid < 32) {
+  if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc<256>(*tslot);
+    tmem_dealloc<512>(*tslot);
   }
 }
 
-// dQ of one (batch, head, 128-query tile); thread t owns query row q0 + t.
-constexpr int kDqSmem = 32768 * 2 + 16384 * 3 + 32768 + 256 + 1024;
+// dQ of one (batch, head, 128-query tile), warp-specialised and pipelined over 64-key tiles j:
+//   warp 4 (one lane) loads K/V tiles (double-buffered) and issues S(j) = Q K(j)^T and
+//   dP(j) = dO V(j)^T into TMEM (double-buffered) as soon as their tiles land, then
+//   dQ += dS(j) K(j) with dS read from TMEM (written there by the compute warps);
+//   warps 0-3 (thread = query row) turn S, dP into dS = P (dP - Di) / 8 while the tensor core
+//   works on the neighbouring tiles.
+// smem: Q, dO 32 KB each + 2 stages x (K K-major, V K-major, K MN-major) 48 KB = 160 KB;
+// TMEM: S 2 x 64, dP 2 x 64, dS 2 x 64, dQ 64 columns.
+constexpr int kDqSmem = 32768 * 2 + 2 * 49152 + 256 + 1024;
 
-__global__ void __launch_bounds__(128) attn_dq_kernel(
+__global__ void __launch_bounds__(160) attn_dq_kernel(
     const __grid_constant__ CUtensorMap mq128, const __grid_constant__ CUtensorMap mdo128,
     const __grid_constant__ CUtensorMap mk64, const __grid_constant__ CUtensorMap mkmn, int T, int H,
     const float* __restrict__ lse2, const float* __restrict__ Di, float* __restrict__ dqkv) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sQ = align1024(smem_raw);
-  uint8_t* sG = sQ + 32768;    // dO tile, K-major A
-  uint8_t* sKk = sG + 32768;   // K tile, K-major B (S = Q K^T)
-  uint8_t* sKm = sKk + 16384;  // K tile, MN-major B (dQ += dS K)
-  uint8_t* sVk = sKm + 16384;  // V tile, K-major B (dP = dO V^T)
-  uint8_t* sS = sVk + 16384;   // dS [128 q x 64 keys], K-major A
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sS + 32768);  // q, kv, mma1, mma2
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 8);
+  uint8_t* sG = sQ + 32768;
+  uint8_t* sKV = sG + 32768;  // stage s: Kk at +0, Vk at +16K, Km at +32K
+  // barriers: 0 q/do, 1-2 kv[2], 3-4 sp[2] (S, dP landed), 5-6 ds[2] (dS written), 7-8 dq[2]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sKV + 2 * 49152);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 10);
   const int tid = threadIdx.x;
+  const int warp = tid >> 5;
   const int nqt = (T + 127) / 128;
   const int bh = blockIdx.x / nqt;
   const int qt = nqt - 1 - blockIdx.x % nqt;
@@ -409,88 +543,120 @@ __global__ void __launch_bounds__(128) attn_dq_kernel(
     tma_prefetch_desc(&mdo128);
     tma_prefetch_desc(&mk64);
     tma_prefetch_desc(&mkmn);
-    for (int i = 0; i < 4; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 9; ++i) mbar_init(&bar[i], i == 5 || i == 6 ? 4 : 1);
     fence_barrier_init();
   }
-  if (tid < 32) tmem_alloc<256>(tslot);
+  if (warp == 0) tmem_alloc<512>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tS = *tslot, tP = *tslot + 64, tdQ = *tslot + 128;
-  const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
-  auto load_kv = [&](int k0) {
-    mbar_expect_tx(&bar[1], 3 * 16384);
-    for (int kb = 0; kb < 2; ++kb) {
-      tma_load_2d(sKk + kb * 8192, &mk64, &bar[1], D + h * HD + 32 * kb, row0 + k0);
-      tma_load_2d(sVk + kb * 8192, &mk64, &bar[1], 2 * D + h * HD + 32 * kb, row0 + k0);
-      for (int jn = 0; jn < 2; ++jn)
-        tma_load_2d(sKm + kb * 8192 + jn * 4096, &mkmn, &bar[1], D + h * HD + 32 * jn, row0 + k0 + 32 * kb);
+  const uint32_t tb = *tslot;  // S: tb + 64s, dP: tb + 128 + 64s, dS: tb + 256 + 64s, dQ: tb + 384
+  const uint32_t tdQ = tb + 384;
+  if (warp == 4) {
+    if (lane_id() == 0) {
+      auto load_kv = [&](int j) {
+        uint8_t* st = sKV + (j & 1) * 49152;
+        uint64_t* bb = &bar[1 + (j & 1)];
+        const int k0 = 64 * j;
+        mbar_expect_tx(bb, 3 * 16384);
+        for (int kb = 0; kb < 2; ++kb) {
+          tma_load_2d(st + kb * 8192, &mk64, bb, D + h * HD + 32 * kb, row0 + k0);
+          tma_load_2d(st + 16384 + kb * 8192, &mk64, bb, 2 * D + h * HD + 32 * kb, row0 + k0);
+          for (int jn = 0; jn < 2; ++jn)
+            tma_load_2d(st + 32768 + kb * 8192 + jn * 4096, &mkmn, bb, D + h * HD + 32 * jn, row0 + k0 + 32 * kb);
+        }
+      };
+      constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
+      constexpr uint32_t idQ = idesc_tf32(128, 64, false, true);
+      auto issue_sp = [&](int j) {
+        uint8_t* st = sKV + (j & 1) * 49152;
+        mbar_wait(&bar[1 + (j & 1)], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tS = tb + (j & 1) * 64, tP = tb + 128 + (j & 1) * 64;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(st, kk, 8192), idS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sG, kk, 16384), desc_k(st + 16384, kk, 8192), idS, kk > 0);
+        mma_commit(&bar[3 + (j & 1)]);
+      };
+      mbar_expect_tx(&bar[0], 65536);
+      for (int kb = 0; kb < 2; ++kb) {
+        tma_load_2d(sQ + kb * 16384, &mq128, &bar[0], h * HD + 32 * kb, row0 + q0);
+        tma_load_2d(sG + kb * 16384, &mdo128, &bar[0], h * HD + 32 * kb, row0 + q0);
+      }
+      load_kv(0);
+      if (nkt > 1) load_kv(1);
+      mbar_wait(&bar[0], 0);
+      issue_sp(0);
+      for (int j = 0; j < nkt; ++j) {
+        // S/dP(j+1) into the TMEM buffers the compute warps released with dS(j-1)
+        if (j + 1 < nkt) issue_sp(j + 1);  // its buffers held tile j-1, whose dS was waited for
+        mbar_wait(&bar[5 + (j & 1)], (j >> 1) & 1);  // dS(j) in TMEM
+        tc_fence_after();
+        const uint32_t tdS = tb + 256 + (j & 1) * 64;
+        uint8_t* km = sKV + (j & 1) * 49152 + 32768;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdQ, tdS + kk * 8, desc_mn(km, kk), idQ, (j | kk) > 0);
+        mma_commit(&bar[7 + (j & 1)]);
+        if (j + 2 < nkt) {  // stage j&1 is free once dQ(j) has read K(j)
+          mbar_wait(&bar[7 + (j & 1)], (j >> 1) & 1);
+          load_kv(j + 2);
+        }
+      }
     }
-  };
-  if (tid == 0) {
-    mbar_expect_tx(&bar[0], 65536);
-    for (int kb = 0; kb < 2; ++kb) {
-      tma_load_2d(sQ + kb * 16384, &mq128, &bar[0], h * HD + 32 * kb, row0 + q0);
-      tma_load_2d(sG + kb * 16384, &mdo128, &bar[0], h * HD + 32 * kb, row0 + q0);
-    }
-    load_kv(0);
-  }
-  constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
-  constexpr uint32_t idQ = idesc_tf32(128, 64, false, true);
-  const int q = q0 + tid;
-  const long li = static_cast<long>(bh) * T + min(q, T - 1);
-  const float my_lse = lse2[li], my_di = Di[li];
-  uint32_t ph = 0;
-  for (int j = 0; j < nkt; ++j, ph ^= 1) {
-    const int k0 = 64 * j;
-    if (tid == 0) {
-      if (j == 0) mbar_wait(&bar[0], 0);
-      mbar_wait(&bar[1], ph);
+    __syncwarp();
+  } else {
+    const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
+    const int q = q0 + tid;
+    const long li = static_cast<long>(bh) * T + min(q, T - 1);
+    const float my_lse = lse2[li], my_di = Di[li];
+    for (int j = 0; j < nkt; ++j) {
+      const int k0 = 64 * j;
+      mbar_wait(&bar[3 + (j & 1)], (j >> 1) & 1);
       tc_fence_after();
+      float s[64], dp[64];
+      tmem_ld64(tb + (j & 1) * 64 + lane_off, s);
+      tmem_ld64(tb + 128 + (j & 1) * 64 + lane_off, dp);
+      if (k0 + 63 <= q0) {  // whole tile visible (CTA-uniform)
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sKk, kk, 8192), idS, kk > 0);
+        for (int c = 0; c < 64; ++c) {
+          const float p = fast_exp2(fmaf(s[c], kScaleLog2, -my_lse));
+          s[c] = tf32_rna(p * (dp[c] - my_di) * 0.125f);
+        }
+      } else {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sG, kk, 16384), desc_k(sVk, kk, 8192), idS, kk > 0);
-      mma_commit(&bar[2]);
+        for (int c = 0; c < 64; ++c) {
+          const bool valid = k0 + c <= q;
+          const float p = valid ? fast_exp2(fmaf(s[c], kScaleLog2, -my_lse)) : 0.f;
+          s[c] = valid ? tf32_rna(p * (dp[c] - my_di) * 0.125f) : 0.f;
+        }
+      }
+      if (j >= 2) {  // dQ(j-2) has finished reading this dS buffer
+        mbar_wait(&bar[7 + (j & 1)], ((j - 2) >> 1) & 1);
+      }
+      const uint32_t tdS = tb + 256 + (j & 1) * 64 + lane_off;
+      tmem_st_x32(tdS, s);
+      tmem_st_x32(tdS + 32, s + 32);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane_id() == 0) mbar_arrive(&bar[5 + (j & 1)]);
     }
-    mbar_wait(&bar[2], ph);
+    mbar_wait(&bar[7 + ((nkt - 1) & 1)], ((nkt - 1) >> 1) & 1);
     tc_fence_after();
-    float s[64], dp[64];
-    tmem_ld64(tS + lane_off, s);
-    tmem_ld64(tP + lane_off, dp);
+    float dq[64];
+    tmem_ld64(tdQ + lane_off, dq);
+    if (q < T) {
+      float4* g = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + q) * 3 * D + h * HD);
 #pragma unroll
-    for (int c = 0; c < 64; ++c) {
-      const bool valid = k0 + c <= q;
-      const float p = valid ? exp2f(s[c] * kScaleLog2 - my_lse) : 0.f;
-      s[c] = valid ? p * (dp[c] - my_di) * 0.125f : 0.f;
+      for (int c = 0; c < 16; ++c) g[c] = make_float4(dq[4 * c], dq[4 * c + 1], dq[4 * c + 2], dq[4 * c + 3]);
     }
-    store_row64(sS, tid, 16384, s);
-    proxy_fence();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32(tdQ, desc_k(sS, kk, 16384), desc_mn(sKm, kk), idQ, (j | kk) > 0);
-      mma_commit(&bar[3]);
-      mbar_wait(&bar[3], ph);
-      if (j + 1 < nkt) load_kv(k0 + 64);
-    }
-    mbar_wait(&bar[3], ph);
-    tc_fence_after();
-  }
-  float dq[64];
-  tmem_ld64(tdQ + lane_off, dq);
-  if (q < T) {
-    float4* g = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + q) * 3 * D + h * HD);
-#pragma unroll
-    for (int c = 0; c < 16; ++c) g[c] = make_float4(dq[4 * c], dq[4 * c + 1], dq[4 * c + 2], dq[4 * c + 3]);
   }
   tc_fence_before();
   __syncthreads();
-  if (tid < 32) {
+  if (warp == 0) {
     tc_fence_after();
-    tmem_dealloc<256>(*tslot);
+    tmem_dealloc<512>(*tslot);
   }
 }
 
@@ -540,9 +706,9 @@ cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* 
   attn_di_kernel<<<static_cast<int>((n * 32 + 255) / 256), 256, 0, st>>>(n, T, H, out, dout, Di);
   const int tiles = (T + 127) / 128;
   count_launch();
-  attn_dkdv_kernel<<<B * H * tiles, 128, kDkvSmem, st>>>(mkv128, mq64, mqmn, mdo64, mdomn, T, H, lse2, Di, dqkv);
+  attn_dkdv_kernel<<<B * H * tiles, 160, kDkvSmem, st>>>(mkv128, mq64, mqmn, mdo64, mdomn, T, H, lse2, Di, dqkv);
   count_launch();
-  attn_dq_kernel<<<B * H * tiles, 128, kDqSmem, st>>>(mq128, mdo128, mk64, mkmn, T, H, lse2, Di, dqkv);
+  attn_dq_kernel<<<B * H * tiles, 160, kDqSmem, st>>>(mq128, mdo128, mk64, mkmn, T, H, lse2, Di, dqkv);
   return cudaGetLastError();
 }
 

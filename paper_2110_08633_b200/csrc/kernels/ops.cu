@@ -185,6 +185,90 @@ __global__ void reduce_parts_kernel(int parts, int N, const float* __restrict__ 
   }
 }
 
+// Column sums in one launch, deterministic: block (x, y) sums rows [y*rpb, (y+1)*rpb) of the
+// 128-column strip x (32 lanes x float4, 8 row groups, fixed-order smem reduction) into
+// part[y]; the last block of a strip to finish (atomic ticket) adds the strip's partials in
+// row-block order and resets the ticket, so the result does not depend on block timing.
+__device__ unsigned g_colsum_ticket[4096];
+
+__global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const float* __restrict__ X, long ldx,
+                                                           float* __restrict__ part, float* __restrict__ out,
+                                                           int accumulate, int rows_per_block) {
+  __shared__ float4 red[8][33];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int c = (blockIdx.x * 32 + lane) * 4;
+  const int r0 = blockIdx.y * rows_per_block;
+  const int r1 = min(M, r0 + rows_per_block);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c < N) {
+#pragma unroll 4
+    for (int r = r0 + ty; r < r1; r += 8) {
+      const float4 v = *reinterpret_cast<const float4*>(X + static_cast<long>(r) * ldx + c);
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+  }
+  red[ty][lane] = acc;
+  __syncthreads();
+  if (ty == 0) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) {
+      const float4 u = red[y][lane];
+      t.x += u.x;
+      t.y += u.y;
+      t.z += u.z;
+      t.w += u.w;
+    }
+    if (c < N) *reinterpret_cast<float4*>(part + static_cast<long>(blockIdx.y) * N + c) = t;
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(&g_colsum_ticket[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // this strip's 128 columns over gridDim.y partials: 8 row groups, fixed order
+  float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (c < N) {
+    for (int b = ty; b < static_cast<int>(gridDim.y); b += 8) {
+      const float4 u = __ldcg(reinterpret_cast<const float4*>(part + static_cast<long>(b) * N + c));
+      t.x += u.x;
+      t.y += u.y;
+      t.z += u.z;
+      t.w += u.w;
+    }
+  }
+  red[ty][lane] = t;
+  __syncthreads();
+  if (ty == 0) {
+    float4 f = red[0][lane];
+#pragma unroll
+    for (int y = 1; y < 8; ++y) {
+      const float4 u = red[y][lane];
+      f.x += u.x;
+      f.y += u.y;
+      f.z += u.z;
+      f.w += u.w;
+    }
+    if (c < N) {
+      float4* o = reinterpret_cast<float4*>(out + c);
+      if (accumulate) {
+        const float4 p = *o;
+        f.x += p.x;
+        f.y += p.y;
+        f.z += p.z;
+        f.w += p.w;
+      }
+      *o = f;
+    }
+    if (lane == 0) g_colsum_ticket[blockIdx.x] = 0;
+  }
+}
+
 // Partial column sums over a row range per block; 256 threads stride the columns.
 __global__ void colsum_part_kernel(int M, int N, const float* __restrict__ X, long ldx, float* __restrict__ part,
                                    int rows_per_block) {
@@ -743,6 +827,18 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
 }
 
 cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float* out, bool accumulate, float* ws) {
+  const int strips = (N + 127) / 128;
+  if (N % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(out) & 15) == 0 && strips <= 4096 && M > 0) {
+    // ~2 waves of blocks, >= 32 rows per block, <= colsum_blocks(M) partials (the ws size)
+    int nb = std::max(1, std::min(colsum_blocks(M), (2 * sms() + strips - 1) / strips));
+    nb = std::min(nb, std::max(1, M / 32));
+    const int rpb = (M + nb - 1) / nb;
+    nb = (M + rpb - 1) / rpb;
+    count_launch();
+    colsum_fused_kernel<<<dim3(strips, nb), 256, 0, s>>>(M, N, X, ldx, ws, out, accumulate ? 1 : 0, rpb);
+    return cudaGetLastError();
+  }
   const int nb = colsum_blocks(M);
   const int rpb = (M + nb - 1) / nb;
   dim3 grid((N + 255) / 256, nb);
