@@ -316,24 +316,28 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ C
   }
 }
 
-// Di[bh*T + q] = sum_c dO[q, h*64 + c] * O[q, h*64 + c]; one warp per (row, head).
+// Di[bh*T + q] = sum_c dO[q, h*64 + c] * O[q, h*64 + c]; one thread per (row, head): 32
+// independent 128-bit loads in flight per thread (the 256-byte head slices are fully used).
 __global__ void attn_di_kernel(long n, int T, int H, const float* __restrict__ out, const float* __restrict__ dout,
                                float* __restrict__ Di) {
-  const long w = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  const long w = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (w >= n) return;
   const long row = w / H;
   const int h = static_cast<int>(w % H);
   const long D = static_cast<long>(H) * HD;
-  const float2 a = reinterpret_cast<const float2*>(out + row * D + h * HD)[lane];
-  const float2 g = reinterpret_cast<const float2*>(dout + row * D + h * HD)[lane];
-  float v = a.x * g.x + a.y * g.y;
+  const float4* a = reinterpret_cast<const float4*>(out + row * D + h * HD);
+  const float4* g = reinterpret_cast<const float4*>(dout + row * D + h * HD);
+  float4 av[16], gv[16];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) {
-    const long b = row / T, q = row % T;
-    Di[(b * H + h) * T + q] = v;
+  for (int c = 0; c < 16; ++c) {
+    av[c] = __ldg(a + c);
+    gv[c] = __ldg(g + c);
   }
+  float v = 0.f;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) v += (av[c].x * gv[c].x + av[c].y * gv[c].y) + (av[c].z * gv[c].z + av[c].w * gv[c].w);
+  const long b = row / T, q = row % T;
+  Di[(b * H + h) * T + q] = v;
 }
 
 // dK, dV of one (batch, head, 128-key tile), warp-specialised and pipelined over 64-query
@@ -703,7 +707,7 @@ cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* 
   }
   const long n = rows * H;
   count_launch();
-  attn_di_kernel<<<static_cast<int>((n * 32 + 255) / 256), 256, 0, st>>>(n, T, H, out, dout, Di);
+  attn_di_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, st>>>(n, T, H, out, dout, Di);
   const int tiles = (T + 127) / 128;
   count_launch();
   attn_dkdv_kernel<<<B * H * tiles, 160, kDkvSmem, st>>>(mkv128, mq64, mqmn, mdo64, mdomn, T, H, lse2, Di, dqkv);
