@@ -248,6 +248,11 @@ def run_hydra(args, cfg):
     req = dict(strategy="sharp", gpus=n, run_devices=[rank], device_ids=device_ids,
                passes=args.steps, warmup_passes=args.warmup, host_opt_fraction=args.host_opt_fraction,
                opt_state=args.opt_state)
+    if args.schedule == "dynamic":
+        # one process drives every GPU (one worker thread each) so the live scheduler sees them all
+        if world > 1:
+            raise SystemExit("--schedule dynamic runs all GPUs from one process: launch without torchrun")
+        req.update(schedule="dynamic", run_devices=list(range(n)), device_ids=list(range(n)))
     t_setup = time.perf_counter()
     ex = P.Executor(cfg, **req)
     setup_s = time.perf_counter() - t_setup
@@ -295,7 +300,7 @@ def run_hydra(args, cfg):
         "dtype": "fp32 (tf32 tensor-core GEMMs)",
         "data": "synthetic tokens (splitmix64), GPT-2 random init",
         "config": dict(workload_desc(cfg, args.config), host_opt_fraction=args.host_opt_fraction,
-                       opt_state=args.opt_state),
+                       opt_state=args.opt_state, schedule=args.schedule),
         "e2e": {"value": round(samples / wall, 3), "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "note": "host wall clock around the public hy_executor_run call; every step moves params, "
@@ -419,6 +424,9 @@ def main():
     ap.add_argument("--host-opt-fraction", type=float, default=0.0)
     ap.add_argument("--opt-state", default="fp32", choices=["fp32", "bf16"])
     ap.add_argument("--no-variants", action="store_true", help="skip the other opt-state measurement")
+    ap.add_argument("--schedule", default="plan", choices=["plan", "dynamic"],
+                    help="plan: replay the reference engine's dispatch log (default); dynamic: the SHARP "
+                         "scheduler driven live by measured completions, all GPUs in this one process")
     args = ap.parse_args()
     cfg = load_config(args.config)
     if args.impl == "reference":

@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -55,6 +56,12 @@ struct ExecOptions {
   // layers' moments resident across the owning job's minibatches (write-back jobs only).
   bool mv_cache = true;
   double mv_cache_max_bytes = -1;  // < 0: no limit beyond the cap (tests use a small limit)
+  // Dynamic-time scheduling: run the strategy's TaskScheduler live on measured completions
+  // (one fresh scheduler per pass from the factory) instead of replaying the plan. Jobs may
+  // then land on other GPUs than in the virtual plan; all of them are set up on every GPU of
+  // this process.
+  bool dynamic = false;
+  std::function<std::unique_ptr<TaskScheduler>()> scheduler_factory;
 };
 
 struct ExecStats {
@@ -84,6 +91,7 @@ struct ExecResult {
   std::vector<double> pass_seconds;            // per timed pass (max over devices)
   std::map<std::string, double> op_profile_ms; // HY_PROFILE=1: compute-stream time per op (last pass)
   ExecStats stats;
+  std::vector<Dispatch> dispatch_log;          // dynamic mode: the measured dispatch order (last pass)
 };
 
 struct ExecutorImpl;

@@ -93,6 +93,17 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   ex.write_through = req.value("write_through", false);
   ex.mv_cache = req.value("mv_cache", true);
   ex.mv_cache_max_bytes = req.value("mv_cache_max_bytes", -1.0);
+  const std::string schedule = req.value("schedule", std::string("plan"));
+  if (schedule != "plan" && schedule != "dynamic") throw InvalidArgument("schedule must be 'plan' or 'dynamic'");
+  if (schedule == "dynamic") {
+    ex.dynamic = true;
+    Session* raw = S.get();
+    ex.scheduler_factory = [raw]() {
+      CompiledStrategy c = build_strategy(strategy_for(raw->cfg, strategy_kind_from_string(raw->strategy)), raw->jobs,
+                                          raw->cfg.cluster, raw->cfg.options.buffer_policy);
+      return std::move(c.scheduler);
+    };
+  }
   const std::string prec = req.value("precision", std::string("tf32"));
   if (prec != "tf32" && prec != "fp32") throw InvalidArgument("precision must be 'tf32' or 'fp32'");
   ex.precision_fp32 = prec == "fp32";
@@ -136,6 +147,16 @@ ojson session_result(Session& S, bool with_trace) {
   char h[32];
   std::snprintf(h, sizeof h, "%016llx", S.plan.hash());
   out["dispatch_hash"] = h;
+  if (!r.dispatch_log.empty()) {  // dynamic mode: what actually ran (last pass)
+    DispatchPlan measured;
+    measured.order = r.dispatch_log;
+    std::snprintf(h, sizeof h, "%016llx", measured.hash());
+    out["dispatch_hash_measured"] = h;
+    ojson dl = ojson::array();
+    for (const Dispatch& d : r.dispatch_log) dl.push_back({d.task, d.device, d.prefetch ? 1 : 0});
+    out["dispatch_measured"] = dl;
+    out["schedule"] = "dynamic";
+  }
   out["virtual_makespan_s"] = S.plan.trace.makespan_s;
   out["plan_wall_s"] = S.plan_s;
   out["pass_seconds"] = r.pass_seconds;

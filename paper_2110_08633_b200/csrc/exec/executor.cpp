@@ -26,6 +26,7 @@
 #include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <optional>
 #include <cstdio>
 #include <cstring>
 #include <deque>
@@ -292,6 +293,15 @@ struct ExecutorImpl {
   void setup_host_job(int j);
   void setup_worker(Worker& w);
   void run_pass(int pass, bool timed, ExecResult& res);
+  void dynamic_dispatch(Worker& w, int pass);
+  // dynamic-time scheduling state (one scheduler per pass, shared by the GPU workers)
+  struct Dynamic {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::unique_ptr<TaskScheduler> sched;
+    int done = 0;
+    std::vector<Dispatch> log;
+  } dyn;
   void enqueue_task(Worker& w, int t, int pass);
   void adam_layer(Worker& w, HostJob& hj, int s, float* base, int layer, const float* grads, int step,
                   cudaEvent_t done, int part = 0);
@@ -659,6 +669,10 @@ void ExecutorImpl::setup(ExecResult& res) {
     w->plan_dev = d;
     w->cuda_dev = exec.device_ids.empty() ? d : exec.device_ids.at(static_cast<size_t>(d));
     w->tasks = per_dev[static_cast<size_t>(d)];
+    if (exec.dynamic) {  // any job may land on any executed GPU: size for all of them
+      w->tasks.clear();
+      for (size_t t = 0; t < tasks.size(); ++t) w->tasks.push_back(static_cast<int>(t));
+    }
     for (int t : w->tasks) {
       const int j = tasks[static_cast<size_t>(t)].t.job;
       if (!jobs.count(j)) {
@@ -676,7 +690,9 @@ void ExecutorImpl::setup(ExecResult& res) {
       if (dev < 0) dev = task_device[t];
       one = one && task_device[t] == dev;
     }
-    kv.second.write_back = one && !exec.write_through;
+    // dynamic mode: the scheduler keeps a job on one GPU within a pass (double buffering);
+    // every cache is written back and released at the end of each pass
+    kv.second.write_back = (one || exec.dynamic) && !exec.write_through;
   }
   for (auto& w : workers) setup_worker(*w);
   host_loss = static_cast<double*>(pinned(sizeof(double) * tasks.size()));
@@ -861,7 +877,10 @@ Worker::MvEntry* ExecutorImpl::acquire_moments(Worker& w, HostJob& hj, int layer
     if (w.mv_owner >= 0) {
       // the owner still has tasks ahead of it on this GPU in this pass: stream instead
       auto it = w.last_local_of_job.find(w.mv_owner);
-      if (w.mv_owner_pass == w.cur_pass && it != w.last_local_of_job.end() && it->second > w.cur_local) return nullptr;
+      if (!exec.dynamic && w.mv_owner_pass == w.cur_pass && it != w.last_local_of_job.end() &&
+          it->second > w.cur_local) {
+        return nullptr;
+      }
       release_moments(w, false);
     }
     w.mv_owner = hj.job;
@@ -1550,7 +1569,82 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   flag_cv.notify_all();
 }
 
+// Dynamic-time scheduling (ExecOptions::dynamic): instead of replaying the virtual engine's
+// dispatch log, every GPU's worker asks the strategy's own TaskScheduler (a fresh instance per
+// pass, shared under one mutex, so its single-threaded semantics hold) with the engine's
+// protocol (sim.cpp enqueue / start_compute / compute_finished / finish): an idle GPU asks
+// next_task(dev, false, -1); when a task starts computing with nothing queued behind it the
+// GPU asks for a prefetch next_task(dev, true, task) whose loads overlap that compute; a task
+// completes (on_complete) when its compute ends on the device (CUDA event), and idle GPUs
+// re-ask. Durations are therefore the
+// real ones: which GPU frees up first, and so which job goes where, follows the hardware
+// rather than the cost model.
+void ExecutorImpl::dynamic_dispatch(Worker& w, int pass) {
+  w.tasks.clear();
+  std::deque<int> queue;  // dispatched, compute not yet finished
+  auto dispatch = [&](int t, bool prefetch) {
+    task_device[static_cast<size_t>(t)] = w.plan_dev;
+    task_local[static_cast<size_t>(t)] = static_cast<int>(w.tasks.size());
+    w.tasks.push_back(t);
+    dyn.sched->on_dispatch(t, w.plan_dev);
+    dyn.log.push_back(Dispatch{t, w.plan_dev, prefetch, 0.0});
+  };
+  const int total = static_cast<int>(tasks.size());
+  for (;;) {
+    if (queue.empty()) {  // idle GPU: ask for new work
+      int t = -1;
+      {
+        std::unique_lock<std::mutex> lk(dyn.mu);
+        if (dyn.done >= total) break;
+        const std::optional<int> pick = dyn.sched->next_task(w.plan_dev, false, -1);
+        if (pick) {
+          t = *pick;
+          dispatch(t, false);
+        } else {
+          dyn.cv.wait_for(lk, std::chrono::milliseconds(1));  // until another GPU completes a task
+          continue;
+        }
+      }
+      enqueue_task(w, t, pass);
+      queue.push_back(t);
+    }
+    const int front = queue.front();
+    if (queue.size() == 1 && options.double_buffering) {  // front starts computing: prefetch ask
+      int t2 = -1;
+      {
+        std::lock_guard<std::mutex> lk(dyn.mu);
+        const std::optional<int> pick = dyn.sched->next_task(w.plan_dev, true, front);
+        if (pick) {
+          t2 = *pick;
+          dispatch(t2, true);
+        }
+      }
+      if (t2 >= 0) {
+        enqueue_task(w, t2, pass);
+        queue.push_back(t2);
+      }
+    }
+    const TaskTiming& tm = w.timing[static_cast<size_t>(task_local[static_cast<size_t>(front)])];
+    check_cuda(cudaEventSynchronize(tm.c1), "compute done");
+    queue.pop_front();
+    {
+      // The engine completes a task before its chain successor may start computing (the
+      // successor's predecessors include it); here its drains may still be in flight, but
+      // every data hazard is ordered on the device, so the scheduler is told now.
+      std::lock_guard<std::mutex> lk(dyn.mu);
+      dyn.sched->on_complete(front);
+      ++dyn.done;
+    }
+    dyn.cv.notify_all();
+  }
+}
+
 void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
+  if (exec.dynamic) {
+    dyn.sched = exec.scheduler_factory();
+    dyn.done = 0;
+    dyn.log.clear();
+  }
   std::vector<std::thread> threads;
   std::vector<std::exception_ptr> errs(workers.size());
   for (size_t i = 0; i < workers.size(); ++i) {
@@ -1567,10 +1661,15 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
           check_cuda(cudaStreamWaitEvent(s, w.t0, 0), "t0 wait");
         }
         const auto h0 = std::chrono::steady_clock::now();
-        for (int t : w.tasks) enqueue_task(w, t, pass);
+        if (exec.dynamic) {
+          dynamic_dispatch(w, pass);
+        } else {
+          for (int t : w.tasks) enqueue_task(w, t, pass);
+        }
         // end of pass: the cache's updated params reach the host (they stay cached)
         for (auto& e : w.live) write_back(w, *e);
-        release_moments(w, true);
+        // (dynamic: a job may run on another GPU next pass, so moments are released too)
+        release_moments(w, !exec.dynamic);
         w.enqueue_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count();
         // join all streams into comp, then record the end
         cudaStream_t others[6] = {w.down, w.up, w.opt, w.hopt, w.opt2, w.optin};
@@ -1593,6 +1692,7 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res) {
   for (auto& e : errs) {
     if (e) std::rethrow_exception(e);
   }
+  if (exec.dynamic) res.dispatch_log = dyn.log;
   if (timed) collect(pass, res);
 }
 

@@ -170,3 +170,30 @@ def test_moment_cache_matches_oracle(tmp_path):
     res = compare(cfg, tmp_path, precision="fp32", loss_tol=1e-5, param_tol=1e-4, hbm_slack_bytes=60e6,
                   opt_chunk_floats=65536)
     assert res["stats"]["mv_resident_updates_per_pass"] > 0
+
+
+def test_dynamic_schedule_one_gpu(tmp_path):
+    """Dynamic-time scheduling (the strategy's TaskScheduler driven live by measured
+    completions, §8f row 1): on one GPU SHARP's choices do not depend on timing, so the measured
+    dispatch order equals the virtual plan's; numerics match the oracle."""
+    cfg = tiny_config(mbs=3)
+    res = compare(cfg, tmp_path, schedule="dynamic", precision="fp32", loss_tol=1e-5, param_tol=1e-4)
+    assert res["schedule"] == "dynamic"
+    assert res["dispatch_hash_measured"] == res["dispatch_hash"]
+
+
+def test_dynamic_schedule_two_workers(tmp_path):
+    """Two plan devices driven by two worker threads on the one physical GPU: every task runs
+    exactly once, each job stays on one device (double buffering), results match the oracle."""
+    cfg = tiny_config(mbs=2, jobs=4)
+    res = compare(cfg, tmp_path, schedule="dynamic", gpus=2, device_ids=[0, 0], precision="fp32", loss_tol=1e-5,
+                  param_tol=1e-4)
+    disp = res["dispatch_measured"]
+    n_tasks = len(P.plan(cfg, gpus=2)["tasks"])
+    assert sorted(t for t, _, _ in disp) == list(range(n_tasks))
+    plan = P.plan(cfg, gpus=2)
+    dev_of_job = {}
+    for t, d, _ in disp:
+        j = plan["tasks"][t]["job"]
+        assert dev_of_job.setdefault(j, d) == d
+    assert set(dev_of_job.values()) == {0, 1}
