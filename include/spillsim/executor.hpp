@@ -61,6 +61,9 @@ struct ExecOptions {
   // then land on other GPUs than in the virtual plan; all of them are set up on every GPU of
   // this process.
   bool dynamic = false;
+  // P2P hand-off: a boundary activation / gradient still resident on another GPU of this process
+  // is copied device to device instead of promoted from the host checkpoint
+  bool p2p = true;
   std::function<std::unique_ptr<TaskScheduler>()> scheduler_factory;
 };
 
@@ -74,6 +77,7 @@ struct ExecStats {
   double host_grad_d2h_bytes = 0, refresh_h2d_bytes = 0;  // their GradOffload / resident-slot refresh
   double writeback_d2h_bytes = 0;   // params written back by the cache (eviction / pass end)
   double mv_load_h2d_bytes = 0, mv_writeback_d2h_bytes = 0;  // moment cache fills / write-backs
+  double p2p_bytes = 0;             // boundary activations / gradients handed over GPU to GPU
   double mv_resident_updates = 0;   // parameter updates whose moments were HBM-resident
   std::vector<double> mv_cache_bytes;  // per executed device: HBM given to the moment cache
   std::vector<double> arena_bytes;  // per executed device: HBM reserved (<= mem_bytes)

@@ -93,6 +93,7 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   ex.write_through = req.value("write_through", false);
   ex.mv_cache = req.value("mv_cache", true);
   ex.mv_cache_max_bytes = req.value("mv_cache_max_bytes", -1.0);
+  ex.p2p = req.value("p2p", true);
   const std::string schedule = req.value("schedule", std::string("plan"));
   if (schedule != "plan" && schedule != "dynamic") throw InvalidArgument("schedule must be 'plan' or 'dynamic'");
   if (schedule == "dynamic") {
@@ -190,6 +191,7 @@ ojson session_result(Session& S, bool with_trace) {
   st["mv_writeback_d2h_bytes_per_pass"] = r.stats.mv_writeback_d2h_bytes / np;
   st["mv_resident_updates_per_pass"] = r.stats.mv_resident_updates / np;
   st["mv_cache_bytes"] = r.stats.mv_cache_bytes;
+  st["p2p_bytes_per_pass"] = r.stats.p2p_bytes / np;
   st["arena_bytes"] = r.stats.arena_bytes;
   st["pinned_bytes"] = r.stats.pinned_bytes;
   st["device_busy_s_last_pass"] = r.stats.device_busy_s.empty() ? 0.0 : r.stats.device_busy_s.back();

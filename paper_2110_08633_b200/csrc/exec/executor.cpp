@@ -294,6 +294,10 @@ struct ExecutorImpl {
   void setup_worker(Worker& w);
   void run_pass(int pass, bool timed, ExecResult& res);
   void dynamic_dispatch(Worker& w, int pass);
+  // P2P hand-off between the GPUs of this process: boundary activations / gradients resident
+  // on the producer's GPU are copied device to device (NVLink) instead of through the host.
+  std::mutex peer_mu;  // guards the act/grad buffer tags of every worker
+  bool peer_fetch(Worker& w, float* dst, const Tag& want, bool grad, size_t bytes);
   // dynamic-time scheduling state (one scheduler per pass, shared by the GPU workers)
   struct Dynamic {
     std::mutex mu;
@@ -695,6 +699,19 @@ void ExecutorImpl::setup(ExecResult& res) {
     kv.second.write_back = (one || exec.dynamic) && !exec.write_through;
   }
   for (auto& w : workers) setup_worker(*w);
+  // NVLink peer access between the GPUs of this process (P2P hand-off)
+  for (auto& a : workers) {
+    for (auto& b : workers) {
+      if (a->cuda_dev == b->cuda_dev) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, a->cuda_dev, b->cuda_dev);
+      if (!can) continue;
+      check_cuda(cudaSetDevice(a->cuda_dev), "set device");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b->cuda_dev, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) check_cuda(e, "enable peer access");
+      cudaGetLastError();
+    }
+  }
   host_loss = static_cast<double*>(pinned(sizeof(double) * tasks.size()));
   host_threads = exec.host_opt_threads > 0 ? exec.host_opt_threads
                                            : std::max(1, static_cast<int>(std::thread::hardware_concurrency()) - 4);
@@ -1328,16 +1345,20 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       ain = 0;
       // don't clobber a resident buffer that the forward output will need: pick the older
       if (w.abuf_tag[0].job >= 0 && w.abuf_tag[1].job < 0) ain = 1;
+      std::lock_guard<std::mutex> lk(peer_mu);
+      w.abuf_tag[ain] = Tag{};
       w.abuf_tr[ain].before_write(w.down);
-      hj.ckpt_tr[static_cast<size_t>(s - 1)]->before_read(w.down);
-      check_cuda(xfer(w.abuf[ain], hj.ckpt[static_cast<size_t>(s - 1)], act_bytes, cudaMemcpyHostToDevice,
-                                 w.down),
-                 "act h2d");
-      hj.ckpt_tr[static_cast<size_t>(s - 1)]->after_read(w.down);
+      if (!peer_fetch(w, w.abuf[ain], at, false, act_bytes)) {
+        hj.ckpt_tr[static_cast<size_t>(s - 1)]->before_read(w.down);
+        check_cuda(xfer(w.abuf[ain], hj.ckpt[static_cast<size_t>(s - 1)], act_bytes, cudaMemcpyHostToDevice,
+                                   w.down),
+                   "act h2d");
+        hj.ckpt_tr[static_cast<size_t>(s - 1)]->after_read(w.down);
+        w.st.act_h2d_bytes += static_cast<double>(act_bytes);
+        w.st.h2d_bytes += static_cast<double>(act_bytes);
+      }
       w.abuf_tr[ain].after_write(w.down);
       w.abuf_tag[ain] = at;
-      w.st.act_h2d_bytes += static_cast<double>(act_bytes);
-      w.st.h2d_bytes += static_cast<double>(act_bytes);
     } else {
       w.st.elided_act_bytes += static_cast<double>(act_bytes);
     }
@@ -1348,16 +1369,20 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     gin = find_tag(w.gbd_tag, 2, gt);
     if (gin < 0) {
       gin = 0;
+      std::lock_guard<std::mutex> lk(peer_mu);
+      w.gbd_tag[gin] = Tag{};
       w.gbd_tr[gin].before_write(w.down);
-      hj.grad_tr[static_cast<size_t>(s)]->before_read(w.down);
-      check_cuda(xfer(w.gbd[gin], hj.grad[static_cast<size_t>(s)], act_bytes, cudaMemcpyHostToDevice,
-                                 w.down),
-                 "grad h2d");
-      hj.grad_tr[static_cast<size_t>(s)]->after_read(w.down);
+      if (!peer_fetch(w, w.gbd[gin], gt, true, act_bytes)) {
+        hj.grad_tr[static_cast<size_t>(s)]->before_read(w.down);
+        check_cuda(xfer(w.gbd[gin], hj.grad[static_cast<size_t>(s)], act_bytes, cudaMemcpyHostToDevice,
+                                   w.down),
+                   "grad h2d");
+        hj.grad_tr[static_cast<size_t>(s)]->after_read(w.down);
+        w.st.act_h2d_bytes += static_cast<double>(act_bytes);
+        w.st.h2d_bytes += static_cast<double>(act_bytes);
+      }
       w.gbd_tr[gin].after_write(w.down);
       w.gbd_tag[gin] = gt;
-      w.st.act_h2d_bytes += static_cast<double>(act_bytes);
-      w.st.h2d_bytes += static_cast<double>(act_bytes);
     } else {
       w.st.elided_act_bytes += static_cast<double>(act_bytes);
     }
@@ -1402,6 +1427,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     io.act_in = ain >= 0 ? w.abuf[ain] : nullptr;
     if (!g.has_head) {
       aout = ain >= 0 ? 1 - ain : (w.abuf_tag[0].job < 0 ? 0 : (w.abuf_tag[1].job < 0 ? 1 : 0));
+      std::lock_guard<std::mutex> lk(peer_mu);
+      w.abuf_tag[aout] = Tag{};  // being overwritten: no peer may copy the old content now
       w.abuf_tr[aout].before_write(w.comp);
       io.act_out = w.abuf[aout];
     }
@@ -1411,6 +1438,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     io.grad_in = gin >= 0 ? w.gbd[gin] : nullptr;
     if (s > 0) {
       gout = gin >= 0 ? 1 - gin : 0;
+      std::lock_guard<std::mutex> lk(peer_mu);
+      w.gbd_tag[gout] = Tag{};
       w.gbd_tr[gout].before_write(w.comp);
       io.grad_out = w.gbd[gout];
     }
@@ -1514,10 +1543,12 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   if (gin >= 0) w.gbd_tr[gin].after_read(w.comp);
   if (needs_z) w.z_tr.after_read(w.comp);
   if (aout >= 0) {
+    std::lock_guard<std::mutex> lk(peer_mu);
     w.abuf_tr[aout].after_write(w.comp);
     w.abuf_tag[aout] = Tag{j, gmb, s, 0};
   }
   if (gout >= 0) {
+    std::lock_guard<std::mutex> lk(peer_mu);
     w.gbd_tr[gout].after_write(w.comp);
     w.gbd_tag[gout] = Tag{j, gmb, s - 1, 1};
   }
@@ -1567,6 +1598,31 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     enqueued_pass[static_cast<size_t>(t)] = pass;
   }
   flag_cv.notify_all();
+}
+
+// P2P hand-off (BoundaryOut::kPeer's role for SHARP chains that change GPU): when a
+// task's boundary input is still resident on another GPU of this process (the producer ran
+// there), copy it over NVLink on this GPU's down stream instead of promoting it from the host
+// checkpoint (the producer's ActDemote still writes the checkpoint, as the reference does). The
+// copy waits for the producer's write on the other GPU and registers a read, so the producer's
+// next reuse of that buffer waits for it. Caller holds peer_mu.
+bool ExecutorImpl::peer_fetch(Worker& w, float* dst, const Tag& want, bool grad, size_t bytes) {
+  if (!exec.p2p || workers.size() < 2) return false;
+  for (auto& op : workers) {
+    Worker& o = *op;
+    if (&o == &w) continue;
+    for (int i = 0; i < 2; ++i) {
+      if (!((grad ? o.gbd_tag[i] : o.abuf_tag[i]) == want)) continue;
+      Tracked& src = grad ? o.gbd_tr[i] : o.abuf_tr[i];
+      src.before_read(w.down);
+      check_cuda(cudaMemcpyPeerAsync(dst, w.cuda_dev, grad ? o.gbd[i] : o.abuf[i], o.cuda_dev, bytes, w.down),
+                 "p2p hand-off");
+      src.after_read(w.down);
+      w.st.p2p_bytes += static_cast<double>(bytes);
+      return true;
+    }
+  }
+  return false;
 }
 
 // Dynamic-time scheduling (ExecOptions::dynamic): instead of replaying the virtual engine's
@@ -1806,6 +1862,7 @@ void Executor::run(int passes, bool timed) {
       a.mv_load_h2d_bytes += b.mv_load_h2d_bytes;
       a.mv_writeback_d2h_bytes += b.mv_writeback_d2h_bytes;
       a.mv_resident_updates += b.mv_resident_updates;
+      a.p2p_bytes += b.p2p_bytes;
       a.elided_act_bytes += b.elided_act_bytes;
       a.kernel_launches += b.kernel_launches;
     }

@@ -3,6 +3,8 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cfloat>
 
 #include "launch_count.cuh"
@@ -189,11 +191,10 @@ __global__ void reduce_parts_kernel(int parts, int N, const float* __restrict__ 
 // 128-column strip x (32 lanes x float4, 8 row groups, fixed-order smem reduction) into
 // part[y]; the last block of a strip to finish (atomic ticket) adds the strip's partials in
 // row-block order and resets the ticket, so the result does not depend on block timing.
-__device__ unsigned g_colsum_ticket[4096];
-
 __global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const float* __restrict__ X, long ldx,
                                                            float* __restrict__ part, float* __restrict__ out,
-                                                           int accumulate, int rows_per_block) {
+                                                           int accumulate, int rows_per_block,
+                                                           unsigned* __restrict__ ticket) {
   __shared__ float4 red[8][33];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const f
     __threadfence();
   }
   __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(&g_colsum_ticket[blockIdx.x], 1u) == gridDim.y - 1;
+  if (threadIdx.x == 0) last = atomicAdd(&ticket[blockIdx.x], 1u) == gridDim.y - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const f
       }
       *o = f;
     }
-    if (lane == 0) g_colsum_ticket[blockIdx.x] = 0;
+    if (lane == 0) ticket[blockIdx.x] = 0;
   }
 }
 
@@ -826,9 +827,27 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
   return cudaGetLastError();
 }
 
+// The colsum tickets of a stream (allocated on first use, zeroed, self-resetting). Executor
+// workers sharing a GPU run colsums concurrently on their own compute streams, so the tickets
+// cannot live in a module global; per stream they are serialised by stream order.
+unsigned* colsum_tickets(cudaStream_t s) {
+  static std::mutex mu;
+  static std::map<cudaStream_t, unsigned*> per_stream;
+  std::lock_guard<std::mutex> lk(mu);
+  unsigned*& p = per_stream[s];
+  if (!p) {
+    if (cudaMalloc(&p, 4096 * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemsetAsync(p, 0, 4096 * sizeof(unsigned), s) != cudaSuccess) {
+      p = nullptr;
+    }
+  }
+  return p;
+}
+
 cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float* out, bool accumulate, float* ws) {
   const int strips = (N + 127) / 128;
-  if (N % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
+  unsigned* tickets = colsum_tickets(s);
+  if (tickets && N % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(out) & 15) == 0 && strips <= 4096 && M > 0) {
     // ~2 waves of blocks, >= 32 rows per block, <= colsum_blocks(M) partials (the ws size)
     int nb = std::max(1, std::min(colsum_blocks(M), (2 * sms() + strips - 1) / strips));
@@ -836,7 +855,7 @@ cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float
     const int rpb = (M + nb - 1) / nb;
     nb = (M + rpb - 1) / rpb;
     count_launch();
-    colsum_fused_kernel<<<dim3(strips, nb), 256, 0, s>>>(M, N, X, ldx, ws, out, accumulate ? 1 : 0, rpb);
+    colsum_fused_kernel<<<dim3(strips, nb), 256, 0, s>>>(M, N, X, ldx, ws, out, accumulate ? 1 : 0, rpb, tickets);
     return cudaGetLastError();
   }
   const int nb = colsum_blocks(M);

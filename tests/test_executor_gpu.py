@@ -197,3 +197,25 @@ def test_dynamic_schedule_two_workers(tmp_path):
         j = plan["tasks"][t]["job"]
         assert dev_of_job.setdefault(j, d) == d
     assert set(dev_of_job.values()) == {0, 1}
+
+
+def test_p2p_handoff_alternating_jobs(tmp_path):
+    """Double buffering off: SHARP alternates jobs between two GPUs (plan devices 0, 1 on the
+    one physical GPU here), so boundary activations / gradients produced on one GPU are consumed
+    on the other. They are handed over device to device (the reference routes them through the
+    host checkpoint); results still match the oracle, and the host promotes shrink."""
+    cfg = tiny_config(mbs=3, jobs=3)
+    plan = P.plan(cfg, gpus=2, double_buffering=False)
+    last, moves = {}, 0
+    for t, d, _ in plan["dispatch"]:
+        j = plan["tasks"][t]["job"]
+        moves += j in last and last[j] != d
+        last[j] = d
+    assert moves > 0
+    kw = dict(gpus=2, device_ids=[0, 0], double_buffering=False, precision="fp32", loss_tol=1e-5, param_tol=1e-4)
+    on = compare(cfg, tmp_path, **kw)
+    off_dir = tmp_path / "off"
+    off_dir.mkdir()
+    off = compare(cfg, off_dir, p2p=False, **kw)
+    assert on["stats"]["p2p_bytes_per_pass"] > 0 and off["stats"]["p2p_bytes_per_pass"] == 0
+    assert on["stats"]["act_h2d_bytes_per_pass"] < off["stats"]["act_h2d_bytes_per_pass"]
