@@ -68,6 +68,30 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return fmaf(2.f * x * sg * (1.f - sg), k0 * fmaf(3.f * k1, x * x, 1.f), sg);
 }
 
+// Programmatic dependent launch: the prologue above (barrier init, TMEM allocation, descriptor
+// prefetch) overlaps the previous kernel's tail; nothing the previous kernel writes is touched
+// before griddepcontrol.wait. The grid is persistent (every CTA resident from the start), so
+// letting the next GEMM launch right away only lets its CTAs take SMs as ours retire.
+__device__ __forceinline__ void pdl_wait_and_trigger() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename Kern, typename... Args>
+cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 struct TileInfo {
   int m0, n0, z1, z2;
   int kb0, nkb;  // first k-block, number of k-blocks
@@ -328,6 +352,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait_and_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -556,6 +581,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait_and_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -747,8 +773,7 @@ cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, lon
   const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
   count_launch();
-  kern<<<grid, kThreads, Smem<BN, P3>::kTotal, stream>>>(ma, mb, M, N, K, epi, b);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), Smem<BN, P3>::kTotal, stream, ma, mb, M, N, K, epi, b);
 }
 
 template <int BN, bool A_MN, bool B_MN, int MODE>
@@ -772,8 +797,8 @@ cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const float* A
   const long tiles = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
   const long pairs = std::min<long>(tiles, sm_count() / 2);
   count_launch();
-  kern<<<static_cast<int>(2 * pairs), kThreads, SmemPair<BN>::kTotal, stream>>>(ma, mb, M, N, K, epi, b);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(kThreads), SmemPair<BN>::kTotal, stream, ma, mb,
+                    M, N, K, epi, b);
 }
 
 template <int BN, int MODE>
