@@ -28,6 +28,7 @@
 #include "launch_count.cuh"
 #include "ops.cuh"
 #include "ptx.cuh"
+#include "pdl.cuh"
 
 namespace hy {
 namespace {
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ C
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait_and_trigger();
   const uint32_t tbase = *tslot;
   const uint32_t tP = tbase + 128, tPV = tbase + 192;
   const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
@@ -320,6 +322,7 @@ __global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ C
 // independent 128-bit loads in flight per thread (the 256-byte head slices are fully used).
 __global__ void attn_di_kernel(long n, int T, int H, const float* __restrict__ out, const float* __restrict__ dout,
                                float* __restrict__ Di) {
+  pdl_wait_and_trigger();
   const long w = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (w >= n) return;
   const long row = w / H;
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(160) attn_dkdv_kernel(
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait_and_trigger();
   // S^T: tb + 64s, dP^T: tb + 128 + 64s, P^T: tb + 256, dS^T: tb + 320, dV: tb + 384, dK: tb + 448
   const uint32_t tb = *tslot;
   const uint32_t tPT = tb + 256, tDST = tb + 320, tdV = tb + 384, tdK = tb + 448;
@@ -554,6 +558,7 @@ __global__ void __launch_bounds__(160) attn_dq_kernel(
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_wait_and_trigger();
   const uint32_t tb = *tslot;  // S: tb + 64s, dP: tb + 128 + 64s, dS: tb + 256 + 64s, dQ: tb + 384
   const uint32_t tdQ = tb + 384;
   if (warp == 4) {
@@ -682,8 +687,7 @@ cudaError_t attention_fwd_fa(cudaStream_t st, int B, int T, int H, const float* 
   }
   const int grid = B * H * ((T + 127) / 128);
   count_launch();
-  attn_fwd_kernel<<<grid, 128, kFwdSmem, st>>>(mq, mk, mv, T, H, out, lse2);
-  return cudaGetLastError();
+  return launch_pdl(attn_fwd_kernel, dim3(grid), dim3(128), kFwdSmem, st, mq, mk, mv, T, H, out, lse2);
 }
 
 cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* qkv, const float* out,
@@ -707,12 +711,21 @@ cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* 
   }
   const long n = rows * H;
   count_launch();
-  attn_di_kernel<<<static_cast<int>((n + 127) / 128), 128, 0, st>>>(n, T, H, out, dout, Di);
+  {
+    const cudaError_t e = launch_pdl(attn_di_kernel, dim3(static_cast<unsigned>((n + 127) / 128)), dim3(128), 0, st, n, T, H, out, dout, Di);
+    if (e != cudaSuccess) return e;
+  }
   const int tiles = (T + 127) / 128;
   count_launch();
-  attn_dkdv_kernel<<<B * H * tiles, 160, kDkvSmem, st>>>(mkv128, mq64, mqmn, mdo64, mdomn, T, H, lse2, Di, dqkv);
+  {
+    const cudaError_t e = launch_pdl(attn_dkdv_kernel, dim3(B * H * tiles), dim3(160), kDkvSmem, st, mkv128, mq64, mqmn, mdo64, mdomn, T, H, static_cast<const float*>(lse2), static_cast<const float*>(Di), dqkv);
+    if (e != cudaSuccess) return e;
+  }
   count_launch();
-  attn_dq_kernel<<<B * H * tiles, 160, kDqSmem, st>>>(mq128, mdo128, mk64, mkmn, T, H, lse2, Di, dqkv);
+  {
+    const cudaError_t e = launch_pdl(attn_dq_kernel, dim3(B * H * tiles), dim3(160), kDqSmem, st, mq128, mdo128, mk64, mkmn, T, H, static_cast<const float*>(lse2), static_cast<const float*>(Di), dqkv);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

@@ -23,6 +23,7 @@
 #include "gemm.cuh"
 #include "launch_count.cuh"
 #include "ptx.cuh"
+#include "pdl.cuh"
 
 namespace hy {
 namespace {
@@ -68,30 +69,10 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return fmaf(2.f * x * sg * (1.f - sg), k0 * fmaf(3.f * k1, x * x, 1.f), sg);
 }
 
-// Programmatic dependent launch: the prologue above (barrier init, TMEM allocation, descriptor
-// prefetch) overlaps the previous kernel's tail; nothing the previous kernel writes is touched
-// before griddepcontrol.wait. The grid is persistent (every CTA resident from the start), so
-// letting the next GEMM launch right away only lets its CTAs take SMs as ours retire.
-__device__ __forceinline__ void pdl_wait_and_trigger() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-template <typename Kern, typename... Args>
-cudaError_t launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...);
-}
-
+// Programmatic dependent launch (pdl.cuh): the prologue (barrier init, TMEM allocation,
+// descriptor prefetch) overlaps the previous kernel's tail. The grid is persistent (every CTA
+// resident from the start), so letting the next GEMM launch right away only lets its CTAs take
+// SMs as ours retire.
 struct TileInfo {
   int m0, n0, z1, z2;
   int kb0, nkb;  // first k-block, number of k-blocks

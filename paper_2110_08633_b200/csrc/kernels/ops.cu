@@ -9,9 +9,15 @@
 
 #include "launch_count.cuh"
 #include "ops.cuh"
+#include "pdl.cuh"
 
 namespace hy {
 namespace {
+
+// a failed launch_pdl leaves its error in the thread's last-error state, which the wrappers
+// return (cudaGetLastError) exactly as for <<<>>> launches
+inline void check_launch(cudaError_t e) { (void)e; }
+
 
 constexpr int kWarpsPerBlock = 8;
 
@@ -44,6 +50,7 @@ template <int kMaxVec>
 __global__ void ln_fwd_kernel(int rows, int d, const float* __restrict__ x, const float* __restrict__ g,
                               const float* __restrict__ b, float* __restrict__ y, float* __restrict__ mean_out,
                               float* __restrict__ rstd_out) {
+  pdl_wait_and_trigger();
   const int row = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (row >= rows) return;
@@ -94,6 +101,7 @@ __global__ void ln_bwd_kernel(int rows, int d, const float* __restrict__ x, cons
                               const float* __restrict__ mean, const float* __restrict__ rstd,
                               const float* __restrict__ dy, float* __restrict__ dx, int accumulate,
                               float* __restrict__ ws_dg, float* __restrict__ ws_db, int rows_per_block) {
+  pdl_wait_and_trigger();
   extern __shared__ float sh[];  // [warps][2][d]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_warps = blockDim.x >> 5;
@@ -171,6 +179,7 @@ __global__ void ln_bwd_kernel(int rows, int d, const float* __restrict__ x, cons
 // partials in fixed order => deterministic, and 8x the memory parallelism of one thread/column.
 __global__ void reduce_parts_kernel(int parts, int N, const float* __restrict__ part, float* __restrict__ out,
                                     int accumulate) {
+  pdl_wait_and_trigger();
   __shared__ float acc[8][33];
   const int n = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
@@ -195,6 +204,7 @@ __global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const f
                                                            float* __restrict__ part, float* __restrict__ out,
                                                            int accumulate, int rows_per_block,
                                                            unsigned* __restrict__ ticket) {
+  pdl_wait_and_trigger();
   __shared__ float4 red[8][33];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -320,6 +330,7 @@ __global__ void embed_pos_kernel(int B, int T, int d, const float* __restrict__ 
 // ---- softmax cross-entropy ------------------------------------------------------
 __global__ void xent_kernel(int V, float* __restrict__ logits, long ldl, const int32_t* __restrict__ targets,
                             float grad_scale, float* __restrict__ row_loss) {
+  pdl_wait_and_trigger();
   __shared__ float red_m[32], red_s[32];
   const int row = blockIdx.x;
   float* lr = logits + static_cast<long>(row) * ldl;
@@ -373,6 +384,7 @@ template <int kV4>
 __global__ void __launch_bounds__(512) xent_reg_kernel(int V, float* __restrict__ logits, long ldl,
                                                        const int32_t* __restrict__ targets, float grad_scale,
                                                        float* __restrict__ row_loss) {
+  pdl_wait_and_trigger();
   __shared__ float red[32];
   __shared__ float bcast;
   const int row = blockIdx.x;
@@ -781,13 +793,13 @@ cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const
   const int grid = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock, block = 32 * kWarpsPerBlock;
   if (d <= 1024) {
     count_launch();
-    ln_fwd_kernel<8><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
+    check_launch(launch_pdl(ln_fwd_kernel<8>, dim3(grid), dim3(block), 0, s, rows, d, x, g, b, y, mean, rstd));
   } else if (d <= 2048) {
     count_launch();
-    ln_fwd_kernel<16><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
+    check_launch(launch_pdl(ln_fwd_kernel<16>, dim3(grid), dim3(block), 0, s, rows, d, x, g, b, y, mean, rstd));
   } else {
     count_launch();
-    ln_fwd_kernel<32><<<grid, block, 0, s>>>(rows, d, x, g, b, y, mean, rstd);
+    check_launch(launch_pdl(ln_fwd_kernel<32>, dim3(grid), dim3(block), 0, s, rows, d, x, g, b, y, mean, rstd));
   }
   return cudaGetLastError();
 }
@@ -812,18 +824,18 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
   const int acc = accumulate_dx ? 1 : 0;
   if (d <= 1024) {
     count_launch();
-    ln_bwd_kernel<8><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
+    check_launch(launch_pdl(ln_bwd_kernel<8>, dim3(nb), dim3(32 * n_warps), smem, s, rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb));
   } else if (d <= 2048) {
     count_launch();
-    ln_bwd_kernel<16><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
+    check_launch(launch_pdl(ln_bwd_kernel<16>, dim3(nb), dim3(32 * n_warps), smem, s, rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb));
   } else {
     count_launch();
-    ln_bwd_kernel<32><<<nb, 32 * n_warps, smem, s>>>(rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb);
+    check_launch(launch_pdl(ln_bwd_kernel<32>, dim3(nb), dim3(32 * n_warps), smem, s, rows, d, x, g, mean, rstd, dy, dx, acc, ws_dg, ws_db, rpb));
   }
   count_launch();
-  reduce_parts_kernel<<<(d + 31) / 32, dim3(32, 8), 0, s>>>(nb, d, ws_dg, dg, 1);
+  check_launch(launch_pdl(reduce_parts_kernel, dim3((d + 31) / 32), dim3(32, 8), 0, s, nb, d, static_cast<const float*>(ws_dg), dg, 1));
   count_launch();
-  reduce_parts_kernel<<<(d + 31) / 32, dim3(32, 8), 0, s>>>(nb, d, ws_db, db, 1);
+  check_launch(launch_pdl(reduce_parts_kernel, dim3((d + 31) / 32), dim3(32, 8), 0, s, nb, d, static_cast<const float*>(ws_db), db, 1));
   return cudaGetLastError();
 }
 
@@ -855,7 +867,7 @@ cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float
     const int rpb = (M + nb - 1) / nb;
     nb = (M + rpb - 1) / rpb;
     count_launch();
-    colsum_fused_kernel<<<dim3(strips, nb), 256, 0, s>>>(M, N, X, ldx, ws, out, accumulate ? 1 : 0, rpb, tickets);
+    check_launch(launch_pdl(colsum_fused_kernel, dim3(strips, nb), dim3(256), 0, s, M, N, X, ldx, ws, out, accumulate ? 1 : 0, rpb, tickets));
     return cudaGetLastError();
   }
   const int nb = colsum_blocks(M);
@@ -892,9 +904,9 @@ cudaError_t softmax_xent(cudaStream_t s, int rows, int V, float* logits, long ld
   if (rows <= 0) return cudaSuccess;
   count_launch();
   if (V <= 512 * 4 * 25 && (ldl & 3) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0) {
-    xent_reg_kernel<25><<<rows, 512, 0, s>>>(V, logits, ldl, targets, grad_scale, row_loss);
+    check_launch(launch_pdl(xent_reg_kernel<25>, dim3(rows), dim3(512), 0, s, V, logits, ldl, targets, grad_scale, row_loss));
   } else {
-    xent_kernel<<<rows, 512, 0, s>>>(V, logits, ldl, targets, grad_scale, row_loss);
+    check_launch(launch_pdl(xent_kernel, dim3(rows), dim3(512), 0, s, V, logits, ldl, targets, grad_scale, row_loss));
   }
   return cudaGetLastError();
 }
