@@ -314,6 +314,7 @@ struct ExecutorImpl {
   void param_read_end(HostJob& hj, int s, cudaStream_t st);
   Worker::PoolEntry* acquire_params(Worker& w, HostJob& hj, int j, int s, bool* loaded);
   Worker::MvEntry* acquire_moments(Worker& w, HostJob& hj, int layer, long bytes);
+  bool claim_moments(Worker& w, HostJob& hj);
   void release_moments(Worker& w, bool keep);
   void write_back(Worker& w, Worker::PoolEntry& e);
   void collect(int pass, ExecResult& res);
@@ -888,32 +889,46 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
 // The pool belongs to one job at a time; ownership passes to the next job only once the owner
 // has no task left on this GPU in this pass (SHARP runs a GPU's jobs one after another), so
 // entries are never thrashed between interleaved jobs.
-Worker::MvEntry* ExecutorImpl::acquire_moments(Worker& w, HostJob& hj, int layer, long bytes) {
-  if (!w.mvpool || !hj.write_back) return nullptr;
-  if (w.mv_owner != hj.job) {
-    if (w.mv_owner >= 0) {
-      // the owner still has tasks ahead of it on this GPU in this pass: stream instead
-      auto it = w.last_local_of_job.find(w.mv_owner);
-      if (!exec.dynamic && w.mv_owner_pass == w.cur_pass && it != w.last_local_of_job.end() &&
-          it->second > w.cur_local) {
-        return nullptr;
-      }
-      release_moments(w, false);
-    }
-    w.mv_owner = hj.job;
+bool ExecutorImpl::claim_moments(Worker& w, HostJob& hj) {
+  if (!w.mvpool || !hj.write_back) return false;
+  if (w.mv_owner == hj.job) {
+    w.mv_owner_pass = w.cur_pass;
+    return true;
   }
+  if (w.mv_owner >= 0) {
+    // the owner still has tasks ahead of it on this GPU in this pass: stream instead
+    auto it = w.last_local_of_job.find(w.mv_owner);
+    if (!exec.dynamic && w.mv_owner_pass == w.cur_pass && it != w.last_local_of_job.end() &&
+        it->second > w.cur_local) {
+      return false;
+    }
+    release_moments(w, false);
+  }
+  w.mv_owner = hj.job;
   w.mv_owner_pass = w.cur_pass;
+  // Layout in forward order: the layers the next forward needs first (embedding, then the
+  // first blocks) get resident moments, the head-side layers the backward releases first —
+  // so their streamed update has the whole backward to finish — take what does not fit.
+  const size_t es = exec.opt_state_bf16 ? 2 : 4;
+  for (int l = 0; l < hj.m.L + 2; ++l) {
+    if (hj.host_layer[static_cast<size_t>(l)]) continue;
+    const long half = (static_cast<long>(es) * hy_layer_floats(&hj.m, l) + 511) / 512 * 512;
+    if (w.mvpool_used + 2 * half > w.mvpool_bytes) continue;  // a smaller later layer may fit
+    auto e = std::make_unique<Worker::MvEntry>();
+    e->layer = l;
+    e->off = w.mvpool_used;
+    e->bytes = 2 * half;
+    w.mvpool_used += 2 * half;
+    w.mv_live[l] = std::move(e);
+  }
+  return true;
+}
+
+Worker::MvEntry* ExecutorImpl::acquire_moments(Worker& w, HostJob& hj, int layer, long bytes) {
+  if (!claim_moments(w, hj)) return nullptr;
   auto it = w.mv_live.find(layer);
-  if (it != w.mv_live.end()) return it->second.get();
-  if (w.mvpool_used + bytes > w.mvpool_bytes) return nullptr;
-  auto e = std::make_unique<Worker::MvEntry>();
-  e->layer = layer;
-  e->off = w.mvpool_used;
-  e->bytes = bytes;
-  w.mvpool_used += bytes;
-  Worker::MvEntry* r = e.get();
-  w.mv_live[layer] = std::move(e);
-  return r;
+  if (it == w.mv_live.end() || it->second->bytes < bytes) return nullptr;
+  return it->second.get();
 }
 
 // Write the owner's updated moments back to its host state (up stream). keep = true (end of
@@ -1072,8 +1087,11 @@ struct StreamingSink : hy::GradSink {
 
   // GPU-placed embedding with its optimizer split around the scatter (not with the staging
   // aliased onto the scratch, where every update waits for the end of the backward)
+  // (not when the embedding's moments are HBM-resident: one in-place update after the
+  // scatter is then cheaper than the split's staged passes)
   bool split_embed() const {
-    return !hj.host_layer[0] && w.rowidx && tokens && !w.stg_alias && g_debug_skip != 2;
+    if (hj.host_layer[0] || !w.rowidx || !tokens || w.stg_alias || g_debug_skip == 2) return false;
+    return !(ex.claim_moments(w, hj) && w.mv_live.count(0));
   }
 
   // With the Adam staging aliased onto the backward's scratch (tiny HBM caps), layers are

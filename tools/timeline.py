@@ -16,7 +16,10 @@ import paper_2110_08633_b200 as P  # noqa: E402
 cfg = json.load(open(sys.argv[1]))
 extra = json.loads(sys.argv[2]) if len(sys.argv) > 2 else {}
 n_print = int(sys.argv[3]) if len(sys.argv) > 3 else 24
-ex = P.Executor(cfg, gpus=1, passes=1, warmup_passes=1, **extra)
+G = int(extra.pop("gpus", 1))  # a share of a G-GPU plan: '{"gpus": 8, "run_devices": [0]}'
+if G > 1:
+    extra.setdefault("device_ids", [0] * G)
+ex = P.Executor(cfg, gpus=G, passes=1, warmup_passes=1, **extra)
 ex.run(1, timed=False)
 r = ex.run(1, trace=True)
 tr = json.loads(r["chrome_trace"])
