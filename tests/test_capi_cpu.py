@@ -89,3 +89,17 @@ def test_host_adam_matches_oracle(bf16):
     np.testing.assert_allclose(as_f(mh), mo, rtol=1e-2 if bf16 else 2e-6, atol=1e-9)
     np.testing.assert_allclose(as_f(vh), vo, rtol=1e-2 if bf16 else 2e-6, atol=1e-12)
     assert P.lib().hy_host_adam(-1, 0, 0, 0, 0, 1e-3, 0.9, 0.999, 1e-8, 0.0, 1, 0, 1) == -1
+
+
+@pytest.mark.parametrize("field,value,msg", [("schedule", "eager", "schedule must be"),
+                                             ("precision", "fp16", "precision must be"),
+                                             ("opt_state", "fp8", "opt_state must be"),
+                                             ("host_opt_fraction", 1.5, "host_opt_fraction")])
+def test_execute_request_validation_without_gpu(field, value, msg):
+    """Execution-request fields are validated before any device work, so a bad request fails
+    with InvalidArgument (HY_E_INVALID, -1) and the reason even on a host without a GPU."""
+    with open(os.path.join(ROOT, "configs", "c1_tiny.json")) as f:
+        cfg = json.load(f)
+    with pytest.raises(P.HydraError) as e:
+        P.execute(cfg, **{field: value})
+    assert e.value.code == -1 and msg in str(e.value), (e.value.code, str(e.value))
