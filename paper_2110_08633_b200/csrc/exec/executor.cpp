@@ -315,6 +315,10 @@ struct ExecutorImpl {
   Worker::PoolEntry* acquire_params(Worker& w, HostJob& hj, int j, int s, bool* loaded);
   Worker::MvEntry* acquire_moments(Worker& w, HostJob& hj, int layer, long bytes);
   bool claim_moments(Worker& w, HostJob& hj);
+  bool same_moment_layout(const HostJob& a, const HostJob& b) const {
+    return a.m.L == b.m.L && a.m.d == b.m.d && a.m.V == b.m.V && a.host_layer == b.host_layer;
+  }
+  void flush_moments(Worker& w);
   void release_moments(Worker& w, bool keep);
   void write_back(Worker& w, Worker::PoolEntry& e);
   void collect(int pass, ExecResult& res);
@@ -902,6 +906,15 @@ bool ExecutorImpl::claim_moments(Worker& w, HostJob& hj) {
         it->second > w.cur_local) {
       return false;
     }
+    if (same_moment_layout(jobs.at(w.mv_owner), hj)) {
+      // Same model shape: keep the entries, write the old owner's moments back in the order the
+      // new owner's backward will reload them (head side first), each entry tracked on its own —
+      // the new owner's first load of a layer waits only for that layer's write-back.
+      flush_moments(w);
+      w.mv_owner = hj.job;
+      w.mv_owner_pass = w.cur_pass;
+      return true;
+    }
     release_moments(w, false);
   }
   w.mv_owner = hj.job;
@@ -929,6 +942,38 @@ Worker::MvEntry* ExecutorImpl::acquire_moments(Worker& w, HostJob& hj, int layer
   auto it = w.mv_live.find(layer);
   if (it == w.mv_live.end() || it->second->bytes < bytes) return nullptr;
   return it->second.get();
+}
+
+// Old owner's dirty moments -> host (up stream), head-side layers first; every entry stays in
+// place, invalid, for the next owner (same layout), ordered per entry by its tracker.
+void ExecutorImpl::flush_moments(Worker& w) {
+  HostJob& hj = jobs.at(w.mv_owner);
+  const size_t es = exec.opt_state_bf16 ? 2 : 4;
+  char* hm = reinterpret_cast<char*>(hj.mom);
+  char* hv = reinterpret_cast<char*>(hj.var);
+  for (auto it = w.mv_live.rbegin(); it != w.mv_live.rend(); ++it) {
+    Worker::MvEntry& e = *it->second;
+    e.tr.before_read(w.up);
+    if (e.valid && e.dirty) {
+      int s = 0;
+      while (s + 1 < static_cast<int>(hj.geom.size()) && hj.geom[static_cast<size_t>(s) + 1].l0 <= e.layer) ++s;
+      Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
+      const long nfl = hy_layer_floats(&hj.m, e.layer);
+      const size_t sbytes = es * static_cast<size_t>(nfl);
+      const size_t hoff = es * static_cast<size_t>(hy_layer_offset(&hj.m, e.layer));
+      mvt.before_write(w.up);
+      check_cuda(xfer(hm + hoff, w.mvpool + e.off, sbytes, cudaMemcpyDeviceToHost, w.up), "m write-back");
+      check_cuda(xfer(hv + hoff, w.mvpool + e.off + e.bytes / 2, sbytes, cudaMemcpyDeviceToHost, w.up),
+                 "v write-back");
+      mvt.after_write(w.up);
+      w.st.opt_d2h_bytes += 2.0 * sbytes;
+      w.st.d2h_bytes += 2.0 * sbytes;
+      w.st.mv_writeback_d2h_bytes += 2.0 * sbytes;
+    }
+    e.tr.after_read(w.up);
+    e.valid = false;
+    e.dirty = false;
+  }
 }
 
 // Write the owner's updated moments back to its host state (up stream). keep = true (end of
