@@ -226,3 +226,42 @@ def test_p2p_handoff_alternating_jobs(tmp_path):
     off = compare(cfg, off_dir, p2p=False, **kw)
     assert on["stats"]["p2p_bytes_per_pass"] > 0 and off["stats"]["p2p_bytes_per_pass"] == 0
     assert on["stats"]["act_h2d_bytes_per_pass"] < off["stats"]["act_h2d_bytes_per_pass"]
+
+
+def _mv_on_off(cfg, tmp_path, **kw):
+    runs = {}
+    for on in (False, True):
+        d = tmp_path / f"mv{int(on)}"
+        d.mkdir()
+        runs[on] = P.execute(cfg, params_out_dir=str(d), passes=2, mv_cache=on, opt_chunk_floats=65536,
+                             hbm_slack_bytes=80e6, **kw)
+    assert runs[True]["stats"]["mv_resident_updates_per_pass"] > 0
+    assert runs[False]["stats"]["mv_resident_updates_per_pass"] == 0
+    for j in range(len(cfg["jobs"])):
+        a, b = runs[False]["losses"][j], runs[True]["losses"][j]
+        assert np.allclose(a, b, rtol=1e-5, atol=0), (j, a, b)
+        pa = np.fromfile(tmp_path / "mv0" / f"job{j}.f32", dtype=np.float32)
+        pb = np.fromfile(tmp_path / "mv1" / f"job{j}.f32", dtype=np.float32)
+        assert np.linalg.norm(pa - pb) <= 1e-3 * np.linalg.norm(pa), j
+    return runs
+
+
+@pytest.mark.parametrize("kw", [dict(opt_state="bf16"), dict(host_opt_fraction=0.5)])
+def test_moment_cache_with_bf16_state_and_host_layers(tmp_path, kw):
+    """Moment cache combined with bf16 moments (2-byte entries) and with host-placed layers
+    (excluded from the layout): same results as streaming, 2 passes, 2 jobs (handover)."""
+    cfg = tiny_config(mbs=3)
+    _mv_on_off(cfg, tmp_path, **kw)
+
+
+def test_moment_cache_heterogeneous_jobs(tmp_path):
+    """Jobs of different model shapes on one GPU: the pool is re-laid out for each owner (no
+    in-place handover), results unchanged."""
+    cfg = tiny_config(mem=120e6, mbs=2, jobs=2)
+    big = json.loads(json.dumps(cfg["models"][0]))
+    big["name"] = "tiny_wide"
+    big["generator"].update(d_model=128, n_blocks=3)
+    cfg["models"].append(big)
+    cfg["jobs"].append(dict(cfg["jobs"][0], model="tiny_wide"))
+    cfg["jobs"].append(dict(cfg["jobs"][1]))
+    _mv_on_off(cfg, tmp_path)
