@@ -238,6 +238,7 @@ struct Worker {
     int layer = -1;
     long off = 0, bytes = 0;  // m at off, v at off + bytes / 2
     bool valid = false, dirty = false;
+    int job = -1;             // whose moments the entry holds while valid
     Tracked tr;
   };
   char* mvpool = nullptr;
@@ -249,6 +250,8 @@ struct Worker {
   cudaEvent_t mv_free = nullptr;             // up: previous owner's write-back done
   bool mv_free_pending = false;
   std::map<int, int> last_local_of_job;      // job -> its last local task index on this GPU
+  std::map<std::pair<int, int>, int> last_b_local;  // (job, shard) -> local index of its last backward
+  std::map<int, int> next_job;               // job -> the job this GPU runs after it (plan mode; -1 none)
   int cur_local = -1, cur_pass = -1;
   float* scratch = nullptr;
   double* loss_dev = nullptr;  // per task slot
@@ -318,7 +321,8 @@ struct ExecutorImpl {
   bool same_moment_layout(const HostJob& a, const HostJob& b) const {
     return a.m.L == b.m.L && a.m.d == b.m.d && a.m.V == b.m.V && a.host_layer == b.host_layer;
   }
-  void flush_moments(Worker& w);
+  void flush_moments(Worker& w, int new_owner);
+  void hand_over_moments(Worker& w, HostJob& hj, int layer, Worker::MvEntry& e);
   void release_moments(Worker& w, bool keep);
   void write_back(Worker& w, Worker::PoolEntry& e);
   void collect(int pass, ExecResult& res);
@@ -634,7 +638,19 @@ void ExecutorImpl::setup_worker(Worker& w) {
     w.mvpool_bytes = 4 * mv_f;
   }
   for (size_t i = 0; i < w.tasks.size(); ++i) {
-    w.last_local_of_job[tasks[static_cast<size_t>(w.tasks[i])].t.job] = static_cast<int>(i);
+    const ShardTask& st = tasks[static_cast<size_t>(w.tasks[i])].t;
+    w.last_local_of_job[st.job] = static_cast<int>(i);
+    if (st.direction == Direction::kBackward) w.last_b_local[{st.job, st.shard}] = static_cast<int>(i);
+  }
+  if (!exec.dynamic && !w.tasks.empty()) {
+    // the job that follows each job on this GPU; the last one is followed by the first of the
+    // next pass (the plan repeats)
+    std::vector<int> order;
+    for (int t : w.tasks) {
+      const int j = tasks[static_cast<size_t>(t)].t.job;
+      if (order.empty() || order.back() != j) order.push_back(j);
+    }
+    for (size_t i = 0; i < order.size(); ++i) w.next_job[order[i]] = order[(i + 1) % order.size()];
   }
   w.mv_free = new_event(false);
   check_cuda(cudaMemset(w.arena, 0, static_cast<size_t>(w.arena_bytes)), "arena memset");
@@ -807,6 +823,7 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
         check_cuda(xfer(dv, hv + hoff, sbytes, cudaMemcpyHostToDevice, w.optin), "v load");
         e->tr.after_write(w.optin);
         e->valid = true;
+        e->job = hj.job;
         w.st.opt_h2d_bytes += 2.0 * sbytes;
         w.st.h2d_bytes += 2.0 * sbytes;
         w.st.mv_load_h2d_bytes += 2.0 * sbytes;
@@ -826,6 +843,8 @@ void ExecutorImpl::adam_layer(Worker& w, HostJob& hj, int s, float* base, int la
       e->dirty = true;
       w.st.mv_resident_updates += static_cast<double>(nfl);
       if (done) check_cuda(cudaEventRecord(done, os), "adam done");
+      auto lb = w.last_b_local.find({hj.job, s});
+      if (!exec.dynamic && lb != w.last_b_local.end() && lb->second == w.cur_local) hand_over_moments(w, hj, layer, *e);
       return;
     }
   }
@@ -910,7 +929,7 @@ bool ExecutorImpl::claim_moments(Worker& w, HostJob& hj) {
       // Same model shape: keep the entries, write the old owner's moments back in the order the
       // new owner's backward will reload them (head side first), each entry tracked on its own —
       // the new owner's first load of a layer waits only for that layer's write-back.
-      flush_moments(w);
+      flush_moments(w, hj.job);
       w.mv_owner = hj.job;
       w.mv_owner_pass = w.cur_pass;
       return true;
@@ -941,20 +960,75 @@ Worker::MvEntry* ExecutorImpl::acquire_moments(Worker& w, HostJob& hj, int layer
   if (!claim_moments(w, hj)) return nullptr;
   auto it = w.mv_live.find(layer);
   if (it == w.mv_live.end() || it->second->bytes < bytes) return nullptr;
+  if (it->second->job != hj.job) it->second->valid = false;  // holds another job's moments
   return it->second.get();
+}
+
+// Proactive handover: the owner's last update of `layer` in this pass is done, so its moments go
+// back to the host right away (up) and, when the job that follows on this GPU has the same
+// shape, that job's moments for the layer come in behind them (optin) — spread over the owner's
+// last backward instead of piling up when the next job first needs them. The last job of a pass
+// hands over to the first job of the next pass.
+void ExecutorImpl::hand_over_moments(Worker& w, HostJob& hj, int layer, Worker::MvEntry& e) {
+  auto nx = w.next_job.find(hj.job);
+  if (nx == w.next_job.end() || nx->second == hj.job) return;
+  HostJob& nj = jobs.at(nx->second);
+  if (!nj.write_back || !same_moment_layout(hj, nj)) return;
+  const size_t es = exec.opt_state_bf16 ? 2 : 4;
+  const long nfl = hy_layer_floats(&hj.m, layer);
+  const size_t sbytes = es * static_cast<size_t>(nfl);
+  const size_t hoff = es * static_cast<size_t>(hy_layer_offset(&hj.m, layer));
+  const long half = e.bytes / 2;
+  auto shard_of = [&](const HostJob& x) {
+    int s = 0;
+    while (s + 1 < static_cast<int>(x.geom.size()) && x.geom[static_cast<size_t>(s) + 1].l0 <= layer) ++s;
+    return s;
+  };
+  // write the owner's final moments back
+  Tracked& mo = *hj.mv_tr[static_cast<size_t>(shard_of(hj))];
+  e.tr.before_read(w.up);
+  mo.before_write(w.up);
+  check_cuda(xfer(reinterpret_cast<char*>(hj.mom) + hoff, w.mvpool + e.off, sbytes, cudaMemcpyDeviceToHost, w.up),
+             "m hand-over write-back");
+  check_cuda(xfer(reinterpret_cast<char*>(hj.var) + hoff, w.mvpool + e.off + half, sbytes, cudaMemcpyDeviceToHost,
+                  w.up),
+             "v hand-over write-back");
+  mo.after_write(w.up);
+  e.tr.after_read(w.up);
+  w.st.opt_d2h_bytes += 2.0 * sbytes;
+  w.st.d2h_bytes += 2.0 * sbytes;
+  w.st.mv_writeback_d2h_bytes += 2.0 * sbytes;
+  // ... and the next job's in behind them
+  Tracked& mn = *nj.mv_tr[static_cast<size_t>(shard_of(nj))];
+  e.tr.before_write(w.optin);
+  mn.before_read(w.optin);
+  check_cuda(xfer(w.mvpool + e.off, reinterpret_cast<char*>(nj.mom) + hoff, sbytes, cudaMemcpyHostToDevice, w.optin),
+             "m hand-over load");
+  check_cuda(xfer(w.mvpool + e.off + half, reinterpret_cast<char*>(nj.var) + hoff, sbytes, cudaMemcpyHostToDevice,
+                  w.optin),
+             "v hand-over load");
+  mn.after_read(w.optin);
+  e.tr.after_write(w.optin);
+  w.st.opt_h2d_bytes += 2.0 * sbytes;
+  w.st.h2d_bytes += 2.0 * sbytes;
+  w.st.mv_load_h2d_bytes += 2.0 * sbytes;
+  e.valid = true;
+  e.dirty = false;
+  e.job = nj.job;
 }
 
 // Old owner's dirty moments -> host (up stream), head-side layers first; every entry stays in
 // place, invalid, for the next owner (same layout), ordered per entry by its tracker.
-void ExecutorImpl::flush_moments(Worker& w) {
+void ExecutorImpl::flush_moments(Worker& w, int new_owner) {
   HostJob& hj = jobs.at(w.mv_owner);
   const size_t es = exec.opt_state_bf16 ? 2 : 4;
   char* hm = reinterpret_cast<char*>(hj.mom);
   char* hv = reinterpret_cast<char*>(hj.var);
   for (auto it = w.mv_live.rbegin(); it != w.mv_live.rend(); ++it) {
     Worker::MvEntry& e = *it->second;
+    if (e.valid && e.job == new_owner) continue;  // already handed over (proactive handover)
     e.tr.before_read(w.up);
-    if (e.valid && e.dirty) {
+    if (e.valid && e.dirty && e.job == w.mv_owner) {
       int s = 0;
       while (s + 1 < static_cast<int>(hj.geom.size()) && hj.geom[static_cast<size_t>(s) + 1].l0 <= e.layer) ++s;
       Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
@@ -988,7 +1062,7 @@ void ExecutorImpl::release_moments(Worker& w, bool keep) {
   for (auto& kv : w.mv_live) {
     Worker::MvEntry& e = *kv.second;
     e.tr.before_read(w.up);
-    if (e.dirty) {
+    if (e.dirty && e.job == w.mv_owner) {
       int s = 0;
       while (s + 1 < static_cast<int>(hj.geom.size()) && hj.geom[static_cast<size_t>(s) + 1].l0 <= e.layer) ++s;
       Tracked& mvt = *hj.mv_tr[static_cast<size_t>(s)];
