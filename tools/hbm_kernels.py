@@ -1,0 +1,29 @@
+"""HBM-bound kernels of the shard task at the C2 (4096 x 768) and C3 (8192 x 1600) shapes, one
+launch each after warm-up — the ncu target for achieved-HBM-GB/s evidence:
+  ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \\
+      -k regex:"ln_|colsum|adam|xent" python tools/hbm_kernels.py"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2110_08633_b200 import kernels as K
+dev = torch.device("cuda")
+for rows, d in ((4096, 768), (8192, 1600)):
+    x = torch.randn(rows, d, device=dev)
+    g = torch.randn(d, device=dev)
+    b = torch.randn(d, device=dev)
+    dy = torch.randn(rows, d, device=dev)
+    dx = torch.zeros(rows, d, device=dev)
+    dyf = torch.randn(rows, 4 * d, device=dev)
+    n = 12 * d * d  # one block's parameters
+    p, gr, m, v = (torch.randn(n, device=dev) for _ in range(4))
+    v.abs_()
+    for it in range(2):  # second round is the one profiled (--launch-skip per kernel)
+        y, mean, rstd = K.layernorm_fwd(x, g, b)
+        K.layernorm_bwd(x, g, mean, rstd, dy, dx=dx, accumulate=True)
+        K.bias_grad(dyf)
+        K.adam(p, gr, m, v, 1e-4, it + 1)
+logits = torch.randn(500, 50304, device=dev)
+tgt = torch.randint(0, 50257, (500,), device=dev, dtype=torch.int32)
+for _ in range(2):
+    K.softmax_xent(logits, tgt, 50257, 1.0 / 500)
+torch.cuda.synchronize()
