@@ -715,9 +715,10 @@ void ExecutorImpl::setup(ExecResult& res) {
       if (dev < 0) dev = task_device[t];
       one = one && task_device[t] == dev;
     }
-    // dynamic mode: the scheduler keeps a job on one GPU within a pass (double buffering);
-    // every cache is written back and released at the end of each pass
-    kv.second.write_back = (one || exec.dynamic) && !exec.write_through;
+    // dynamic mode: with double buffering the scheduler keeps a job on one GPU within a pass
+    // (its prefetch is always the running job's successor), and every cache is written back and
+    // released at the end of each pass; without it jobs migrate, so they are write-through
+    kv.second.write_back = (one || (exec.dynamic && options.double_buffering)) && !exec.write_through;
   }
   for (auto& w : workers) setup_worker(*w);
   // NVLink peer access between the GPUs of this process (P2P hand-off)

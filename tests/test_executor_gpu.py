@@ -265,3 +265,14 @@ def test_moment_cache_heterogeneous_jobs(tmp_path):
     cfg["jobs"].append(dict(cfg["jobs"][0], model="tiny_wide"))
     cfg["jobs"].append(dict(cfg["jobs"][1]))
     _mv_on_off(cfg, tmp_path)
+
+
+def test_dynamic_schedule_alternating_with_p2p(tmp_path):
+    """Dynamic-time scheduling with double buffering off: the live scheduler moves jobs between
+    the two workers, boundary tensors are handed over device to device; results match the
+    oracle."""
+    cfg = tiny_config(mbs=3, jobs=3)
+    res = compare(cfg, tmp_path, schedule="dynamic", gpus=2, device_ids=[0, 0], double_buffering=False,
+                  precision="fp32", loss_tol=1e-5, param_tol=1e-4)
+    n_tasks = len(P.plan(cfg, gpus=2, double_buffering=False)["tasks"])
+    assert sorted(t for t, _, _ in res["dispatch_measured"]) == list(range(n_tasks))
