@@ -173,25 +173,29 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
     float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
     if (x0.bias) bv = *reinterpret_cast<const float4*>(x0.bias + col);
     const float* be = &bv.x;
-    // two groups of 4 rows; every operand of a group is loaded before any of its stores (the
-    // stores may alias later loads as far as the compiler knows, which would serialise them)
+    // rows in groups; every global operand of a group is in flight before its first use and
+    // loaded before any of the group's stores (which may alias later loads as far as the
+    // compiler knows, and would serialise them). GELU' reads the pre-activation for every
+    // element, so its 8 rows go out at once; the other modes keep groups of 4 (registers).
+    constexpr int kG = MODE == kEpiGeluBwd ? 8 : 4;
 #pragma unroll
-    for (int g = 0; g < 2; ++g) {
-      float4 xv[4], av[4], pv[4];
+    for (int g = 0; g < 8 / kG; ++g) {
+      float4 xv[kG], av[kG], pv[kG];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = (g * 4 + i) * 4 + x0.sub_r;
+      for (int i = 0; i < kG; ++i) {
+        const int r = (g * kG + i) * 4 + x0.sub_r;
         const bool ok = full_rows || r < x0.nrows;
         const long grow = x0.row0 + r;
-        xv[i] = lds128(x0.st_base + (r * 36 + x0.sub_c) * 4);
         av[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         pv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         if (x0.src && ok) av[i] = *reinterpret_cast<const float4*>(x0.src + grow * x0.lds + col);
         if (MODE == kEpiStore && x0.use_beta && ok) pv[i] = *reinterpret_cast<const float4*>(x0.Cb + grow * epi.ldc + col);
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = (g * 4 + i) * 4 + x0.sub_r;
+      for (int i = 0; i < kG; ++i) xv[i] = lds128(x0.st_base + (((g * kG + i) * 4 + x0.sub_r) * 36 + x0.sub_c) * 4);
+#pragma unroll
+      for (int i = 0; i < kG; ++i) {
+        const int r = (g * kG + i) * 4 + x0.sub_r;
         if (!full_rows && r >= x0.nrows) continue;
         const long grow = x0.row0 + r;
         float* xe = &xv[i].x;
