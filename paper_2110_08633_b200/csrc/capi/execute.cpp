@@ -114,6 +114,8 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   if (req.contains("device_ids")) ex.device_ids = req["device_ids"].get<std::vector<int>>();
   if (req.contains("run_devices")) ex.run_devices = req["run_devices"].get<std::vector<int>>();
   if (req.contains("opt_chunk_floats")) ex.opt_chunk_floats = req["opt_chunk_floats"].get<long>();
+  if (req.contains("splitk_max_floats")) ex.splitk_max_floats = req["splitk_max_floats"].get<long>();
+  ex.ring_first = req.value("ring_first", true);
   for (size_t j = 0; j < S->cfg.jobs.size(); ++j) {
     std::vector<int> starts{0};
     if (j < S->cs.partitionings.size()) starts = S->cs.partitionings[j].shard_starts;

@@ -28,6 +28,7 @@
 #include <condition_variable>
 #include <optional>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <list>
@@ -522,7 +523,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
   budget_floats -= ring_f;
   // split-K partials (<= 16 MB) from what the cap leaves, the Adam staging ring, then the
   // parameter cache beyond its two slots
-  long splitk_f = std::min(4L << 20, std::max(0L, budget_floats / 4)) / 1024 * 1024;
+  long splitk_f = std::min(exec.splitk_max_floats, std::max(0L, budget_floats / 4)) / 1024 * 1024;
   if (splitk_f < (256L << 10)) splitk_f = 0;
   budget_floats -= splitk_f;
   long chunk = std::min(exec.opt_chunk_floats, budget_floats / (2 * kStaging));
@@ -554,13 +555,17 @@ void ExecutorImpl::setup_worker(Worker& w) {
     pool_f += ext;
     budget_floats -= ext;
   }
-  // spare budget deepens the gradient ring (up to 4 layers)
-  if (budget_floats > 0) {
-    const long deep = std::min(budget_floats, 2 * hy_pad32(layer_f)) / 32 * 32;
-    ring_f += deep;
-    budget_floats -= deep;
-  }
-  // ... and what is still left keeps optimizer moments resident (write-back jobs only)
+  // Spare budget: a deeper gradient ring (up to 4 layers) and optimizer moments kept resident
+  // (write-back jobs only). Resident moments save their link bytes every minibatch, so they
+  // come first when the budget is tight (exec.ring_first = false); the ring takes the rest.
+  auto deepen_ring = [&]() {
+    if (budget_floats > 0) {
+      const long deep = std::min(budget_floats, 2 * hy_pad32(layer_f)) / 32 * 32;
+      ring_f += deep;
+      budget_floats -= deep;
+    }
+  };
+  if (exec.ring_first) deepen_ring();
   long mv_f = 0;
   if (exec.mv_cache && all_write_back && !w.stg_alias && budget_floats > (2L << 20)) {
     long job_mv_f = 0;  // the largest job's moments: what the cache can usefully hold
@@ -573,6 +578,16 @@ void ExecutorImpl::setup_worker(Worker& w) {
     if (exec.mv_cache_max_bytes >= 0) mv_f = std::min(mv_f, static_cast<long>(exec.mv_cache_max_bytes / 4));
     mv_f = mv_f / 256 * 256;
     budget_floats -= mv_f;
+  }
+  if (!exec.ring_first) deepen_ring();
+  if (std::getenv("HY_DEBUG_ARENA")) {  // diagnostics: where the capped HBM goes (MB)
+    std::fprintf(stderr,
+                 "arena dev %d: slots %.1f embed %.1f act %.1f scratch %.1f crow %.1f | ring %.1f splitk %.1f "
+                 "staging %.1f pool+ %.1f mv %.1f | left %.1f\n",
+                 w.plan_dev, 8.0 * hy_pad32(slot_f) / 1e6, 4.0 * hy_pad32(embed_f) / 1e6, 20.0 * hy_pad32(act_f) / 1e6,
+                 4.0 * hy_pad32(scratch_f) / 1e6, 4.0 * (all_write_back ? 2 : 3) * crow / 1e6, 4.0 * ring_f / 1e6,
+                 4.0 * splitk_f / 1e6, 4.0 * kStaging * 2 * hy_pad32(chunk) / 1e6,
+                 4.0 * (pool_f - 2 * hy_pad32(slot_f)) / 1e6, 4.0 * mv_f / 1e6, 4.0 * budget_floats / 1e6);
   }
   const long floats = base_floats + ring_f + splitk_f + kStaging * 2 * hy_pad32(chunk) + (pool_f - 2 * hy_pad32(slot_f)) +
                       mv_f;
