@@ -551,7 +551,9 @@ void ExecutorImpl::setup_worker(Worker& w) {
   // — physical traffic only, the plan is unchanged.
   long pool_f = 2 * hy_pad32(slot_f);
   if (budget_floats > 0 && model_f > pool_f) {
-    const long ext = std::min(budget_floats, model_f - pool_f) / 32 * 32;
+    long ext = std::min(budget_floats, model_f - pool_f);
+    if (exec.pool_extra_max_bytes >= 0) ext = std::min(ext, static_cast<long>(exec.pool_extra_max_bytes / 4));
+    ext = ext / 32 * 32;
     pool_f += ext;
     budget_floats -= ext;
   }
