@@ -260,7 +260,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
 template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uint32_t q, uint32_t tmem_base,
                                                 float* epi_smem, const GemmEpilogue& epi, const GemmBatch& bat,
-                                                int M, int N) {
+                                                int M, int N, int c_begin = 0, int c_end = BN / 32) {
   static_assert((BN / 32) % 2 == 0, "chunk pairs");
   EpiCtx x;
   x.lane = lane_id();
@@ -278,21 +278,21 @@ __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uin
   const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
   uint32_t b0[32], b1[32];
   if (ti.nkb > 0) {
-    tmem_ld_x32_issue(tbase, b0);
+    tmem_ld_x32_issue(tbase + c_begin * 32, b0);
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; c += 2) {
+    for (int c = c_begin; c < c_end; c += 2) {  // c_end - c_begin even
       tmem_ld_wait();
       tmem_ld_x32_issue(tbase + (c + 1) * 32, b1);
       epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
       tmem_ld_wait();
-      if (c + 2 < BN / 32) tmem_ld_x32_issue(tbase + (c + 2) * 32, b0);
+      if (c + 2 < c_end) tmem_ld_x32_issue(tbase + (c + 2) * 32, b0);
       epilogue_chunk<MODE>(x, b1, ti.n0 + (c + 1) * 32, epi, N);
     }
   } else {
 #pragma unroll
     for (int i = 0; i < 32; ++i) b0[i] = 0u;
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
+    for (int c = c_begin; c < c_end; ++c) epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
   }
 }
 
@@ -529,6 +529,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
   using L = SmemPair<BN>;
   constexpr int kStages = L::kStagesN;
   constexpr int BM2 = 2 * BM;
+  constexpr int kHalfChunks = (BN / 64) * 2 == BN / 32 ? BN / 64 + ((BN / 64) & 1) : BN / 64;  // even split point
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_smem = reinterpret_cast<float*>(smem + L::kRing);
@@ -536,7 +537,8 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* lastbar = tempty + 2;  // the CTA's last accumulator is ready (epilogue warps -> warps 0-3)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lastbar + 1);
 
   const uint32_t warp = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -558,6 +560,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
     }
+    mbar_init(lastbar, 4);
     fence_barrier_init();
   }
   constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
@@ -668,7 +671,14 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       ++local;
       tc_fence_after();
-      epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N);
+      // the CTA's last tile: warps 0-3 (done with loading / issuing) take the second half of
+      // its columns, so the one epilogue nothing overlaps runs on twice the warps
+      const bool last = tile + n_pairs >= n_tiles;
+      if (last) {  // (tfull phases are tracked here; warps 0-3 only learn of the last one)
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(lastbar);
+      }
+      epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N, 0, last ? kHalfChunks : BN / 32);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) {
@@ -676,6 +686,21 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
         else mbar_arrive_cluster(&tempty[acc], 0);
       }
     }
+  }
+
+  if (warp < 4 && pair < n_tiles) {
+    __syncwarp();
+    const int cnt = (n_tiles - 1 - pair) / n_pairs + 1;  // tiles of this CTA
+    const int tile = pair + (cnt - 1) * n_pairs;
+    TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+    ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
+    const int acc = (cnt - 1) & 1;
+    // not tfull itself: an early parity test on it could pass for an earlier phase
+    mbar_wait(lastbar, 0);
+    tc_fence_after();
+    // the pipeline ring is idle now (every TMA landed, every MMA read it): per-warp transposes
+    epilogue_tile_m<BN, MODE>(ti, acc, warp, tmem_base, reinterpret_cast<float*>(smem), epi, bat, M, N, kHalfChunks,
+                              BN / 32);
   }
 
   tc_fence_before();
