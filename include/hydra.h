@@ -21,6 +21,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "hydra_gpt.h"
+
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -133,6 +135,68 @@ int hy_adam_host_state(void* stream, long n, float* p, const float* g, void* m_h
  * (0: all cores). bf16_state != 0: m, v are bf16 bit patterns (uint16), rounded RNE. */
 int hy_host_adam(long n, float* p, const float* g, void* m, void* v, float lr, float beta1, float beta2, float eps,
                  float weight_decay, int step, int bf16_state, int threads);
+
+/* ---------------------------------------------------------------------------------
+ * Device level (SURVEY §8b minimum exports): what a host that runs its own engine loop needs
+ * — the reference's Engine::dispatch / try_compute / on_compute_done (sim.cpp:347-474) with
+ * real copies and kernels. The executor above is the packaged engine over the same pieces.
+ *   hy_open: a device context with an HBM arena capped at hbm_budget (DeviceSpec::mem_bytes,
+ *   model.hpp:62) — hy_arena_alloc fails with HY_E_CAPACITY beyond it — and three lanes:
+ *   DOWN (H2D: ParamLoad / ActPromote), UP (D2H: ActDemote / GradOffload), COMPUTE.
+ * --------------------------------------------------------------------------------- */
+typedef struct hy_dev hy_dev;
+enum { HY_LANE_DOWN = 0, HY_LANE_UP = 1, HY_LANE_COMPUTE = 2 };
+
+int hy_open(int device, size_t hbm_budget, hy_dev** dev);
+void hy_close(hy_dev* dev);
+int hy_lane_stream(hy_dev* dev, int lane, void** stream); /* cudaStream_t for the kernel entry points */
+int hy_arena_alloc(hy_dev* dev, size_t bytes, void** ptr); /* 1 KB aligned bump allocation */
+int hy_arena_reset(hy_dev* dev);
+int hy_arena_peak(hy_dev* dev, size_t* bytes);
+int hy_pinned_alloc(size_t bytes, void** ptr);             /* portable + mapped pinned host memory */
+int hy_pinned_free(void* ptr);
+int hy_copy_h2d(hy_dev* dev, void* dst, const void* src, size_t bytes);            /* DOWN lane */
+int hy_copy_d2h(hy_dev* dev, void* dst, const void* src, size_t bytes);            /* UP lane */
+int hy_copy_p2p(hy_dev* dev, void* dst, int src_device, const void* src, size_t bytes); /* DOWN, NVLink */
+int hy_event_record(hy_dev* dev, int lane, void** event);   /* creates and records a timing event */
+int hy_lane_wait(hy_dev* dev, int lane, void* event);
+int hy_event_query(void* event, int* done);
+int hy_event_elapsed(void* start, void* end, float* ms);
+int hy_event_destroy(void* event);
+int hy_lane_sync(hy_dev* dev, int lane);
+
+/* One ShardTask's compute (model.cpp:165-216 layers l0..l1-1 of the GPT in hydra_gpt.h) on the
+ * COMPUTE lane. params: the shard's layers, contiguous in the hydra_gpt.h layout. wte: the tied
+ * embedding when the shard has the head but not layer 0. Forward: act_in (l0 > 0) -> act_out
+ * (no head) or the loss. Backward (recompute + backward, strategies.cpp:743-782): grads (same
+ * layout as params, zeroed by the caller) +=, grad_in (no head) -> grad_out (l0 > 0); a head
+ * shard without the embedding leaves ln_f's output in z_out for the embedding shard's deferred
+ * tied-wte gradient, which that shard's backward takes as z_in. loss (host, nullable): mean
+ * token cross-entropy when the shard has the head. scratch: >= hy_shard_scratch_bytes. */
+typedef struct {
+  hy_dims dims;
+  int l0, l1;
+} hy_shard_desc;
+
+typedef struct {
+  const float* params;
+  const float* wte;
+  const int32_t* tokens;
+  const int32_t* targets;
+  const float* act_in;
+  float* act_out;
+  const float* grad_in;
+  float* grad_out;
+  const float* z_in;
+  float* z_out;
+  float* grads;
+  void* scratch;
+  size_t scratch_bytes;
+} hy_shard_bufs;
+
+int hy_shard_scratch_bytes(const hy_dims* dims, int max_blocks, size_t* bytes);
+int hy_shard_forward(hy_dev* dev, const hy_shard_desc* shard, const hy_shard_bufs* bufs, double* loss);
+int hy_shard_backward(hy_dev* dev, const hy_shard_desc* shard, const hy_shard_bufs* bufs, double* loss);
 
 #ifdef __cplusplus
 }

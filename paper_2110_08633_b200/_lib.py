@@ -50,7 +50,42 @@ _SIGS = {
     "hy_flash_attention_bwd": (ctypes.c_int, [ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p] * 6),
     "hy_host_adam": (ctypes.c_int, [ctypes.c_long] + [ctypes.c_void_p] * 4 + [ctypes.c_float] * 5
                      + [ctypes.c_int] * 3),
+    # device level (include/hydra.h "Device level")
+    "hy_open": (ctypes.c_int, [ctypes.c_int, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "hy_close": (None, [ctypes.c_void_p]),
+    "hy_lane_stream": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "hy_arena_alloc": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "hy_arena_reset": (ctypes.c_int, [ctypes.c_void_p]),
+    "hy_arena_peak": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_size_t)]),
+    "hy_pinned_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "hy_pinned_free": (ctypes.c_int, [ctypes.c_void_p]),
+    "hy_copy_h2d": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
+    "hy_copy_d2h": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t]),
+    "hy_copy_p2p": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t]),
+    "hy_event_record": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "hy_lane_wait": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]),
+    "hy_event_query": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int)]),
+    "hy_event_elapsed": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float)]),
+    "hy_event_destroy": (ctypes.c_int, [ctypes.c_void_p]),
+    "hy_lane_sync": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "hy_shard_scratch_bytes": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_size_t)]),
+    "hy_shard_forward": (ctypes.c_int, [ctypes.c_void_p] * 3 + [ctypes.POINTER(ctypes.c_double)]),
+    "hy_shard_backward": (ctypes.c_int, [ctypes.c_void_p] * 3 + [ctypes.POINTER(ctypes.c_double)]),
 }
+
+
+class Dims(ctypes.Structure):  # hy_dims (include/hydra_gpt.h)
+    _fields_ = [(n, ctypes.c_int) for n in ("V", "d", "L", "T", "B", "H")]
+
+
+class ShardDesc(ctypes.Structure):  # hy_shard_desc
+    _fields_ = [("dims", Dims), ("l0", ctypes.c_int), ("l1", ctypes.c_int)]
+
+
+class ShardBufs(ctypes.Structure):  # hy_shard_bufs
+    _fields_ = [(n, ctypes.c_void_p) for n in ("params", "wte", "tokens", "targets", "act_in", "act_out", "grad_in",
+                                               "grad_out", "z_in", "z_out", "grads", "scratch")] + [
+        ("scratch_bytes", ctypes.c_size_t)]
 
 EXPORTED = sorted(_SIGS)
 
