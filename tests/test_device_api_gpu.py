@@ -120,7 +120,7 @@ def test_shard_forward_backward_match_oracle(split):
             for layer in range(m.L + 2):
                 lo, hi = O.layer_offset(m, layer), O.layer_offset(m, layer + 1)
                 rel = np.linalg.norm(g[lo:hi] - g_ref[lo:hi]) / np.linalg.norm(g_ref[lo:hi])
-                assert rel < 1e-4, (layer, rel)
+                assert rel < 5e-4, (layer, rel)  # raw gradients: 3xTF32 vs fp64 accumulation
         else:
             cut = O.layer_offset(m, split + 1)  # layers [0, split+1) | [split+1, L+2)
             p0, p1 = d.put(params[:cut]), d.put(params[cut:])
