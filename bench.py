@@ -223,6 +223,40 @@ def live_gemm_roofline(torch, cfg):
             "launch_us": round(t * 1e6, 2)}
 
 
+def probe_link(torch, nbytes=1 << 29, reps=4):
+    """Pinned host<->HBM copy rates of this box (GB/s): each direction alone, then both at once on two
+    streams (the duplex rate a shard pass can use). Timed with CUDA events on the copying streams."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    hs = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    hd = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    ds = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    dd = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    s_dn, s_up = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(which):
+        torch.cuda.synchronize()
+        ev = {}
+        for name, s in (("h2d", s_dn), ("d2h", s_up)):
+            if name not in which:
+                continue
+            with torch.cuda.stream(s):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                for _ in range(reps):
+                    (ds.copy_(hs, non_blocking=True) if name == "h2d" else hd.copy_(dd, non_blocking=True))
+                b.record(s)
+                ev[name] = (a, b)
+        torch.cuda.synchronize()
+        return {k: round(nbytes * reps / (a.elapsed_time(b) * 1e-3) / 1e9, 2) for k, (a, b) in ev.items()}
+
+    timed(("h2d", "d2h"))  # warm
+    one = {**timed(("h2d",)), **timed(("d2h",))}
+    both = timed(("h2d", "d2h"))
+    return {"h2d_GBps": one["h2d"], "d2h_GBps": one["d2h"],
+            "duplex_h2d_GBps": both["h2d"], "duplex_d2h_GBps": both["d2h"],
+            "method": f"{reps} x {nbytes >> 20} MiB pinned copies per direction, CUDA events on the copy streams"}
+
+
 def shard_roofline(res, per_rank_time, link_GBps):
     """north_star roofline: sum over executed shard tasks of max(F/peak, H2D/BW, D2H/BW)."""
     return None
@@ -248,6 +282,8 @@ def run_hydra(args, cfg):
     req = dict(strategy="sharp", gpus=n, run_devices=[rank], device_ids=device_ids,
                passes=args.steps, warmup_passes=args.warmup, host_opt_fraction=args.host_opt_fraction,
                opt_state=args.opt_state)
+    if args.exec_json:  # executor tuning knobs (ExecOptions fields of the C-ABI request), e.g. '{"opt_chunk_floats": 4194304}'
+        req.update(json.loads(args.exec_json))
     if args.schedule == "dynamic":
         # one process drives every GPU (one worker thread each) so the live scheduler sees them all
         if world > 1:
@@ -327,9 +363,19 @@ def run_hydra(args, cfg):
         "measured_makespan_s": round(dev_time / args.steps, 5),
         "frac": round(virt / (dev_time / args.steps), 4),
         "link_GBps_assumed": link / 1e9,
-        "physical_h2d_GBps": round(h2d / (dev_time / args.steps) / 1e9, 2),
-        "physical_d2h_GBps": round(d2h / (dev_time / args.steps) / 1e9, 2),
+        "achieved_h2d_GBps": round(h2d / (dev_time / args.steps) / 1e9, 2),
+        "achieved_d2h_GBps": round(d2h / (dev_time / args.steps) / 1e9, 2),
     }
+    try:
+        lp = probe_link(torch)
+        # the same pass against this box's measured duplex link and the bytes actually moved
+        # (cost-model bytes + Adam m/v + tied wte + biases): how close the pass runs to the physical link
+        t_link = max(h2d / (lp["duplex_h2d_GBps"] * 1e9), d2h / (lp["duplex_d2h_GBps"] * 1e9))
+        out["shard_roofline"]["link_probe"] = lp
+        out["shard_roofline"]["actual_bytes_link_bound_s"] = round(t_link, 5)
+        out["shard_roofline"]["actual_bytes_link_frac"] = round(t_link / (dev_time / args.steps), 4)
+    except Exception as e:  # pragma: no cover
+        out["shard_roofline"]["link_probe"] = {"error": str(e)}
     try:
         out["roofline"] = live_gemm_roofline(torch, cfg)
     except Exception as e:  # pragma: no cover
@@ -427,6 +473,7 @@ def main():
     ap.add_argument("--schedule", default="plan", choices=["plan", "dynamic"],
                     help="plan: replay the reference engine's dispatch log (default); dynamic: the SHARP "
                          "scheduler driven live by measured completions, all GPUs in this one process")
+    ap.add_argument("--exec-json", default="", help="extra executor request fields (JSON object)")
     args = ap.parse_args()
     cfg = load_config(args.config)
     if args.impl == "reference":

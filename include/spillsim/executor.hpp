@@ -35,6 +35,7 @@ struct ExecOptions {
   long opt_chunk_floats = 2L << 20;  // Adam m/v streaming chunk (elements)
   long splitk_max_floats = 4L << 20;  // split-K partials workspace cap (elements)
   bool ring_first = true;             // spare HBM: deepen the gradient ring before the moment cache
+  bool opt_priority = false;          // optimizer streams at the device's highest stream priority
   double pool_extra_max_bytes = -1;   // cap on the parameter cache beyond its two slots (< 0: none)
   bool opt_state_bf16 = false;       // Adam moments stored/streamed as bf16 (halves their link bytes)
   std::string params_out_dir;      // if set: final params of every executed job as job<j>.f32

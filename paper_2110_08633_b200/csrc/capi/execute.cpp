@@ -116,6 +116,7 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   if (req.contains("opt_chunk_floats")) ex.opt_chunk_floats = req["opt_chunk_floats"].get<long>();
   if (req.contains("splitk_max_floats")) ex.splitk_max_floats = req["splitk_max_floats"].get<long>();
   ex.ring_first = req.value("ring_first", true);
+  ex.opt_priority = req.value("opt_priority", ex.opt_priority);
   ex.pool_extra_max_bytes = req.value("pool_extra_max_bytes", -1.0);
   for (size_t j = 0; j < S->cfg.jobs.size(); ++j) {
     std::vector<int> starts{0};

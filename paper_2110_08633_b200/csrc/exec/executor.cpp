@@ -479,9 +479,13 @@ void ExecutorImpl::setup_worker(Worker& w) {
   check_cuda(cudaStreamCreateWithFlags(&w.comp, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.down, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.up, cudaStreamNonBlocking), "stream");
-  check_cuda(cudaStreamCreateWithFlags(&w.opt, cudaStreamNonBlocking), "stream");
+  // the Adam kernels sit between an H2D and a D2H copy of each moment chunk: at high priority the
+  // block scheduler runs them ahead of queued compute blocks so the link pipeline does not drain
+  int prio_lo = 0, prio_hi = 0;
+  if (exec.opt_priority) check_cuda(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "priority range");
+  check_cuda(cudaStreamCreateWithPriority(&w.opt, cudaStreamNonBlocking, prio_hi), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.hopt, cudaStreamNonBlocking), "stream");
-  check_cuda(cudaStreamCreateWithFlags(&w.opt2, cudaStreamNonBlocking), "stream");
+  check_cuda(cudaStreamCreateWithPriority(&w.opt2, cudaStreamNonBlocking, prio_hi), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.optin, cudaStreamNonBlocking), "stream");
   // Size the arena from the tasks this GPU will run.
   bool all_write_back = true;
