@@ -1,5 +1,6 @@
 // Host entry of the tcgen05 TF32 GEMM: split-K planning and the per-mode dispatch. The
 // kernels live in gemm_kernels.cuh, instantiated per epilogue mode in gemm_m{0,1,2}.cu.
+#include <cstdlib>
 #include <cuda.h>
 
 #include <algorithm>
@@ -77,9 +78,16 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + 127) / 128);
   const int kb_all = (K + BK - 1) / BK;
   const bool plain = !batch && e.mode == kEpiStore && !e.bias && !e.R;
+  static const int forced_split = [] {  // diagnostics: HY_GEMM_SPLIT=S forces S-way split-K
+    const char* v = std::getenv("HY_GEMM_SPLIT");
+    return v ? std::atoi(v) : 0;
+  }();
   if (plain && t_splitk_ws && tiles * 2 <= sm_count_host() && kb_all >= 32) {
     split = static_cast<int>(std::min<long>(sm_count_host() / tiles, kb_all / 16));
     split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
+  }
+  if (forced_split >= 2 && plain && t_splitk_ws) {
+    split = static_cast<int>(std::min<long>(forced_split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
   if (split >= 2) {
     bat.nb1 = split;

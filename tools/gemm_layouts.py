@@ -12,6 +12,8 @@ from paper_2110_08633_b200 import kernels as K  # noqa: E402
 
 M, N, Kd = (int(x) for x in (sys.argv[1:4] if len(sys.argv) > 3 else (3072, 768, 4096)))
 dev = torch.device("cuda")
+ws = torch.empty(32 << 20, device=dev)  # split-K partials (used when the dispatcher splits)
+K.gemm_config(False, ws)
 out = {}
 for amn in (0, 1):
     for bmn in (0, 1):
