@@ -7,6 +7,7 @@
 
 #include "gemm.cuh"
 #include "launch_count.cuh"
+#include "pdl.cuh"
 
 namespace hy {
 cudaError_t gemm_dispatch_m0(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
@@ -25,17 +26,42 @@ thread_local float* t_splitk_ws = nullptr;
 thread_local bool t_prec3 = false;
 thread_local long t_splitk_floats = 0;
 
-// C = alpha * sum_s part[s] + beta * C   (fixed summation order: deterministic)
+// C = alpha * sum_s part[s] + beta * C   (fixed summation order: deterministic). Rows over
+// grid.y (grid-stride), columns over grid.x, float4 when N and ldc allow; PDL-chained behind the
+// split GEMM (griddepcontrol.wait before the partials are read).
+template <bool VEC>
 __global__ void splitk_reduce_kernel(int M, int N, int S, const float* __restrict__ part, float* __restrict__ C,
                                      long ldc, float alpha, float beta) {
+  pdl_wait_and_trigger();
   const long total = static_cast<long>(M) * N;
-  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<long>(gridDim.x) * blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < S; ++s) acc += part[s * total + i];
-    const long m = i / N, n = i % N;
-    float* c = C + m * ldc + n;
-    *c = alpha * acc + (beta != 0.f ? beta * *c : 0.f);
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) * (VEC ? 4 : 1);
+  if (n >= N) return;
+  for (int m = blockIdx.y; m < M; m += gridDim.y) {
+    const long i = static_cast<long>(m) * N + n;
+    float* c = C + static_cast<long>(m) * ldc + n;
+    if constexpr (VEC) {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < S; ++s) {
+        const float4 v = *reinterpret_cast<const float4*>(part + s * total + i);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      float4 o = make_float4(alpha * acc.x, alpha * acc.y, alpha * acc.z, alpha * acc.w);
+      if (beta != 0.f) {
+        const float4 p = *reinterpret_cast<const float4*>(c);
+        o.x += beta * p.x;
+        o.y += beta * p.y;
+        o.z += beta * p.z;
+        o.w += beta * p.w;
+      }
+      *reinterpret_cast<float4*>(c) = o;
+    } else {
+      float acc = 0.f;
+      for (int s = 0; s < S; ++s) acc += part[s * total + i];
+      *c = alpha * acc + (beta != 0.f ? beta * *c : 0.f);
+    }
   }
 }
 
@@ -86,6 +112,20 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
     split = static_cast<int>(std::min<long>(sm_count_host() / tiles, kb_all / 16));
     split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
+  // Long-K GEMMs whose 256-wide CTA-pair tiles cover under half the pairs (the weight gradients,
+  // K = tokens): split K so 256-wide tiles fill the GPU (BN 256 halves the operand traffic per
+  // flop of the 128-wide single wave; profiles/r01_ncu_gemm_dw_mn_major.txt).
+  static const bool split256 = [] {
+    const char* v = std::getenv("HY_GEMM_SPLIT256");
+    return !(v && v[0] == '0');
+  }();
+  const long tiles256 = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
+  const long pairs = sm_count_host() / 2;
+  if (split256 && split == 1 && plain && t_splitk_ws && !t_prec3 && M > BM && N > 128 && kb_all >= 64 &&
+      tiles256 * 2 <= pairs) {
+    split = static_cast<int>(std::min<long>(pairs / tiles256, kb_all / 32));
+    split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
+  }
   if (forced_split >= 2 && plain && t_splitk_ws) {
     split = static_cast<int>(std::min<long>(forced_split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
@@ -98,11 +138,15 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
     pe.ldc = N;
     const cudaError_t r = dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, pe, bat);
     if (r != cudaSuccess) return r;
-    const long total = static_cast<long>(M) * N;
-    const int grid = static_cast<int>(std::min<long>((total + 255) / 256, sm_count_host() * 8L));
+    const bool vec = (N % 4 == 0) && (e.ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(e.C) % 16 == 0);
+    const int cols = vec ? N / 4 : N;
+    const int gx = (cols + 255) / 256;
+    const int gy = static_cast<int>(std::min<long>(M, std::max<long>(1, sm_count_host() * 8L / gx)));
     count_launch();
-    splitk_reduce_kernel<<<grid, 256, 0, stream>>>(M, N, split, t_splitk_ws, e.C, e.ldc, e.alpha, e.beta);
-    return cudaGetLastError();
+    return vec ? launch_pdl(splitk_reduce_kernel<true>, dim3(gx, gy), dim3(256), 0, stream, M, N, split,
+                            static_cast<const float*>(t_splitk_ws), e.C, e.ldc, e.alpha, e.beta)
+               : launch_pdl(splitk_reduce_kernel<false>, dim3(gx, gy), dim3(256), 0, stream, M, N, split,
+                            static_cast<const float*>(t_splitk_ws), e.C, e.ldc, e.alpha, e.beta);
   }
   return dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
 }
