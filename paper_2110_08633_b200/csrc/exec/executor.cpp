@@ -525,7 +525,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
   // gradient ring: at least two of the largest non-embedding layers
   long ring_f = 2 * hy_pad32(layer_f) + 64;
   budget_floats -= ring_f;
-  // split-K partials (<= 16 MB) from what the cap leaves, the Adam staging ring, then the
+  // split-K partials (<= splitk_max_floats) from what the cap leaves, the Adam staging ring, then the
   // parameter cache beyond its two slots
   long splitk_f = std::min(exec.splitk_max_floats, std::max(0L, budget_floats / 4)) / 1024 * 1024;
   if (splitk_f < (256L << 10)) splitk_f = 0;
