@@ -257,11 +257,6 @@ def probe_link(torch, nbytes=1 << 29, reps=4):
             "method": f"{reps} x {nbytes >> 20} MiB pinned copies per direction, CUDA events on the copy streams"}
 
 
-def shard_roofline(res, per_rank_time, link_GBps):
-    """north_star roofline: sum over executed shard tasks of max(F/peak, H2D/BW, D2H/BW)."""
-    return None
-
-
 def run_hydra(args, cfg):
     import torch
     import paper_2110_08633_b200 as P

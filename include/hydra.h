@@ -69,7 +69,10 @@ int hy_execute_json(const char* request_json, char* out, size_t out_len, size_t*
  * request_json as for hy_execute_json ("passes" + "warmup_passes" bound the total). */
 int hy_executor_create(const char* request_json, void** handle);
 /* Replays the plan `passes` times; timed passes are measured with CUDA events and
- * accumulate into the result JSON (pass_seconds, losses, byte counters, report). */
+ * accumulate into the result JSON (pass_seconds, losses, byte counters, report).
+ * timed: 0 untimed, 1 timed, 2 timed + interval log (result "links": copy-only link time
+ * per direction, compute-op time and the transfer-overlap fraction per GPU; adds two event
+ * records per op / copy, so throughput is measured on passes run with timed = 1). */
 int hy_executor_run(void* handle, int passes, int timed, int with_trace, char* out, size_t out_len,
                     size_t* needed);
 int hy_executor_dump_params(void* handle, const char* dir);

@@ -93,6 +93,19 @@ struct ExecStats {
   double setup_s = 0;
 };
 
+// Copy-only link intervals of one GPU's last logged pass (Executor::run interval_log).
+// overlap = 1 - exposed / link_busy: the share of link time hidden under shard compute.
+struct LinkStats {
+  int plan_device = -1;
+  double pass_s = 0;
+  double h2d_busy_s = 0, d2h_busy_s = 0;  // union of copy intervals per direction
+  double link_busy_s = 0;                 // union over both directions
+  double compute_busy_s = 0;              // union of compute-stream op intervals
+  double exposed_s = 0;                   // link busy while no compute op runs
+  double h2d_bytes = 0, d2h_bytes = 0;    // bytes of the logged copies
+  long copies = 0, ops = 0;
+};
+
 struct ExecResult {
   SimTrace trace;                              // measured, last timed pass
   std::vector<std::vector<double>> losses;     // [job][global minibatch] (executed jobs)
@@ -100,6 +113,7 @@ struct ExecResult {
   std::map<std::string, double> op_profile_ms; // HY_PROFILE=1: compute-stream time per op (last pass)
   ExecStats stats;
   std::vector<Dispatch> dispatch_log;          // dynamic mode: the measured dispatch order (last pass)
+  std::vector<LinkStats> links;                // interval-logged pass: per executed GPU
 };
 
 struct ExecutorImpl;
@@ -117,7 +131,10 @@ class Executor {
 
   /// Replays the plan `passes` times. Timed passes append to result(): pass_seconds (CUDA
   /// events on each GPU, max over this process's GPUs), losses, byte counters, trace.
-  void run(int passes, bool timed);
+  /// interval_log: also record every compute op and host<->device copy of the (timed) passes
+  /// (result().links: copy-only link time and the transfer-overlap fraction); it adds two
+  /// event records per op / copy, so measure throughput on passes without it.
+  void run(int passes, bool timed, bool interval_log = false);
   ExecResult& result() { return res_; }
   void dump_params(const std::string& dir) const;
 

@@ -41,20 +41,7 @@ std::string report_to_json(const RunReport& report);
 std::string report_to_csv(const RunReport& report);
 std::string report_to_text(const RunReport& report);
 
-struct ComparisonRow {
-  std::string strategy;
-  double makespan_s = 0;
-  double speedup_vs_baseline = 0;
-  double cost_ratio = 0;
-  double energy_ratio = 0;
-  bool feasible = true;
-};
-
-struct ComparisonTable {
-  std::string baseline;
-  std::vector<ComparisonRow> rows;
-};
-
-ComparisonTable compare(const std::vector<RunReport>& reports, const std::string& baseline);
+// (The reference's compare() / ComparisonTable build its paper tables and are out of scope
+// here.)
 
 }  // namespace spillsim

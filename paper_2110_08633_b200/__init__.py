@@ -36,7 +36,10 @@ class Executor:
         check(lib().hy_executor_create(_json.dumps(req).encode(), ctypes.byref(h)))
         self._h = h
 
-    def run(self, passes: int, timed: bool = True, trace: bool = False) -> dict:
+    def run(self, passes: int, timed: bool = True, trace: bool = False, interval_log: bool = False) -> dict:
+        """Replay the plan `passes` times (hy_executor_run). interval_log: timed passes also log
+        every compute op and host<->device copy (result "links": copy-only link time and the
+        transfer-overlap fraction per GPU) — measure throughput on passes without it."""
         import ctypes
         import json as _json
 
@@ -46,7 +49,8 @@ class Executor:
         needed = ctypes.c_size_t(0)
         while True:
             buf = ctypes.create_string_buffer(size)
-            rc = lib().hy_executor_run(self._h, int(passes), int(timed), int(trace), buf, size, ctypes.byref(needed))
+            mode = (2 if interval_log else 1) if timed else 0
+            rc = lib().hy_executor_run(self._h, int(passes), mode, int(trace), buf, size, ctypes.byref(needed))
             if rc == -9:
                 size = needed.value + 1
                 continue

@@ -107,7 +107,7 @@ int hy_executor_run(void* handle, int passes, int timed, int with_trace, char* o
                     size_t* needed) {
   try {
     if (!handle) return hy::set_error(HY_E_INVALID, "null executor handle");
-    return hy::write_out(hy::session_run(handle, passes, timed != 0, with_trace != 0), out, out_len, needed);
+    return hy::write_out(hy::session_run(handle, passes, timed, with_trace != 0), out, out_len, needed);
   } catch (...) {
     return hy::status_from_current_exception();
   }

@@ -12,7 +12,7 @@ int status_from_current_exception();
 std::string plan_json(const std::string& request);
 std::string execute_json(const std::string& request);
 void* session_create(const std::string& request);
-std::string session_run(void* handle, int passes, bool timed, bool with_trace);
+std::string session_run(void* handle, int passes, int timed, bool with_trace);
 void session_dump_params(void* handle, const std::string& dir);
 void session_destroy(void* handle);
 

@@ -203,6 +203,17 @@ ojson session_result(Session& S, bool with_trace) {
   st["enqueue_s_last_pass"] = r.stats.enqueue_s.empty() ? 0.0 : r.stats.enqueue_s.back();
   out["stats"] = st;
   if (!r.op_profile_ms.empty()) out["op_profile_ms"] = r.op_profile_ms;
+  if (!r.links.empty()) {
+    ojson ls = ojson::array();
+    for (const LinkStats& l : r.links) {
+      ls.push_back({{"plan_device", l.plan_device}, {"pass_s", l.pass_s}, {"h2d_busy_s", l.h2d_busy_s},
+                    {"d2h_busy_s", l.d2h_busy_s}, {"link_busy_s", l.link_busy_s},
+                    {"compute_busy_s", l.compute_busy_s}, {"exposed_s", l.exposed_s},
+                    {"overlap_frac", l.link_busy_s > 0 ? 1.0 - l.exposed_s / l.link_busy_s : 1.0},
+                    {"h2d_bytes", l.h2d_bytes}, {"d2h_bytes", l.d2h_bytes}, {"copies", l.copies}, {"ops", l.ops}});
+    }
+    out["links"] = ls;
+  }
   if (!r.pass_seconds.empty()) {
     out["report"] = ojson::parse(report_to_json(summarize(r.trace, S.cfg.cluster, S.strategy)));
     if (with_trace) out["chrome_trace"] = to_chrome_trace_json(r.trace);
@@ -224,10 +235,10 @@ std::string execute_json(const std::string& request) {
 
 void* session_create(const std::string& request) { return make_session(request).release(); }
 
-std::string session_run(void* handle, int passes, bool timed, bool with_trace) {
+std::string session_run(void* handle, int passes, int timed, bool with_trace) {
   Session* S = static_cast<Session*>(handle);
   const auto t0 = std::chrono::steady_clock::now();
-  S->exec->run(passes, timed);
+  S->exec->run(passes, timed != 0, timed == 2);
   ojson out = session_result(*S, with_trace);
   out["wall_s"] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return out.dump();

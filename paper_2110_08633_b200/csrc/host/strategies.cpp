@@ -497,62 +497,4 @@ std::pair<double, double> lower_bounds(const TaskInstance& inst) {
   return {total / inst.devices, longest};
 }
 
-std::vector<SimTask> tasks_from_instance(const TaskInstance& inst) {
-  validate(inst);
-  std::vector<SimTask> tasks;
-  std::vector<int> chain_of(inst.tasks.size(), 0);
-  int n_chains = 0;
-  for (size_t i = 0; i < inst.tasks.size(); ++i) {
-    const TaskInstance::Task& t = inst.tasks[i];
-    chain_of[i] = t.pred < 0 ? n_chains++ : chain_of[static_cast<size_t>(t.pred)];
-    SimTask task;
-    task.t.job = chain_of[i];
-    task.t.shard = t.pred < 0 ? 0 : tasks[static_cast<size_t>(t.pred)].t.shard + 1;
-    task.t.compute_s = t.duration_s;
-    task.act_in_from_host = false;
-    task.act_out = BoundaryOut::kNone;
-    if (t.pred >= 0) task.preds.push_back(t.pred);
-    task.label = t.id.empty() ? "t" + std::to_string(i) : t.id;
-    tasks.push_back(std::move(task));
-  }
-  return tasks;
-}
-
-SimTrace run_lrtf_on_instance(const TaskInstance& inst) {
-  ClusterSpec cluster;
-  for (int d = 0; d < inst.devices; ++d) {
-    DeviceSpec dev;
-    dev.device_id = "g" + std::to_string(d);
-    dev.mem_bytes = 1;
-    cluster.devices.push_back(dev);
-  }
-  cluster.host_dram_bytes = 1;
-  cluster.h2d.bandwidth_Bps = 1;
-  std::vector<SimTask> tasks = tasks_from_instance(inst);
-  std::vector<double> est(tasks.size());
-  for (size_t i = 0; i < tasks.size(); ++i) est[i] = tasks[i].t.compute_s;
-  SharpScheduler sched(tasks, est);
-  SimOptions opt;
-  opt.double_buffering = false;
-  return run_simulation(cluster, tasks, sched, opt);
-}
-
-TaskInstance reduce_tasks(const std::vector<SimTask>& tasks, const InterconnectSpec& h2d, int devices) {
-  TaskInstance inst;
-  inst.devices = devices;
-  for (size_t i = 0; i < tasks.size(); ++i) {
-    const SimTask& task = tasks[i];
-    if (task.preds.size() > 1) throw InvalidArgument("reduction requires chain-shaped tasks");
-    TaskInstance::Task t;
-    t.id = task.label.empty() ? "t" + std::to_string(i) : task.label;
-    t.duration_s = task.t.compute_s + xfer_s(task.t.param_load_bytes, h2d) +
-                   xfer_s(task.t.activation_in_bytes, h2d) + xfer_s(task.t.activation_out_bytes, h2d) +
-                   xfer_s(task.t.grad_offload_bytes, h2d);
-    t.pred = task.preds.empty() ? -1 : task.preds.front();
-    inst.tasks.push_back(std::move(t));
-  }
-  validate(inst);
-  return inst;
-}
-
 }  // namespace spillsim

@@ -679,11 +679,9 @@ cudaError_t attention_fwd_fa(cudaStream_t st, int B, int T, int H, const float* 
       !map2d(&mv, qkv, 3 * D, rows, 3 * D, 32, true)) {
     return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    const cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kFwdSmem);
+  {
+    const cudaError_t e = ensure_smem_limit(attn_fwd_kernel, kFwdSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int grid = B * H * ((T + 127) / 128);
   count_launch();
@@ -702,12 +700,10 @@ cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* 
       !map2d(&mkmn, qkv, 3 * D, rows, 3 * D, 32, true)) {
     return cudaErrorInvalidValue;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_dkdv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDkvSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(attn_dq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kDqSmem);
+  {
+    cudaError_t e = ensure_smem_limit(attn_dkdv_kernel, kDkvSmem);
+    if (e == cudaSuccess) e = ensure_smem_limit(attn_dq_kernel, kDqSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const long n = rows * H;
   count_launch();

@@ -66,12 +66,13 @@ __global__ void splitk_reduce_kernel(int M, int N, int S, const float* __restric
 }
 
 int sm_count_host() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
+  // every GPU of a node is the same part; initialised once, thread-safe (magic static)
+  static const int n = [] {
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
   return n;
 }
 

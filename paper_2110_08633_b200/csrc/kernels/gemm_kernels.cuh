@@ -753,12 +753,13 @@ bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long l
 }
 
 int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
+  // every GPU of a node is the same part; initialised once, thread-safe (magic static)
+  static const int n = [] {
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
   return n;
 }
 
@@ -774,11 +775,9 @@ cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, lon
                          : make_map(&mb, B, K, N, ldb, BK, BN, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
   auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, P3, MODE>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN, P3>::kTotal);
+  {
+    const cudaError_t e = ensure_smem_limit(kern, Smem<BN, P3>::kTotal);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
   const int grid = static_cast<int>(tiles < sm_count() ? tiles : sm_count());
@@ -798,11 +797,9 @@ cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const float* A
                          : make_map(&mb, B, K, N, ldb, BK, BN / 2, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
   if (!ok_a || !ok_b) return cudaErrorInvalidValue;
   auto kern = gemm_tf32_pair_kernel<BN, A_MN, B_MN, MODE>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SmemPair<BN>::kTotal);
+  {
+    const cudaError_t e = ensure_smem_limit(kern, SmemPair<BN>::kTotal);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const long tiles = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
   const long pairs = std::min<long>(tiles, sm_count() / 2);

@@ -33,12 +33,13 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 int sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
+  // every GPU of a node is the same part; initialised once, thread-safe (magic static)
+  static const int n = [] {
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
   return n;
 }
 
@@ -1055,12 +1056,11 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
   const int rpb = (rows + nb - 1) / nb;
   const int n_warps = d <= 3072 ? kWarpsPerBlock : 4;
   const size_t smem = static_cast<size_t>(n_warps) * 2 * d * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(ln_bwd_rr_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(ln_bwd_rr_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(ln_bwd_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
+  {
+    cudaError_t e = ensure_smem_limit(ln_bwd_rr_kernel<8>, 200 * 1024);
+    if (e == cudaSuccess) e = ensure_smem_limit(ln_bwd_rr_kernel<16>, 200 * 1024);
+    if (e == cudaSuccess) e = ensure_smem_limit(ln_bwd_kernel<32>, 200 * 1024);
+    if (e != cudaSuccess) return e;
   }
   float* ws_dg = ws;
   float* ws_db = ws + static_cast<long>(nb) * d;

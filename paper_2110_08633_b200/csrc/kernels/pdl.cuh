@@ -7,11 +7,33 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace hy {
 
 __device__ __forceinline__ void pdl_wait_and_trigger() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Raises `kern`'s dynamic shared-memory limit to `bytes` on the calling thread's current device.
+// Function attributes belong to each device's context, so the "already set" record is kept per
+// (kernel, device ordinal) and guarded for the executor's worker threads (one per GPU).
+template <typename Kern>
+cudaError_t ensure_smem_limit(Kern kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_pair(reinterpret_cast<const void*>(kern), dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 template <typename Kern, typename... Args>

@@ -86,6 +86,41 @@ def test_gemm_splitk(M, N, Kd, b_mn, a_mn):
     assert torch.equal(C, C2)
 
 
+DW_SHAPES = [(3072, 768, 4096), (2304, 768, 4096), (768, 3072, 4096), (768, 2304, 4096), (768, 768, 4096),
+             (6400, 1600, 1024), (1600, 6400, 1024)]
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", DW_SHAPES)
+def test_gemm_split256_weight_grads(shape, a_mn, b_mn):
+    """The weight-gradient shapes of C2 (K = 4096 tokens) and XL b2 (K = 1024) through the
+    256-wide CTA-pair split-K path (taken when a workspace is set: the executor's default),
+    beta = 1 accumulation into an existing gradient: equal to torch fp32 within the TF32 bound,
+    equal to the unsplit kernel within TF32 rounding of the partial sums, and bitwise
+    deterministic across calls."""
+    M, N, Kd = shape
+    torch.manual_seed(M * 7 + N + Kd)
+    A = torch.randn(M, Kd, device=dev) * 0.1
+    B = torch.randn(N, Kd, device=dev) * 0.1
+    C0 = torch.randn(M, N, device=dev)
+    Ain = A.T.contiguous() if a_mn else A
+    Bin = B.T.contiguous() if b_mn else B
+    ws = torch.empty(2 * 3072 * 768 + 16, device=dev)  # the executor's C2 split-K workspace size
+    try:
+        K.gemm_config(splitk_ws=ws)
+        C1 = K.gemm(Ain, Bin, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=Kd, C=C0.clone(), beta=1.0)
+        C2 = K.gemm(Ain, Bin, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=Kd, C=C0.clone(), beta=1.0)
+    finally:
+        K.gemm_config()
+    Cu = K.gemm(Ain, Bin, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=Kd, C=C0.clone(), beta=1.0)  # no workspace: unsplit
+    torch.cuda.synchronize()
+    ref = C0 + A @ B.T
+    assert rel(C1, ref) < 3e-3, rel(C1, ref)
+    assert rel(C1 - C0, Cu - C0) < 1e-4  # same TF32 operands, fp32 partial sums in another order
+    assert torch.equal(C1, C2)
+
+
 def test_gemm_epilogues():
     M, N, Kd = 512, 640, 256
     A = torch.randn(M, Kd, device=dev)
