@@ -47,7 +47,7 @@ $(B)/test_spillsim: tests/native/test_spillsim.cpp $(PKG)/libhydra.so
 	$(CXX) $(CXXFLAGS) $< -o $@ -L$(PKG) -lhydra -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle/liboracle_gpt.so: oracle/gpt_oracle.c oracle/gpt_oracle.h
-	gcc -std=c11 -O2 -fPIC -fopenmp -shared $< -o $@ -lm
+	gcc -std=gnu11 -O3 -fPIC -fopenmp -shared $< -o $@ -lm
 
 ref:
 	$(MAKE) -C oracle ref

@@ -6,6 +6,7 @@
 #include <omp.h>
 #include <stdlib.h>
 #include <string.h>
+#include <immintrin.h>
 
 #define LN_EPS 1e-5
 
@@ -16,66 +17,127 @@ static float* falloc(long n) {
   return p;
 }
 
+/* Blocked GEMM for the oracle: operands packed into fp64 panels (192 x 256 of A, 256 x 256
+ * of B), 8 x 16 register micro-tiles (AVX-512 when the host has it, else plain C), every
+ * output accumulated in double over the whole K (the per-tile accumulator is double; the
+ * k-blocks add into it). Same arithmetic contract as a plain fp64 dot product of the fp32
+ * inputs (exactly representable in double); only the summation order differs. */
+#define MR 8
+#define NR 16
+#define MB 192
+#define NB 256
+#define KC 256
+
+__attribute__((target("avx512f")))
+static void ukern_avx512(int kc, const double* restrict a, const double* restrict b, double* restrict c, int ldc) {
+  __m512d c00 = _mm512_setzero_pd(), c01 = _mm512_setzero_pd(), c10 = _mm512_setzero_pd(), c11 = _mm512_setzero_pd(),
+          c20 = _mm512_setzero_pd(), c21 = _mm512_setzero_pd(), c30 = _mm512_setzero_pd(), c31 = _mm512_setzero_pd(),
+          c40 = _mm512_setzero_pd(), c41 = _mm512_setzero_pd(), c50 = _mm512_setzero_pd(), c51 = _mm512_setzero_pd(),
+          c60 = _mm512_setzero_pd(), c61 = _mm512_setzero_pd(), c70 = _mm512_setzero_pd(), c71 = _mm512_setzero_pd();
+  for (int k = 0; k < kc; ++k) {
+    const __m512d b0 = _mm512_load_pd(b + k * NR), b1 = _mm512_load_pd(b + k * NR + 8);
+    const double* ak = a + k * MR;
+    __m512d av;
+    av = _mm512_set1_pd(ak[0]); c00 = _mm512_fmadd_pd(av, b0, c00); c01 = _mm512_fmadd_pd(av, b1, c01);
+    av = _mm512_set1_pd(ak[1]); c10 = _mm512_fmadd_pd(av, b0, c10); c11 = _mm512_fmadd_pd(av, b1, c11);
+    av = _mm512_set1_pd(ak[2]); c20 = _mm512_fmadd_pd(av, b0, c20); c21 = _mm512_fmadd_pd(av, b1, c21);
+    av = _mm512_set1_pd(ak[3]); c30 = _mm512_fmadd_pd(av, b0, c30); c31 = _mm512_fmadd_pd(av, b1, c31);
+    av = _mm512_set1_pd(ak[4]); c40 = _mm512_fmadd_pd(av, b0, c40); c41 = _mm512_fmadd_pd(av, b1, c41);
+    av = _mm512_set1_pd(ak[5]); c50 = _mm512_fmadd_pd(av, b0, c50); c51 = _mm512_fmadd_pd(av, b1, c51);
+    av = _mm512_set1_pd(ak[6]); c60 = _mm512_fmadd_pd(av, b0, c60); c61 = _mm512_fmadd_pd(av, b1, c61);
+    av = _mm512_set1_pd(ak[7]); c70 = _mm512_fmadd_pd(av, b0, c70); c71 = _mm512_fmadd_pd(av, b1, c71);
+  }
+#define ST(r, x0, x1) \
+  _mm512_storeu_pd(c + r * ldc, _mm512_add_pd(_mm512_loadu_pd(c + r * ldc), x0)); \
+  _mm512_storeu_pd(c + r * ldc + 8, _mm512_add_pd(_mm512_loadu_pd(c + r * ldc + 8), x1));
+  ST(0, c00, c01) ST(1, c10, c11) ST(2, c20, c21) ST(3, c30, c31)
+  ST(4, c40, c41) ST(5, c50, c51) ST(6, c60, c61) ST(7, c70, c71)
+#undef ST
+}
+
+static void ukern_generic(int kc, const double* restrict a, const double* restrict b, double* restrict c, int ldc) {
+  double acc[MR][NR];
+  for (int r = 0; r < MR; ++r) for (int j = 0; j < NR; ++j) acc[r][j] = 0.0;
+  for (int k = 0; k < kc; ++k)
+    for (int r = 0; r < MR; ++r)
+      for (int j = 0; j < NR; ++j) acc[r][j] += a[k * MR + r] * b[k * NR + j];
+  for (int r = 0; r < MR; ++r) for (int j = 0; j < NR; ++j) c[r * ldc + j] += acc[r][j];
+}
+
+/* pack rows [0,n) x k [0,kc) of X (element (r,k) at X[r*sr + k*sk]) into panels of P rows:
+ * out[(p*KC + k)*P + r], zero-padded to a multiple of P */
+static void pack(int n, int kc, const float* X, long sr, long sk, int P, int npanels, double* out) {
+  for (int p = 0; p < npanels; ++p) {
+    double* o = out + (long)p * KC * P;
+    if (sk == 1) {
+      for (int r = 0; r < P; ++r) {
+        const int i = p * P + r;
+        if (i < n) { const float* x = X + (long)i * sr; for (int k = 0; k < kc; ++k) o[k * P + r] = x[k]; }
+        else for (int k = 0; k < kc; ++k) o[k * P + r] = 0.0;
+      }
+    } else {
+      for (int k = 0; k < kc; ++k) {
+        const float* x = X + (long)k * sk;
+        for (int r = 0; r < P; ++r) { const int i = p * P + r; o[k * P + r] = i < n ? x[(long)i * sr] : 0.0; }
+      }
+    }
+  }
+}
+
+static void gemm64(int M, int N, int K, const float* A, long sam, long sak, const float* B, long sbk, long sbn,
+            float* C, long ldc, const float* bias, int acc) {
+  const int mt = (M + MB - 1) / MB, nt = (N + NB - 1) / NB;
+  const int avx512 = __builtin_cpu_supports("avx512f");
+#pragma omp parallel
+  {
+    double* ap = (double*)aligned_alloc(64, sizeof(double) * MB * KC);
+    double* bp = (double*)aligned_alloc(64, sizeof(double) * NB * KC);
+    double* ct = (double*)aligned_alloc(64, sizeof(double) * MB * NB);
+#pragma omp for schedule(dynamic) collapse(2)
+    for (int tj = 0; tj < nt; ++tj)
+      for (int ti = 0; ti < mt; ++ti) {
+        const int i0 = ti * MB, j0 = tj * NB;
+        const int mb = M - i0 < MB ? M - i0 : MB, nb = N - j0 < NB ? N - j0 : NB;
+        const int pm = (mb + MR - 1) / MR, pn = (nb + NR - 1) / NR;
+        memset(ct, 0, sizeof(double) * MB * NB);
+        for (int k0 = 0; k0 < K; k0 += KC) {
+          const int kc = K - k0 < KC ? K - k0 : KC;
+          pack(mb, kc, A + (long)i0 * sam + (long)k0 * sak, sam, sak, MR, pm, ap);
+          pack(nb, kc, B + (long)j0 * sbn + (long)k0 * sbk, sbn, sbk, NR, pn, bp);
+          for (int q = 0; q < pn; ++q)
+            for (int p = 0; p < pm; ++p) {
+              if (avx512) ukern_avx512(kc, ap + (long)p * KC * MR, bp + (long)q * KC * NR, ct + p * MR * NB + q * NR, NB);
+              else ukern_generic(kc, ap + (long)p * KC * MR, bp + (long)q * KC * NR, ct + p * MR * NB + q * NR, NB);
+            }
+        }
+        for (int i = 0; i < mb; ++i) {
+          float* c = C + (long)(i0 + i) * ldc + j0;
+          for (int j = 0; j < nb; ++j) {
+            double s = ct[i * NB + j] + (bias ? bias[j0 + j] : 0.0);
+            c[j] = acc ? (float)(c[j] + s) : (float)s;
+          }
+        }
+      }
+    free(ap); free(bp); free(ct);
+  }
+}
+
 /* C[M,N] (+)= A[M,K] * B[N,K]^T (+ bias[N]) */
 static void mm_nt(int M, int N, int K, const float* A, long lda, const float* B, long ldb, float* C, long ldc,
                   const float* bias, int acc) {
-#pragma omp parallel for schedule(static)
-  for (int i = 0; i < M; ++i) {
-    const float* a = A + (long)i * lda;
-    for (int j = 0; j < N; ++j) {
-      const float* b = B + (long)j * ldb;
-      double s = 0.0;
-      for (int k = 0; k < K; ++k) s += (double)a[k] * (double)b[k];
-      if (bias) s += bias[j];
-      float* c = C + (long)i * ldc + j;
-      *c = acc ? (float)(*c + s) : (float)s;
-    }
-  }
+  gemm64(M, N, K, A, lda, 1, B, 1, ldb, C, ldc, bias, acc);
 }
 
 /* C[M,N] (+)= A[M,K] * B[K,N] */
 static void mm_nn(int M, int N, int K, const float* A, long lda, const float* B, long ldb, float* C, long ldc,
                   int acc) {
-#pragma omp parallel
-  {
-    double* row = (double*)malloc(sizeof(double) * (size_t)N);
-#pragma omp for schedule(static)
-    for (int i = 0; i < M; ++i) {
-      for (int j = 0; j < N; ++j) row[j] = 0.0;
-      const float* a = A + (long)i * lda;
-      for (int k = 0; k < K; ++k) {
-        const double av = a[k];
-        if (av == 0.0) continue;
-        const float* b = B + (long)k * ldb;
-        for (int j = 0; j < N; ++j) row[j] += av * (double)b[j];
-      }
-      float* c = C + (long)i * ldc;
-      for (int j = 0; j < N; ++j) c[j] = acc ? (float)(c[j] + row[j]) : (float)row[j];
-    }
-    free(row);
-  }
+  gemm64(M, N, K, A, lda, 1, B, ldb, 1, C, ldc, NULL, acc);
 }
 
 /* C[M,N] (+)= A[K,M]^T * B[K,N]  (weight gradients) */
 static void mm_tn(int M, int N, int K, const float* A, long lda, const float* B, long ldb, float* C, long ldc,
                   int acc) {
-#pragma omp parallel
-  {
-    double* row = (double*)malloc(sizeof(double) * (size_t)N);
-#pragma omp for schedule(static)
-    for (int i = 0; i < M; ++i) {
-      for (int j = 0; j < N; ++j) row[j] = 0.0;
-      for (int k = 0; k < K; ++k) {
-        const double av = A[(long)k * lda + i];
-        if (av == 0.0) continue;
-        const float* b = B + (long)k * ldb;
-        for (int j = 0; j < N; ++j) row[j] += av * (double)b[j];
-      }
-      float* c = C + (long)i * ldc;
-      for (int j = 0; j < N; ++j) c[j] = acc ? (float)(c[j] + row[j]) : (float)row[j];
-    }
-    free(row);
-  }
+  gemm64(M, N, K, A, 1, lda, B, ldb, 1, C, ldc, NULL, acc);
 }
 
 static void colsum_acc(int M, int N, const float* X, float* out) {
@@ -147,6 +209,34 @@ static double gelu_grad(double x) {
   return 0.5 * (1.0 + t) + 0.5 * x * (1.0 - t * t) * k0 * (1.0 + 3.0 * k1 * x * x);
 }
 
+/* one (batch, head) slice of qkv as contiguous double [T][hd] arrays */
+static void head_slices(const hy_dims* m, const float* qkv, int b, int h, double* q, double* k, double* v,
+                        double* kt, double* vt) {
+  const int T = m->T, D = m->d, hd = D / m->H;
+  for (int i = 0; i < T; ++i) {
+    const float* row = qkv + ((long)b * T + i) * 3 * D + h * hd;
+    for (int c = 0; c < hd; ++c) {
+      q[i * hd + c] = row[c];
+      k[i * hd + c] = row[D + c];
+      v[i * hd + c] = row[2 * D + c];
+      kt[(long)c * T + i] = row[D + c];
+      vt[(long)c * T + i] = row[2 * D + c];
+    }
+  }
+}
+
+/* s[j] = scale * q . k_j for j <= i: each score is a fp64 dot product over c in order
+ * (vectorised across keys through the transposed K) */
+static void scores(int i, int T, int hd, const double* qi, const double* kt, double scale, double* s) {
+  for (int j = 0; j <= i; ++j) s[j] = 0.0;
+  for (int c = 0; c < hd; ++c) {
+    const double qc = qi[c];
+    const double* kc = kt + (long)c * T;
+    for (int j = 0; j <= i; ++j) s[j] += qc * kc[j];
+  }
+  for (int j = 0; j <= i; ++j) s[j] *= scale;
+}
+
 /* causal attention; qkv [B*T, 3D]; out [B*T, D] */
 static void attn_fwd(const hy_dims* m, const float* qkv, float* out) {
   const int B = m->B, T = m->T, H = m->H, D = m->d, hd = D / H;
@@ -154,34 +244,39 @@ static void attn_fwd(const hy_dims* m, const float* qkv, float* out) {
 #pragma omp parallel
   {
     double* p = (double*)malloc(sizeof(double) * (size_t)T);
+    double* q = (double*)malloc(sizeof(double) * (size_t)T * hd * 5);
+    double* k = q + (long)T * hd;
+    double* v = k + (long)T * hd;
+    double* kt = v + (long)T * hd;
+    double* vt = kt + (long)T * hd;
+    double* o = (double*)malloc(sizeof(double) * (size_t)hd);
 #pragma omp for collapse(2) schedule(static)
     for (int b = 0; b < B; ++b) {
       for (int h = 0; h < H; ++h) {
+        head_slices(m, qkv, b, h, q, k, v, kt, vt);
         for (int i = 0; i < T; ++i) {
-          const float* q = qkv + ((long)b * T + i) * 3 * D + h * hd;
+          const double* qi = q + (long)i * hd;
+          scores(i, T, hd, qi, kt, scale, p);
           double mx = -1e300;
-          for (int j = 0; j <= i; ++j) {
-            const float* k = qkv + ((long)b * T + j) * 3 * D + D + h * hd;
-            double s = 0.0;
-            for (int c = 0; c < hd; ++c) s += (double)q[c] * k[c];
-            p[j] = s * scale;
-            if (p[j] > mx) mx = p[j];
-          }
+          for (int j = 0; j <= i; ++j) mx = p[j] > mx ? p[j] : mx;
           double z = 0.0;
           for (int j = 0; j <= i; ++j) {
             p[j] = exp(p[j] - mx);
             z += p[j];
           }
-          float* o = out + ((long)b * T + i) * D + h * hd;
-          for (int c = 0; c < hd; ++c) {
-            double s = 0.0;
-            for (int j = 0; j <= i; ++j) s += p[j] * qkv[((long)b * T + j) * 3 * D + 2 * D + h * hd + c];
-            o[c] = (float)(s / z);
+          for (int c = 0; c < hd; ++c) o[c] = 0.0;
+          for (int j = 0; j <= i; ++j) {
+            const double* vj = v + (long)j * hd;
+            for (int c = 0; c < hd; ++c) o[c] += p[j] * vj[c];
           }
+          float* orow = out + ((long)b * T + i) * D + h * hd;
+          for (int c = 0; c < hd; ++c) orow[c] = (float)(o[c] / z);
         }
       }
     }
     free(p);
+    free(q);
+    free(o);
   }
 }
 
@@ -189,52 +284,52 @@ static void attn_fwd(const hy_dims* m, const float* qkv, float* out) {
 static void attn_bwd(const hy_dims* m, const float* qkv, const float* dout, float* dqkv) {
   const int B = m->B, T = m->T, H = m->H, D = m->d, hd = D / H;
   const double scale = 1.0 / sqrt((double)hd);
-  memset(dqkv, 0, sizeof(float) * (size_t)B * T * 3 * D);
 #pragma omp parallel
   {
     double* p = (double*)malloc(sizeof(double) * (size_t)T);
     double* dp = (double*)malloc(sizeof(double) * (size_t)T);
     double* dq = (double*)malloc(sizeof(double) * (size_t)hd);
-    double* dkv = (double*)malloc(sizeof(double) * (size_t)T * 2 * hd);
+    double* go = (double*)malloc(sizeof(double) * (size_t)hd);
+    double* q = (double*)malloc(sizeof(double) * (size_t)T * hd * 7);
+    double* k = q + (long)T * hd;
+    double* v = k + (long)T * hd;
+    double* kt = v + (long)T * hd;
+    double* vt = kt + (long)T * hd;
+    double* dk = vt + (long)T * hd;
+    double* dv = dk + (long)T * hd;
 #pragma omp for collapse(2) schedule(static)
     for (int b = 0; b < B; ++b) {
       for (int h = 0; h < H; ++h) {
-        memset(dkv, 0, sizeof(double) * (size_t)T * 2 * hd);
+        head_slices(m, qkv, b, h, q, k, v, kt, vt);
+        memset(dk, 0, sizeof(double) * (size_t)T * hd * 2);
         for (int i = 0; i < T; ++i) {
-          const float* q = qkv + ((long)b * T + i) * 3 * D + h * hd;
-          const float* go = dout + ((long)b * T + i) * D + h * hd;
+          const double* qi = q + (long)i * hd;
+          const float* gor = dout + ((long)b * T + i) * D + h * hd;
+          for (int c = 0; c < hd; ++c) go[c] = gor[c];
+          scores(i, T, hd, qi, kt, scale, p);
           double mx = -1e300;
-          for (int j = 0; j <= i; ++j) {
-            const float* k = qkv + ((long)b * T + j) * 3 * D + D + h * hd;
-            double s = 0.0;
-            for (int c = 0; c < hd; ++c) s += (double)q[c] * k[c];
-            p[j] = s * scale;
-            if (p[j] > mx) mx = p[j];
-          }
+          for (int j = 0; j <= i; ++j) mx = p[j] > mx ? p[j] : mx;
           double z = 0.0;
           for (int j = 0; j <= i; ++j) {
             p[j] = exp(p[j] - mx);
             z += p[j];
           }
+          scores(i, T, hd, go, vt, 1.0, dp); /* dp[j] = dO_i . v_j */
           double delta = 0.0;
           for (int j = 0; j <= i; ++j) {
             p[j] /= z;
-            const float* v = qkv + ((long)b * T + j) * 3 * D + 2 * D + h * hd;
-            double s = 0.0;
-            for (int c = 0; c < hd; ++c) s += (double)go[c] * v[c];
-            dp[j] = s;
-            delta += p[j] * s;
+            delta += p[j] * dp[j];
           }
           for (int c = 0; c < hd; ++c) dq[c] = 0.0;
           for (int j = 0; j <= i; ++j) {
             const double ds = p[j] * (dp[j] - delta) * scale;
-            const float* k = qkv + ((long)b * T + j) * 3 * D + D + h * hd;
-            double* dk = dkv + (long)j * 2 * hd;
-            double* dv = dk + hd;
+            const double* kj = k + (long)j * hd;
+            double* dkj = dk + (long)j * hd;
+            double* dvj = dv + (long)j * hd;
             for (int c = 0; c < hd; ++c) {
-              dq[c] += ds * k[c];
-              dk[c] += ds * q[c];
-              dv[c] += p[j] * go[c];
+              dq[c] += ds * kj[c];
+              dkj[c] += ds * qi[c];
+              dvj[c] += p[j] * go[c];
             }
           }
           float* dqr = dqkv + ((long)b * T + i) * 3 * D + h * hd;
@@ -244,8 +339,8 @@ static void attn_bwd(const hy_dims* m, const float* qkv, const float* dout, floa
           float* dkr = dqkv + ((long)b * T + j) * 3 * D + D + h * hd;
           float* dvr = dkr + D;
           for (int c = 0; c < hd; ++c) {
-            dkr[c] = (float)dkv[(long)j * 2 * hd + c];
-            dvr[c] = (float)dkv[(long)j * 2 * hd + hd + c];
+            dkr[c] = (float)dk[(long)j * hd + c];
+            dvr[c] = (float)dv[(long)j * hd + c];
           }
         }
       }
@@ -253,7 +348,8 @@ static void attn_bwd(const hy_dims* m, const float* qkv, const float* dout, floa
     free(p);
     free(dp);
     free(dq);
-    free(dkv);
+    free(go);
+    free(q);
   }
 }
 
@@ -289,11 +385,14 @@ static void block_fwd(const hy_dims* m, const float* w, const float* h_in, float
   mm_nt(R, 3 * d, d, c->ln1, d, BT(w, HY_WQKV), d, c->qkv, 3 * d, BT(w, HY_BQKV), 0);
   attn_fwd(m, c->qkv, c->att);
   mm_nt(R, d, d, c->att, d, BT(w, HY_WO), d, c->hmid, d, BT(w, HY_BO), 0);
+#pragma omp parallel for schedule(static)
   for (long i = 0; i < (long)R * d; ++i) c->hmid[i] += h_in[i];
   ln_fwd(R, d, c->hmid, BT(w, HY_LN2_G), BT(w, HY_LN2_B), c->ln2, c->mean2, c->rstd2);
   mm_nt(R, 4 * d, d, c->ln2, d, BT(w, HY_WFC), d, c->fc, 4 * d, BT(w, HY_BFC), 0);
+#pragma omp parallel for schedule(static)
   for (long i = 0; i < (long)R * 4 * d; ++i) c->act[i] = (float)gelu(c->fc[i]);
   mm_nt(R, d, 4 * d, c->act, 4 * d, BT(w, HY_WPR), 4 * d, h_out, d, BT(w, HY_BPR), 0);
+#pragma omp parallel for schedule(static)
   for (long i = 0; i < (long)R * d; ++i) h_out[i] += c->hmid[i];
 }
 
@@ -310,6 +409,7 @@ static void block_bwd(const hy_dims* m, const float* w, float* g, const float* h
   mm_tn(d, 4 * d, R, dh, d, c->act, 4 * d, BT(g, HY_WPR), 4 * d, 1);
   colsum_acc(R, d, dh, BT(g, HY_BPR));
   mm_nn(R, 4 * d, d, dh, d, BT(w, HY_WPR), 4 * d, dact, 4 * d, 0);
+#pragma omp parallel for schedule(static)
   for (long i = 0; i < (long)R * 4 * d; ++i) dact[i] = (float)(dact[i] * gelu_grad(c->fc[i]));
   mm_tn(4 * d, d, R, dact, 4 * d, c->ln2, d, BT(g, HY_WFC), d, 1);
   colsum_acc(R, 4 * d, dact, BT(g, HY_BFC));
@@ -339,24 +439,28 @@ static double head_fwd_bwd(const hy_dims* m, const float* params, float* grads, 
   float* mean = falloc(R);
   float* rstd = falloc(R);
   ln_fwd(R, d, h, lnf, lnf + hy_pad32(d), z, mean, rstd);
-  const int CH = 64;
+  const int CH = 2048;
   float* logits = falloc((long)CH * V);
   float* dz = dh ? falloc((long)R * d) : NULL;
   double loss = 0.0;
   for (int r0 = 0; r0 < R; r0 += CH) {
     const int rows = R - r0 < CH ? R - r0 : CH;
     mm_nt(rows, V, d, z + (long)r0 * d, d, wte, d, logits, V, NULL, 0);
+    double* rl = (double*)malloc(sizeof(double) * (size_t)rows);
+#pragma omp parallel for schedule(static)
     for (int r = 0; r < rows; ++r) {
       float* l = logits + (long)r * V;
       double mx = -1e300, s = 0.0;
       for (int j = 0; j < V; ++j) if (l[j] > mx) mx = l[j];
       for (int j = 0; j < V; ++j) s += exp(l[j] - mx);
       const int t = targets[r0 + r];
-      loss += log(s) + mx - l[t];
+      rl[r] = log(s) + mx - l[t];
       if (dh) {
         for (int j = 0; j < V; ++j) l[j] = (float)((exp(l[j] - mx) / s - (j == t ? 1.0 : 0.0)) / R);
       }
     }
+    for (int r = 0; r < rows; ++r) loss += rl[r]; /* row order: deterministic */
+    free(rl);
     if (dh) {
       mm_nn(rows, d, V, logits, V, wte, d, dz + (long)r0 * d, d, 0);
       mm_tn(V, d, rows, logits, V, z + (long)r0 * d, d, grads, d, 1); /* dwte += dlogits^T z */
@@ -421,11 +525,11 @@ int oracle_shard_bwd(const hy_dims* m, const float* params, float* grads, int l0
                      const int32_t* targets, const float* act_in, const float* grad_out, float* grad_in) {
   const long n = (long)m->B * m->T * m->d;
   const int nl = l1 - l0;
-  /* recompute: inputs of every layer in the shard */
+  /* recompute (strategies.cpp:771-776: B(s) re-runs the shard forward from its checkpoint):
+   * the input of every layer plus each block's intermediates, kept for the backward */
   float** inp = (float**)calloc((size_t)nl, sizeof(float*));
+  block_cache* cs = (block_cache*)calloc((size_t)nl, sizeof(block_cache));
   float* h = falloc(n);
-  block_cache c;
-  cache_alloc(m, &c);
   if (l0 > 0) memcpy(h, act_in, sizeof(float) * (size_t)n);
   for (int l = l0; l < l1; ++l) {
     inp[l - l0] = falloc(n);
@@ -433,10 +537,8 @@ int oracle_shard_bwd(const hy_dims* m, const float* params, float* grads, int l0
     if (l == 0) {
       embed_fwd(m, params, tokens, h);
     } else if (l <= m->L) {
-      float* out = falloc(n);
-      block_fwd(m, params + hy_layer_offset(m, l), h, out, &c);
-      memcpy(h, out, sizeof(float) * (size_t)n);
-      free(out);
+      cache_alloc(m, &cs[l - l0]);
+      block_fwd(m, params + hy_layer_offset(m, l), inp[l - l0], h, &cs[l - l0]);
     }
   }
   float* dh = falloc(n);
@@ -445,8 +547,8 @@ int oracle_shard_bwd(const hy_dims* m, const float* params, float* grads, int l0
     if (l == m->L + 1) {
       head_fwd_bwd(m, params, grads, inp[l - l0], targets, dh);
     } else if (l >= 1) {
-      block_fwd(m, params + hy_layer_offset(m, l), inp[l - l0], h, &c);
-      block_bwd(m, params + hy_layer_offset(m, l), grads + hy_layer_offset(m, l), inp[l - l0], &c, dh);
+      block_bwd(m, params + hy_layer_offset(m, l), grads + hy_layer_offset(m, l), inp[l - l0], &cs[l - l0], dh);
+      cache_free(&cs[l - l0]);
     } else {
       embed_bwd(m, grads, tokens, dh);
     }
@@ -454,9 +556,9 @@ int oracle_shard_bwd(const hy_dims* m, const float* params, float* grads, int l0
   if (l0 > 0 && grad_in) memcpy(grad_in, dh, sizeof(float) * (size_t)n);
   for (int i = 0; i < nl; ++i) free(inp[i]);
   free(inp);
+  free(cs);
   free(h);
   free(dh);
-  cache_free(&c);
   return 0;
 }
 
