@@ -76,6 +76,9 @@ int hy_executor_create(const char* request_json, void** handle);
 int hy_executor_run(void* handle, int passes, int timed, int with_trace, char* out, size_t out_len,
                     size_t* needed);
 int hy_executor_dump_params(void* handle, const char* dir);
+/* Job `job`'s host parameter vector (layout include/hydra_gpt.h; final after a pass) into
+ * dst (n_floats >= its length) or, with dst == NULL, just its length in *total_floats. */
+int hy_executor_read_params(void* handle, int job, float* dst, size_t n_floats, size_t* total_floats);
 void hy_executor_destroy(void* handle);
 /* Diagnostics: host microseconds per back-to-back launch (kind 0 GEMM, 1 LayerNorm). */
 double hy_host_launch_us(void* stream, int kind, int n, float* a, float* b, float* c);

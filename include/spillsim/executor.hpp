@@ -137,6 +137,9 @@ class Executor {
   void run(int passes, bool timed, bool interval_log = false);
   ExecResult& result() { return res_; }
   void dump_params(const std::string& dir) const;
+  // Copies job `job`'s current host parameter vector (final after a pass) into dst when
+  // dst != nullptr (n_floats must cover it); returns its length in floats.
+  size_t read_params(int job, float* dst, size_t n_floats) const;
 
  private:
   std::unique_ptr<ExecutorImpl> impl_;

@@ -615,6 +615,7 @@ double oracle_train_step(const hy_dims* m, float* params, float* mom, float* var
 }
 
 void oracle_init_params(const hy_dims* m, uint64_t model_key, float* params) {
+#pragma omp parallel for schedule(dynamic)
   for (int l = 0; l < m->L + 2; ++l) hy_init_layer(m, model_key, l, params + hy_layer_offset(m, l));
 }
 

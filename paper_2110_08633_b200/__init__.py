@@ -62,6 +62,21 @@ class Executor:
 
         check(lib().hy_executor_dump_params(self._h, directory.encode()))
 
+    def read_params(self, job: int):
+        """Job `job`'s host parameter vector (final after a pass) as a float32 numpy array."""
+        import ctypes
+
+        import numpy as np
+
+        from ._lib import check
+
+        n = ctypes.c_size_t(0)
+        check(lib().hy_executor_read_params(self._h, int(job), None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.float32)
+        check(lib().hy_executor_read_params(self._h, int(job), out.ctypes.data_as(ctypes.c_void_p), out.size,
+                                            ctypes.byref(n)))
+        return out
+
     def close(self):
         if getattr(self, "_h", None):
             lib().hy_executor_destroy(self._h)

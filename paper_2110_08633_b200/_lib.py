@@ -22,6 +22,8 @@ _SIGS = {
     "hy_executor_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p,
                                        ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
     "hy_executor_dump_params": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_char_p]),
+    "hy_executor_read_params": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t,
+                                               ctypes.POINTER(ctypes.c_size_t)]),
     "hy_executor_destroy": (None, [ctypes.c_void_p]),
     "hy_kernel_launches": (ctypes.c_long, []),
     "hy_host_launch_us": (ctypes.c_double, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,

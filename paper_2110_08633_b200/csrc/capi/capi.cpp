@@ -122,6 +122,17 @@ int hy_executor_dump_params(void* handle, const char* dir) {
   }
 }
 
+int hy_executor_read_params(void* handle, int job, float* dst, size_t n_floats, size_t* total_floats) {
+  try {
+    if (!handle) return hy::set_error(HY_E_INVALID, "null executor handle");
+    const size_t n = hy::session_read_params(handle, job, dst, n_floats);
+    if (total_floats) *total_floats = n;
+    return HY_OK;
+  } catch (...) {
+    return hy::status_from_current_exception();
+  }
+}
+
 void hy_executor_destroy(void* handle) {
   try {
     hy::session_destroy(handle);

@@ -1,6 +1,7 @@
 // Internal glue between the C-ABI and the C++ layers.
 #pragma once
 
+#include <cstddef>
 #include <string>
 
 namespace hy {
@@ -14,6 +15,7 @@ std::string execute_json(const std::string& request);
 void* session_create(const std::string& request);
 std::string session_run(void* handle, int passes, int timed, bool with_trace);
 void session_dump_params(void* handle, const std::string& dir);
+size_t session_read_params(void* handle, int job, float* dst, size_t n);
 void session_destroy(void* handle);
 
 }  // namespace hy

@@ -56,6 +56,7 @@ struct Session {
   WorkloadConfig cfg;
   std::string strategy;
   std::vector<ModelJob> jobs;
+  PinnedBoundaries pinned;
   CompiledStrategy cs;
   DispatchPlan plan;
   ExecOptions ex;
@@ -73,8 +74,9 @@ std::unique_ptr<Session> make_session(const std::string& request) {
   S->strategy = req.value("strategy", std::string("sharp"));
   const bool db = req.value("double_buffering", S->cfg.options.double_buffering);
   S->jobs = materialize_jobs(S->cfg);
+  S->pinned = pinned_boundaries(req, S->jobs.size());
   S->cs = build_strategy(strategy_for(S->cfg, strategy_kind_from_string(S->strategy)), S->jobs, S->cfg.cluster,
-                         S->cfg.options.buffer_policy);
+                         S->cfg.options.buffer_policy, S->pinned);
   S->cs.options.double_buffering = db;
   const auto t0 = std::chrono::steady_clock::now();
   S->plan = plan_simulation(S->cfg.cluster, S->cs.tasks, *S->cs.scheduler, S->cs.options);
@@ -101,7 +103,7 @@ std::unique_ptr<Session> make_session(const std::string& request) {
     Session* raw = S.get();
     ex.scheduler_factory = [raw]() {
       CompiledStrategy c = build_strategy(strategy_for(raw->cfg, strategy_kind_from_string(raw->strategy)), raw->jobs,
-                                          raw->cfg.cluster, raw->cfg.options.buffer_policy);
+                                          raw->cfg.cluster, raw->cfg.options.buffer_policy, raw->pinned);
       return std::move(c.scheduler);
     };
   }
@@ -245,6 +247,9 @@ std::string session_run(void* handle, int passes, int timed, bool with_trace) {
 }
 
 void session_dump_params(void* handle, const std::string& dir) { static_cast<Session*>(handle)->exec->dump_params(dir); }
+size_t session_read_params(void* handle, int job, float* dst, size_t n) {
+  return static_cast<Session*>(handle)->exec->read_params(job, dst, n);
+}
 
 void session_destroy(void* handle) { delete static_cast<Session*>(handle); }
 

@@ -25,7 +25,7 @@ std::string plan_json(const std::string& request) {
   const bool db = req.value("double_buffering", cfg.options.double_buffering);
   const std::vector<ModelJob> jobs = materialize_jobs(cfg);
   CompiledStrategy cs = build_strategy(strategy_for(cfg, strategy_kind_from_string(strategy)), jobs, cfg.cluster,
-                                       cfg.options.buffer_policy);
+                                       cfg.options.buffer_policy, pinned_boundaries(req, jobs.size()));
   cs.options.double_buffering = db;
   const DispatchPlan plan = plan_simulation(cfg.cluster, cs.tasks, *cs.scheduler, cs.options);
 

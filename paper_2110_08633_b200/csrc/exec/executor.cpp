@@ -723,6 +723,18 @@ void Executor::dump_params(const std::string& dir) const {
   }
 }
 
+size_t Executor::read_params(int job, float* dst, size_t n_floats) const {
+  auto it = impl_->jobs.find(job);
+  if (it == impl_->jobs.end()) throw InvalidArgument("read_params: job " + std::to_string(job) + " is not executed here");
+  const size_t total = static_cast<size_t>(it->second.total);
+  if (dst) {
+    if (n_floats < total) throw InvalidArgument("read_params: buffer holds " + std::to_string(n_floats) +
+                                                " floats, job needs " + std::to_string(total));
+    std::memcpy(dst, it->second.params, total * sizeof(float));
+  }
+  return total;
+}
+
 ExecResult run_execution(const ClusterSpec& cluster, const std::vector<SimTask>& tasks, const DispatchPlan& plan,
                          const SimOptions& options, const ExecOptions& exec) {
   Executor ex(cluster, tasks, plan, options, exec);

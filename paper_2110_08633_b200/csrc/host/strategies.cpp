@@ -254,14 +254,24 @@ SimTask plain_task(int job, int mb, int shard, Direction dir, double load, doubl
 }
 
 CompiledStrategy compile_sharp(const StrategyConfig& cfg, const std::vector<ModelJob>& jobs,
-                               const ClusterSpec& cluster, const BufferPolicy& policy) {
+                               const ClusterSpec& cluster, const BufferPolicy& policy,
+                               const PinnedBoundaries* pinned = nullptr) {
   CompiledStrategy out;
   out.config = cfg;
   const DeviceSpec& tight = cluster.devices[static_cast<size_t>(tightest_device(cluster))];
+  auto pinned_for = [&](size_t j) -> const std::vector<int>* {
+    if (!pinned || j >= pinned->size() || (*pinned)[j].empty()) return nullptr;
+    return &(*pinned)[j];
+  };
 
   std::vector<Partitioning> parts;
   parts.reserve(jobs.size());
-  for (const ModelJob& job : jobs) parts.push_back(partition(job.model, tight, policy));
+  for (size_t j = 0; j < jobs.size(); ++j) {
+    // A pinned job reuses its boundaries (partitioner.cpp:157-184: validated against the cap).
+    const std::vector<int>* pin = pinned_for(j);
+    parts.push_back(pin ? partition_with_boundaries(jobs[j].model, *pin, tight, policy)
+                        : partition(jobs[j].model, tight, policy));
+  }
 
   if (policy.kind == BufferPolicy::Kind::kAuto) {
     // One shared prefetch reserve (the largest any job wanted); re-cut the rest.
@@ -270,7 +280,9 @@ CompiledStrategy compile_sharp(const StrategyConfig& cfg, const std::vector<Mode
     BufferPolicy fixed = BufferPolicy::absolute(shared);
     fixed.framework_overhead_bytes = policy.framework_overhead_bytes;
     for (size_t j = 0; j < jobs.size(); ++j) {
-      if (parts[j].buffer_reserve_bytes != shared) parts[j] = partition(jobs[j].model, tight, fixed);
+      if (parts[j].buffer_reserve_bytes == shared) continue;
+      const std::vector<int>* pin = pinned_for(j);
+      parts[j] = pin ? partition_with_boundaries(jobs[j].model, *pin, tight, fixed) : partition(jobs[j].model, tight, fixed);
     }
   }
 
@@ -451,11 +463,22 @@ Feasibility check_feasibility(const StrategyConfig& cfg, const std::vector<Model
 
 CompiledStrategy build_strategy(const StrategyConfig& cfg, const std::vector<ModelJob>& jobs,
                                 const ClusterSpec& cluster, const BufferPolicy& policy) {
+  return build_strategy(cfg, jobs, cluster, policy, PinnedBoundaries{});
+}
+
+CompiledStrategy build_strategy(const StrategyConfig& cfg, const std::vector<ModelJob>& jobs,
+                                const ClusterSpec& cluster, const BufferPolicy& policy,
+                                const PinnedBoundaries& pinned) {
   validate(cluster);
   for (const ModelJob& job : jobs) validate(job);
   if (jobs.empty()) throw InvalidArgument("no jobs to schedule");
+  bool any_pinned = false;
+  for (const auto& b : pinned) any_pinned = any_pinned || !b.empty();
+  if (any_pinned && cfg.kind != StrategyKind::kSharp) {
+    throw InvalidArgument("pinned shard boundaries apply to the sharp strategy only");
+  }
   switch (cfg.kind) {
-    case StrategyKind::kSharp: return compile_sharp(cfg, jobs, cluster, policy);
+    case StrategyKind::kSharp: return compile_sharp(cfg, jobs, cluster, policy, any_pinned ? &pinned : nullptr);
     case StrategyKind::kTaskParallel: return compile_task_parallel(cfg, jobs, cluster);
     default: unsupported(cfg.kind);
   }

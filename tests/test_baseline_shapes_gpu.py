@@ -1,0 +1,144 @@
+"""Executor-vs-oracle parity at the BASELINE configs' own shapes (BASELINE.json configs[0..3]).
+
+Where tests/test_executor_gpu.py pins every executor path on toy dims, this module runs the
+shapes the bench runs, through the same capped HBM budgets and the same plans:
+
+* C1 — 2 tiny jobs at their stated 40e6 cap, cut [0,3] (the real arena: see DESIGN §5).
+* C2 — GPT-2 small (d768, L12, T512, b8) at the 1.2e9 cap with its real cut [0,4,9,13]; two
+  jobs x two minibatches, so the job switch forces the write-back cache's eviction, the
+  split-K weight-gradient GEMMs run at their benched shapes, and T=512 flash attention runs
+  inside the executor. Jobs 0 and 3 of C2: the smallest and the largest learning rate.
+* XL — one GPT-2 XL job (d1600, 25 heads, L48) through 24e9 with the cut C3's b16 jobs get
+  ([0,24,48], pinned through partition_with_boundaries with C3's shared reserve), at b=2 to
+  bound the oracle's CPU time.
+* C4 — GPT-J dims (d4096, 64 heads, L28, b1) through 24e9, cut [0,8,16,24], with half the
+  layers' AdamW on the host as the C4 runs were measured.
+
+Each runs in TF32 (the benched precision) and 3xTF32 ("fp32"); the oracle (fp64-accumulating
+CPU restatement, oracle/gpt_oracle.c) runs once per config and is shared by both precisions.
+Bounds (north_star): per-step losses rel 1e-3 and per-layer ||p_gpu - p_cpu|| / ||p_cpu||
+1e-3 for TF32; 1e-4 / 1e-4 for 3xTF32. Measured deviations are appended to $HY_PARITY_LOG
+(JSON lines) when it is set.
+"""
+import concurrent.futures as cf
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+import paper_2110_08633_b200 as P  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+TOL = {"tf32": dict(loss_tol=1e-3, param_tol=1e-3), "fp32": dict(loss_tol=1e-4, param_tol=1e-4)}
+C3_SHARED_RESERVE = 5359724800.0  # C3's auto-policy shared reserve
+
+
+def load(name):
+    with open(os.path.join(ROOT, "configs", name + ".json")) as f:
+        return json.load(f)
+
+
+def c1():
+    cfg = load("c1_tiny")
+    return cfg, {}, [[0, 3], [0, 3]]
+
+
+def c2():
+    cfg = load("c2_gpt2small_x8")
+    cfg["jobs"] = [dict(cfg["jobs"][i], minibatches_per_epoch=2) for i in (0, 3)]
+    return cfg, {}, [[0, 4, 9, 13]] * 2
+
+
+def xl():
+    cfg = load("c3_gpt2xl_x16")
+    model = dict(cfg["models"][0])
+    model["generator"] = dict(model["generator"], batch_size=2)
+    cfg["models"] = [model]
+    cfg["jobs"] = [dict(cfg["jobs"][0], batch_size=2, minibatches_per_epoch=2)]
+    cfg["options"] = dict(cfg["options"], buffer_policy={"kind": "absolute", "value": C3_SHARED_RESERVE})
+    return cfg, {"shard_boundaries": [[0, 24, 48]]}, [[0, 24, 48]]
+
+
+def c4():
+    cfg = load("c4_gptj6b")
+    cfg["jobs"] = [dict(cfg["jobs"][0], minibatches_per_epoch=2)]
+    return cfg, {"host_opt_fraction": 0.5}, [[0, 8, 16, 24]]
+
+
+CASES = {"c1": c1, "c2": c2, "xl": xl, "c4": c4}
+_pool = cf.ThreadPoolExecutor(max_workers=1)
+_oracle = {}
+
+
+def oracle_result(name, cfg, starts, background):
+    """The oracle's (losses, params) for a case, computed once. `background` starts it on a
+    worker thread (the oracle's C calls release the GIL) so it overlaps the GPU run."""
+    if name not in _oracle:
+        fut = _pool.submit(O.run_workload_cpu, cfg, starts)
+        _oracle[name] = fut
+    fut = _oracle[name]
+    return fut if background else fut.result()
+
+
+def dims_of(cfg, job):
+    g = next(m["generator"] for m in cfg["models"] if m["name"] == cfg["jobs"][job]["model"])
+    return O.make_dims(d=g["d_model"], L=g["n_blocks"], T=g["seq_len"], B=g["batch_size"])
+
+
+def log(rec):
+    path = os.environ.get("HY_PARITY_LOG")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(rec) + "\n")
+
+
+@pytest.mark.parametrize("precision", ["tf32", "fp32"])
+@pytest.mark.parametrize("case", list(CASES))
+def test_baseline_shape_parity(case, precision):
+    cfg, extra, want_starts = CASES[case]()
+    big = case == "c4"  # ~94 GB of oracle state + ~70 GB pinned: never both at once
+    if big:
+        oracle_result(case, cfg, want_starts, background=False)
+    else:
+        oracle_result(case, cfg, want_starts, background=True)
+    ex = P.Executor(cfg, gpus=1, passes=1, precision=precision, **extra)
+    try:
+        res = ex.run(1)
+        assert res["shard_starts"] == want_starts
+        arena = res["stats"]["arena_bytes"][0]
+        assert arena <= cfg["cluster"]["devices"][0]["mem_bytes"]
+        gpu_params = {j: ex.read_params(j) for j in range(len(cfg["jobs"]))}
+    finally:
+        ex.close()
+    losses, params = oracle_result(case, cfg, want_starts, background=False)
+    tol = TOL[precision]
+    worst_loss, worst_param = 0.0, 0.0
+    for j in losses:
+        gl = np.array(res["losses"][j][: len(losses[j])])
+        cl = np.array(losses[j])
+        rel = np.abs(gl - cl) / np.abs(cl)
+        worst_loss = max(worst_loss, float(rel.max()))
+        m = dims_of(cfg, j)
+        pg, pc = gpu_params[j], params[j]
+        assert pg.shape == pc.shape
+        per_layer = []
+        for layer in range(m.L + 2):
+            a, b = O.layer_offset(m, layer), O.layer_offset(m, layer + 1)
+            per_layer.append(float(np.linalg.norm(pg[a:b] - pc[a:b]) / np.linalg.norm(pc[a:b])))
+        worst_param = max(worst_param, max(per_layer))
+        log({"case": case, "precision": precision, "job": j, "gpu_losses": gl.tolist(), "cpu_losses": cl.tolist(),
+             "loss_rel": rel.tolist(), "param_rel_max": max(per_layer),
+             "param_rel_argmax_layer": int(np.argmax(per_layer)), "arena_bytes": arena,
+             "cap": cfg["cluster"]["devices"][0]["mem_bytes"], "shard_starts": res["shard_starts"][j]})
+        assert rel.max() < tol["loss_tol"], (case, precision, j, gl, cl)
+        assert max(per_layer) < tol["param_tol"], (case, precision, j, int(np.argmax(per_layer)), max(per_layer))
+    if big and precision == "fp32":
+        _oracle.pop(case, None)  # last user: release ~24 GB
