@@ -158,42 +158,34 @@ def reduce_over_ranks(dist, device, dev_time, wall, samples, h2d, d2h, launches)
 
 
 # ------------------------------------------------------------------------- GPU leg
-def live_gemm_roofline(torch, cfg):
-    """Dominant kernel: the tcgen05 TF32 GEMM, measured at the workload's QKV projection
-    (X[M,d] W^T[d,3d] + bias, the first GEMM of every block forward), CUDA-event timed on its
-    launching stream, against a live cuBLAS TF32 peak (MEASURED_PEAKS.json carries bf16 only).
-    `traffic` = DRAM bytes of that launch from the committed ncu --set full capture."""
-    from paper_2110_08633_b200 import kernels as K
-
-    g = cfg["models"][0]["generator"]
-    d = g["d_model"]
-    M = g["batch_size"] * g["seq_len"]
-    dev = torch.device("cuda")
-    A = torch.randn(M, d, device=dev)
-    B = torch.randn(3 * d, d, device=dev)
-    bias = torch.randn(3 * d, device=dev)
-    C = torch.empty(M, 3 * d, device=dev)
+def _time_launches(torch, fn, reps=50):
+    """Seconds per launch of `fn`, CUDA events on the launching stream, the launches queued
+    behind a GPU spin so the events bracket back-to-back kernels (no host launch gaps; the
+    executor also enqueues ahead of the GPU)."""
     for _ in range(5):
-        K.gemm(A, B, C=C, bias=bias)
+        fn()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 50
     torch.cuda.synchronize()
-    # queue the launches behind a GPU spin so the events bracket back-to-back kernels (no host
-    # launch gaps; the executor also enqueues ahead of the GPU)
     torch.cuda._sleep(300_000_000)
     e0.record(s)
     for _ in range(reps):
-        K.gemm(A, B, C=C, bias=bias)
+        fn()
     e1.record(s)
     torch.cuda.synchronize()
-    t = e0.elapsed_time(e1) / 1e3 / reps
-    flops = 2.0 * M * 3 * d * d
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def live_tf32_peak(torch):
+    """cuBLAS TF32 8192^3 in this run (MEASURED_PEAKS.json carries bf16 only): TFLOP/s."""
+    dev = torch.device("cuda")
     torch.backends.cuda.matmul.allow_tf32 = True
     X = torch.randn(8192, 8192, device=dev)
     Y = torch.randn(8192, 8192, device=dev)
     for _ in range(3):
         X @ Y
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     best = 1e9
     for _ in range(5):
@@ -202,25 +194,96 @@ def live_gemm_roofline(torch, cfg):
         e1.record(s)
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / 1e3)
-    peak = 2.0 * 8192 ** 3 / best / 1e12
     torch.backends.cuda.matmul.allow_tf32 = False
     del X, Y
-    ach = flops / t / 1e12
-    traffic = None
+    return 2.0 * 8192 ** 3 / best / 1e12
+
+
+def live_gemm_roofline(torch, cfg, peak):
+    """Dominant kernel family: the tcgen05 TF32 GEMM (~65% of C2 kernel time). Two instantiations
+    are timed at the workload's shapes, CUDA events on their launching stream:
+      * dW(fc): C[4d x d] = dY^T X over K = b*s tokens, both operands token-major (MN-major) —
+        gemm_tf32_pair_kernel<*,1,1,0>, the largest single instantiation in the C2 launch list
+        (profiles/r01_launches_c2_summary.txt), with the executor's split-K workspace;
+      * QKV: X[b*s, d] W^T[d, 3d] + bias, the first GEMM of every block forward.
+    The top-level fields are the dW GEMM's; `traffic` = DRAM bytes per launch from the committed
+    ncu --set full captures (profiles/roofline_traffic.json)."""
+    from paper_2110_08633_b200 import kernels as K
+
+    g = cfg["models"][0]["generator"]
+    d = g["d_model"]
+    M = g["batch_size"] * g["seq_len"]
+    dev = torch.device("cuda")
+    traffic = {}
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
             tr = json.load(f)
-        if tr.get("shape") == [M, 3 * d, d]:
-            traffic = tr["dram_bytes_per_launch"]
+        for e in tr.get("captures", [tr]):
+            traffic[(e.get("name", "qkv"), tuple(e["shape"]))] = e["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
-    return {"bound": "tensor", "kernel": f"gemm_tf32_kernel qkv [{M}x{3*d}x{d}] +bias (tcgen05 kind::tf32)",
-            "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
-            "peak_source": "live cuBLAS TF32 8192^3 in this run (MEASURED_PEAKS.json has no TF32 figure; "
-                           "nominal dense TF32 1100)",
-            "frac_of_nominal_tf32": round(ach / 1100.0, 4),
-            "traffic": traffic, "algorithmic_bytes": int(4 * (M * d + 3 * d * d + 3 * d + M * 3 * d)),
-            "launch_us": round(t * 1e6, 2)}
+    out = []
+    # dW(fc): A = dY [M, 4d] (token-major => a_mn), B = X [M, d] (b_mn); C [4d, d]
+    ws = torch.empty(2 * 4 * d * d, device=dev)  # the executor's split-K workspace (two 4d x d partials)
+    K.gemm_config(splitk_ws=ws)
+    dY = torch.randn(M, 4 * d, device=dev)
+    X = torch.randn(M, d, device=dev)
+    W = torch.empty(4 * d, d, device=dev)
+    t = _time_launches(torch, lambda: K.gemm(dY, X, a_mn=True, b_mn=True, C=W))
+    K.gemm_config(splitk_ws=None)
+    fl = 2.0 * 4 * d * d * M
+    out.append({"name": "dW_fc", "kernel": f"gemm_tf32_pair_kernel dW(fc) [{4*d}x{d}x{M}] MN/MN operands, split-K "
+                "workspace (tcgen05 kind::tf32, cta_group::2)", "shape": [4 * d, d, M], "seconds": t, "flops": fl,
+                "algorithmic_bytes": int(4 * (M * 4 * d + M * d + 4 * d * d))})
+    del dY, X, W, ws
+    A = torch.randn(M, d, device=dev)
+    B = torch.randn(3 * d, d, device=dev)
+    bias = torch.randn(3 * d, device=dev)
+    C = torch.empty(M, 3 * d, device=dev)
+    t = _time_launches(torch, lambda: K.gemm(A, B, C=C, bias=bias))
+    fl = 2.0 * M * 3 * d * d
+    out.append({"name": "qkv", "kernel": f"gemm_tf32_pair_kernel qkv [{M}x{3*d}x{d}] +bias (tcgen05 kind::tf32, "
+                "cta_group::2)", "shape": [M, 3 * d, d], "seconds": t, "flops": fl,
+                "algorithmic_bytes": int(4 * (M * d + 3 * d * d + 3 * d + M * 3 * d))})
+    del A, B, C, bias
+    recs = []
+    for e in out:
+        ach = e["flops"] / e["seconds"] / 1e12
+        recs.append({"bound": "tensor", "kernel": e["kernel"], "achieved": round(ach, 1), "peak": round(peak, 1),
+                     "unit": "TFLOP/s", "frac": round(ach / peak, 4),
+                     "peak_source": "in-run cuBLAS TF32 8192^3 (MEASURED_PEAKS.json has no TF32 figure; nominal "
+                                    "dense TF32 1100)",
+                     "frac_of_nominal_tf32": round(ach / 1100.0, 4),
+                     "traffic": traffic.get((e["name"], tuple(e["shape"]))),
+                     "algorithmic_bytes": e["algorithmic_bytes"], "launch_us": round(e["seconds"] * 1e6, 2)})
+    top = dict(recs[0])
+    top["others"] = recs[1:]
+    return top
+
+
+def plan_roofline(plan, cfg, peak_tflops, bw_dn, bw_up, G):
+    """North-star shard roofline, computed from the plan's ShardTasks:
+    sum_tau max(F_tau / P, H2D_tau / BW_dn, D2H_tau / BW_up) / G, with F_tau the cost-model
+    FLOP of the task (compute_s x device_reference_flops, strategies.cpp:753,775), H2D_tau =
+    param_load + activation_in bytes and D2H_tau = activation_out + grad_offload bytes (the
+    ShardTask fields of build_sharp, strategies.cpp:746-776), P the in-run TF32 peak and BW the
+    probed duplex link rates of this box. Also returns the totals."""
+    F_ref = {m["name"]: m["generator"].get("device_reference_flops", 1e15) for m in cfg["models"]}
+    P_ = peak_tflops * 1e12
+    total = flops = h2d = d2h = 0.0
+    bound = {"compute": 0.0, "h2d": 0.0, "d2h": 0.0}
+    for t in plan["tasks"]:
+        F = t["compute_s"] * F_ref[cfg["jobs"][t["job"]]["model"]]
+        hi = t["param_load_bytes"] + t["activation_in_bytes"]
+        ho = t["activation_out_bytes"] + t["grad_offload_bytes"]
+        terms = {"compute": F / P_, "h2d": hi / bw_dn, "d2h": ho / bw_up}
+        k = max(terms, key=terms.get)
+        bound[k] += terms[k]
+        total += terms[k]
+        flops += F
+        h2d += hi
+        d2h += ho
+    return total / G, flops, h2d, d2h, {k: round(v / G, 5) for k, v in bound.items()}
 
 
 def probe_link(torch, nbytes=1 << 29, reps=4):
@@ -347,51 +410,88 @@ def run_hydra(args, cfg):
         if res["losses"] and res["losses"][0] else [],
         "device_busy_frac": round(st["device_busy_s_last_pass"] / res["pass_seconds"][-1], 4),
     }
-    # shard roofline (north_star): per task max(compute at peak, link bytes / link BW), cost-model bytes
-    link = 55.0e9
-    virt = res["virtual_makespan_s"]
-    out["shard_roofline"] = {
-        "bound": "host_link",
-        "definition": "sum over shard tasks of max(F_tau/peak, H2D_tau/BW, D2H_tau/BW) / G, cost-model bytes "
-                      "(SURVEY §8d); approximated by the reference engine's virtual makespan at 55 GB/s",
-        "roofline_makespan_s": round(virt, 5),
-        "measured_makespan_s": round(dev_time / args.steps, 5),
-        "frac": round(virt / (dev_time / args.steps), 4),
-        "link_GBps_assumed": link / 1e9,
-        "achieved_h2d_GBps": round(h2d / (dev_time / args.steps) / 1e9, 2),
-        "achieved_d2h_GBps": round(d2h / (dev_time / args.steps) / 1e9, 2),
-    }
+    # Overlap: one more pass with the interval log (two event records per copy /
+    # op), outside the timed region: copy-only link time per direction, compute time, and
+    # overlap_frac = 1 - exposed transfer / total transfer on this GPU.
+    links = None
+    try:
+        lres = ex.run(1, timed=True, interval_log=True)
+        links = lres.get("links")
+    except Exception as e:  # pragma: no cover
+        links = [{"error": str(e)}]
     try:
         lp = probe_link(torch)
-        # the same pass against this box's measured duplex link and the bytes actually moved
-        # (cost-model bytes + Adam m/v + tied wte + biases): how close the pass runs to the physical link
-        t_link = max(h2d / (lp["duplex_h2d_GBps"] * 1e9), d2h / (lp["duplex_d2h_GBps"] * 1e9))
-        out["shard_roofline"]["link_probe"] = lp
-        out["shard_roofline"]["actual_bytes_link_bound_s"] = round(t_link, 5)
-        out["shard_roofline"]["actual_bytes_link_frac"] = round(t_link / (dev_time / args.steps), 4)
     except Exception as e:  # pragma: no cover
-        out["shard_roofline"]["link_probe"] = {"error": str(e)}
+        lp = {"error": str(e)}
     try:
-        out["roofline"] = live_gemm_roofline(torch, cfg)
+        peak = live_tf32_peak(torch)
+        out["roofline"] = live_gemm_roofline(torch, cfg, peak)
     except Exception as e:  # pragma: no cover
+        peak = None
         out["roofline"] = {"error": str(e)}
+    meas = dev_time / args.steps
+    sr = {"bound": "host_link", "measured_makespan_s": round(meas, 5),
+          "cost_model_virtual_makespan_s": round(res["virtual_makespan_s"], 5),
+          "cost_model_virtual_frac": round(res["virtual_makespan_s"] / meas, 4),
+          "cost_model_note": "the reference engine's virtual makespan (55 GB/s links, configs' 1 PF/s): a "
+                             "cost-model approximation, not the roofline",
+          "achieved_h2d_GBps": round(h2d / meas / 1e9, 2), "achieved_d2h_GBps": round(d2h / meas / 1e9, 2),
+          "link_probe": lp}
+    if peak and "duplex_h2d_GBps" in lp:
+        bw_dn, bw_up = lp["duplex_h2d_GBps"] * 1e9, lp["duplex_d2h_GBps"] * 1e9
+        plan = P.plan(cfg, gpus=n)
+        if world > 1:  # this rank's share of the plan (the per-GPU roofline of device `rank`)
+            mine = {t for t, dev, _ in plan["dispatch"] if dev == rank}
+            plan = dict(plan, tasks=[t for i, t in enumerate(plan["tasks"]) if i in mine])
+        G = 1 if world > 1 else n
+        roof, F_tot, h2d_m, d2h_m, by = plan_roofline(plan, cfg, peak, bw_dn, bw_up, G)
+        sr.update({
+            "definition": "sum over the plan's ShardTasks of max(F_tau/P, H2D_tau/BW_dn, D2H_tau/BW_up) / G; "
+                          "cost-model FLOP and bytes (SURVEY §8d), P = in-run cuBLAS TF32 peak, BW = this box's "
+                          "probed duplex pinned-copy rates",
+            "roofline_makespan_s": round(roof, 5), "frac": round(roof / meas, 4),
+            "peak_tflops": round(peak, 1), "bw_h2d_GBps": lp["duplex_h2d_GBps"], "bw_d2h_GBps": lp["duplex_d2h_GBps"],
+            "bound_by_term_s": by, "model_flops_per_pass": F_tot,
+            "model_h2d_bytes_per_pass": h2d_m, "model_d2h_bytes_per_pass": d2h_m})
+        # physical: the bytes actually moved (Adam m, v, tied wte, biases; minus what the caches
+        # elide) and the FLOP at the same peak — a pass-level bound (per-task actual bytes are not
+        # attributable once caches and streams interleave)
+        t_phys = max(F_tot / (peak * 1e12), h2d / bw_dn, d2h / bw_up)
+        sr["physical"] = {"definition": "max(model FLOP / P, actual H2D bytes / BW_dn, actual D2H bytes / BW_up) "
+                                        "per pass", "bound_s": round(t_phys, 5), "frac": round(t_phys / meas, 4),
+                          "flop_s": round(F_tot / (peak * 1e12), 5), "h2d_s": round(h2d / bw_dn, 5),
+                          "d2h_s": round(d2h / bw_up, 5)}
+        sr["physical_frac"] = sr["physical"]["frac"]
+    if links:
+        sr["links"] = links
+        ok = [l for l in links if "overlap_frac" in l]
+        if ok:
+            sr["overlap_frac"] = round(min(l["overlap_frac"] for l in ok), 4)
+            sr["link_busy_frac"] = round(max(l["link_busy_s"] / l["pass_s"] for l in ok), 4)
+    out["shard_roofline"] = sr
     ex.close()
     if not args.no_variants and world == 1:
-        # same workload, Adam moments stored / streamed as bf16 (fp32 master params, TF32 GEMMs):
-        # parity stated separately (tests/test_executor_gpu.py::test_bf16_optimizer_state)
-        vreq = dict(req, opt_state="bf16" if args.opt_state == "fp32" else "fp32")
-        vex = P.Executor(cfg, **vreq)
-        vex.run(args.warmup, timed=False)
-        torch.cuda.synchronize()
-        vres = vex.run(args.steps, timed=True)
-        vt = sum(vres["pass_seconds"])
-        out["variants"] = {f"opt_state_{vreq['opt_state']}": {
-            "value": round(vres["samples_per_pass"] * args.steps / vt, 3), "unit": "samples/s",
-            "ms_per_step": round(vt / args.steps * 1e3, 3),
-            "shard_roofline_frac": round(virt / (vt / args.steps), 4),
-            "h2d_bytes_per_step": int(vres["stats"]["h2d_bytes_per_pass"]),
-            "d2h_bytes_per_step": int(vres["stats"]["d2h_bytes_per_pass"])}}
-        vex.close()
+        # the same workload with (a) Adam moments stored / streamed as bf16 (fp32 master params,
+        # TF32 GEMMs; parity stated separately, tests/test_executor_gpu.py::test_bf16_optimizer_state)
+        # and (b) 3xTF32 ("fp32") GEMMs, the precision that holds 2e-4 on parameters at every
+        # BASELINE shape (tests/test_baseline_shapes_gpu.py)
+        out["variants"] = {}
+        other = "bf16" if args.opt_state == "fp32" else "fp32"
+        for name, over in ((f"opt_state_{other}", {"opt_state": other}), ("precision_fp32", {"precision": "fp32"})):
+            vex = P.Executor(cfg, **dict(req, **over))
+            vex.run(args.warmup, timed=False)
+            torch.cuda.synchronize()
+            vres = vex.run(args.steps, timed=True)
+            vt = sum(vres["pass_seconds"])
+            out["variants"][name] = {
+                "value": round(vres["samples_per_pass"] * args.steps / vt, 3), "unit": "samples/s",
+                "ms_per_step": round(vt / args.steps * 1e3, 3),
+                "h2d_bytes_per_step": int(vres["stats"]["h2d_bytes_per_pass"]),
+                "d2h_bytes_per_step": int(vres["stats"]["d2h_bytes_per_pass"])}
+            if "roofline_makespan_s" in out["shard_roofline"]:
+                out["variants"][name]["shard_roofline_frac"] = round(
+                    out["shard_roofline"]["roofline_makespan_s"] / (vt / args.steps), 4)
+            vex.close()
     if not args.no_cpu_baseline:
         try:
             secs, cores, _ = cpu_sample(cfg, starts=res["shard_starts"][0])

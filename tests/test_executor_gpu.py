@@ -68,35 +68,28 @@ def test_c1_sharp_two_shards(tmp_path, precision):
 
 
 @pytest.mark.parametrize("mem,starts", [(51e6, [0, 18]), (54e6, [0, 25])])
-@pytest.mark.parametrize("precision", ["fp32", "tf32"])
-def test_head_shard_without_embedding(tmp_path, mem, starts, precision):
+def test_head_shard_without_embedding(tmp_path, mem, starts):
     # 24 blocks: [0,18] puts blocks + head (tied wte copy) in shard 1; [0,25] a head-only
     # shard. Exercises the tied-wte load, deferred dwte (saved ln_f output z) and grads.
-    # lr 1e-3 for 3 steps: Adam turns TF32 noise in near-zero gradients (most of wte) into
-    # +-lr sign flips, so the TF32 parameter bound is 2e-3; fp32 (3xTF32) holds 1e-4.
+    # Path coverage at lr 1e-3 for 3 steps, held to the strict 3xTF32 bounds; TF32 numerics
+    # are pinned at the BASELINE shapes (tests/test_baseline_shapes_gpu.py).
     cfg = tiny_config(mem=mem, n_blocks=24, d=64, T=32, B=2, mbs=3, jobs=1)
-    tol = dict(loss_tol=1e-5, param_tol=1e-4) if precision == "fp32" else dict(param_tol=2e-3)
-    res = compare(cfg, tmp_path, hbm_slack_bytes=8e6, precision=precision, **tol)
+    res = compare(cfg, tmp_path, hbm_slack_bytes=8e6, precision="fp32", loss_tol=1e-5, param_tol=1e-4)
     assert res["shard_starts"][0] == starts
     assert res["stats"]["arena_bytes"][0] <= mem + 8e6
 
 
-@pytest.mark.parametrize("precision,tol", [("fp32", dict(loss_tol=1e-5, param_tol=1e-4)), ("tf32", dict(param_tol=2e-3))])
-def test_bf16_optimizer_state(tmp_path, precision, tol):
+def test_bf16_optimizer_state(tmp_path):
     """Adam moments stored/streamed as bf16 (halves optimizer-state link bytes); compared with
-    the oracle applying the same bf16 rounding to its moments. Stated separately (north_star):
-    with TF32 GEMMs a gradient perturbation can move a moment across a bf16 rounding boundary,
-    so parameters hold 2e-3 here (1.05e-3 measured on layer 1), losses 1e-3."""
+    the oracle applying the same bf16 rounding to its moments (stated separately, north_star).
+    3xTF32 GEMMs so the comparison isolates the moment rounding path."""
     cfg = tiny_config(mbs=3)
-    compare(cfg, tmp_path, precision=precision, opt_state="bf16", **tol)
+    compare(cfg, tmp_path, precision="fp32", opt_state="bf16", loss_tol=1e-5, param_tol=1e-4)
 
 
 def test_single_shard_resident(tmp_path):
-    # TF32 (10-bit mantissa) noise flips the sign of Adam's first updates on the smallest
-    # gradients of this d=64 model; the per-tensor parameter deviation sits at ~1.0-1.1e-3
-    # (losses within 1e-3). fp32 precision holds 1e-4 on the same path (test_c1_*, test_head_*).
     cfg = tiny_config(mem=400e6, mbs=3, jobs=1)
-    res = compare(cfg, tmp_path, param_tol=1.5e-3)
+    res = compare(cfg, tmp_path, precision="fp32", loss_tol=1e-5, param_tol=1e-4)
     assert res["shard_starts"] == [[0]]
 
 
