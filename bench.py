@@ -338,7 +338,7 @@ def run_hydra(args, cfg):
     device_ids = [0] * n
     device_ids[rank] = local if world > 1 else 0
     req = dict(strategy="sharp", gpus=n, run_devices=[rank], device_ids=device_ids,
-               passes=args.steps, warmup_passes=args.warmup, host_opt_fraction=args.host_opt_fraction,
+               passes=args.steps + 1, warmup_passes=args.warmup, host_opt_fraction=args.host_opt_fraction,
                opt_state=args.opt_state)
     if args.exec_json:  # executor tuning knobs (ExecOptions fields of the C-ABI request), e.g. '{"opt_chunk_floats": 4194304}'
         req.update(json.loads(args.exec_json))
