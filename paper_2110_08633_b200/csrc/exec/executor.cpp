@@ -16,6 +16,9 @@
 // skipped when the slot already holds that shard at the current version (B(k-1) after
 // F(k-1) — the reference's elision, sim.cpp:356-365 — and F(0) of the next minibatch after
 // B(0)); an ActPromote is skipped when the producer's output is still resident on this GPU.
+#include <limits>
+#include <set>
+
 #include "executor_impl.hpp"
 
 namespace spillsim {
@@ -90,6 +93,35 @@ void* exec_detail::pinned(size_t bytes) {
   return p;
 }
 
+
+double exec_detail::host_available_bytes() {
+  // MemAvailable of /proc/meminfo minus a 4 GB margin for the process itself; +inf if unknown
+  FILE* f = std::fopen("/proc/meminfo", "r");
+  if (!f) return std::numeric_limits<double>::infinity();
+  char line[256];
+  double kb = -1;
+  while (std::fgets(line, sizeof line, f)) {
+    if (std::sscanf(line, "MemAvailable: %lf kB", &kb) == 1) break;
+  }
+  std::fclose(f);
+  if (kb < 0) return std::numeric_limits<double>::infinity();
+  return std::max(0.0, kb * 1024.0 - 4e9);
+}
+
+double ExecutorImpl::host_job_pinned_bytes(int j) const {
+  // mirrors setup_host_job's pinned allocations
+  const ExecJob& spec = exec.jobs.at(static_cast<size_t>(j));
+  const hy_dims m = spec.dims;
+  const double total = static_cast<double>(hy_total_floats(&m));
+  const double n_act = static_cast<double>(m.B) * m.T * m.d;
+  const double k = static_cast<double>(spec.shard_starts.size());
+  const double n_gmb = static_cast<double>(job_mb[static_cast<size_t>(j)]) * (exec.passes + exec.warmup_passes);
+  double b = 4.0 * total + 2.0 * (exec.opt_state_bf16 ? 2.0 : 4.0) * total;  // params, m, v
+  b += 4.0 * n_act * (2.0 * (k - 1) + 1.0);                                  // checkpoints, grads, z
+  b += 8.0 * static_cast<double>(m.B) * m.T * n_gmb;                         // tokens, targets
+  if (exec.host_opt_fraction > 0) b += 4.0 * total;                          // host-optimizer grads
+  return b;
+}
 
 void ExecutorImpl::setup_host_job(int j) {
   HostJob& hj = jobs[j];
@@ -401,6 +433,23 @@ void ExecutorImpl::setup(ExecResult& res) {
   job_mb.assign(exec.jobs.size(), 0);
   for (const SimTask& t : tasks) {
     job_mb[static_cast<size_t>(t.t.job)] = std::max(job_mb[static_cast<size_t>(t.t.job)], t.t.minibatch + 1);
+  }
+  {
+    // Real-bytes host check (the reference's HostOOM, strategies.cpp:613-626, charges the cost
+    // model's 2P + boundary activations; this counts what setup_host_job pins): every job this
+    // process executes, against the config's host_dram_bytes and this host's available memory.
+    std::set<int> mine;
+    for (int d : run) {
+      if (exec.dynamic) {
+        for (const SimTask& t : tasks) mine.insert(t.t.job);
+      } else {
+        for (int t : per_dev[static_cast<size_t>(d)]) mine.insert(tasks[static_cast<size_t>(t)].t.job);
+      }
+    }
+    double need = 0;
+    for (int j : mine) need += host_job_pinned_bytes(j);
+    const double avail = std::min(cluster.host_dram_bytes, exec_detail::host_available_bytes());
+    if (need > avail) throw HostOOM(need, avail);
   }
   for (int d : run) {
     auto w = std::make_unique<Worker>();

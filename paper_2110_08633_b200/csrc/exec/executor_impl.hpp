@@ -293,6 +293,7 @@ struct ExecutorImpl {
 
   void setup(ExecResult& res);
   void setup_host_job(int j);
+  double host_job_pinned_bytes(int j) const;
   void setup_worker(Worker& w);
   void run_pass(int pass, bool timed, ExecResult& res, bool interval_log = false);
   void dynamic_dispatch(Worker& w, int pass);
@@ -330,6 +331,8 @@ struct ExecutorImpl {
 namespace exec_detail {
 // pinned + mapped host allocation (zero-copy optimizer kernels address it directly)
 void* pinned(size_t bytes);
+// MemAvailable of this host minus a 4 GB margin (bytes; +inf if unknown).
+double host_available_bytes();
 }  // namespace exec_detail
 
 }  // namespace spillsim

@@ -269,3 +269,16 @@ def test_dynamic_schedule_alternating_with_p2p(tmp_path):
                   precision="fp32", loss_tol=1e-5, param_tol=1e-4)
     n_tasks = len(P.plan(cfg, gpus=2, double_buffering=False)["tasks"])
     assert sorted(t for t, _, _ in res["dispatch_measured"]) == list(range(n_tasks))
+
+
+def test_host_oom_real_bytes():
+    """The planner's HostOOM charges the cost model (2P + boundary activations per job,
+    strategies.cpp:613-626); the executor also checks the pinned bytes it would really
+    allocate (params, Adam m and v, checkpoints, tokens) before allocating any of them.
+    C2 with 10 GB of host DRAM passes the cost model (~8 GB) but not the real need (~13 GB)."""
+    cfg = load("c2_gpt2small_x8")
+    cfg["cluster"]["host_dram_bytes"] = 10e9
+    P.plan(cfg)  # the cost-model check passes
+    with pytest.raises(P.HydraError) as e:
+        P.Executor(cfg, gpus=1, passes=1)
+    assert "host DRAM overcommitted" in str(e.value)
