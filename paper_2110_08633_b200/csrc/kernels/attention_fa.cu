@@ -14,9 +14,10 @@
 // Backward (FA2 split, deterministic: no atomics):
 //   attn_dkdv_kernel: one CTA per (batch, head, 128-key tile), thread = key row;
 //     S^T = K Q^T, dP^T = V dO^T, P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - Di);
-//     dV += P^T dO, dK += dS^T Q / 8   (accumulated in TMEM over the query tiles)
+//     dV += P^T dO, dK += dS^T Q   (accumulated in TMEM over the query tiles; the softmax
+//     scale 1/8 is applied once to dK at the end — exact, a power of two)
 //   attn_dq_kernel: one CTA per (batch, head, 128-query tile), thread = query row;
-//     S = Q K^T, dP = dO V^T, dS = P (dP - Di); dQ += dS K / 8 (TMEM)
+//     S = Q K^T, dP = dO V^T, dS = P (dP - Di); dQ += dS K (TMEM), dQ / 8 at the end
 //   Di = rowsum(dO * O) per (query, head) from a small warp-per-row kernel.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -92,6 +93,11 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
+// The same rounding (to nearest, ties away from zero, on the 10-bit TF32 mantissa) as one
+// integer add: the tensor core drops the low 13 bits the add has carried into. Finite inputs
+// only (softmax probabilities and dS values here).
+__device__ __forceinline__ float tf32_round_add(float x) { return __uint_as_float(__float_as_uint(x) + 0x1000u); }
+
 // Row r (of a K-major 128B-swizzled operand with k-block stride kb_bytes) <- 64 floats,
 // rounded to TF32 (nearest, ties away) — the tensor core would otherwise truncate them.
 __device__ __forceinline__ void store_row64(uint8_t* base, int r, int kb_bytes, const float (&x)[64]) {
@@ -146,173 +152,230 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
-// Forward, software-pipelined over 64-key tiles j (S, K, V double-buffered; P in TMEM):
-//   S(j+1) = Q K(j+1)^T is issued as soon as S(j) lands, so it runs under softmax(j);
-//   P(j) goes registers -> TMEM (tcgen05.st, TF32-rounded) and PV(j) = P(j) V(j) reads it as
-//   the MMA's A operand, running under the next tile's softmax; O lives in registers and
-//   takes PV(j-1) one iteration late (O = O * alpha(j-1) + PV(j-1)).
-// smem: Q 32 KB + K 2 x 16 KB + V 2 x 16 KB (two CTAs per SM); TMEM: S 2 x 64, P 64, PV 64.
-constexpr int kFwdSmem = 32768 + 2 * 16384 + 2 * 16384 + 256 + 1024;
+// Forward: a persistent, warp-specialised kernel. Work units are (batch, head, 128-query tile),
+// longest (most key tiles) first, dealt to the CTAs in snake order; each CTA streams the key
+// tiles of all its units through one pipeline, so the next unit's Q / K / V loads and its first
+// S = Q K^T overlap the current unit's last softmax and epilogue (a CTA per unit paid a cold
+// TMA + TMEM start per 2-8 tiles of work).
+//   warp 5 (one lane): TMA loads — Q of each unit (single buffer, reloaded once the unit's last
+//     S has been computed), K(g) / V(g) double-buffered over the CTA's global tile sequence g;
+//   warp 4 (one lane): tcgen05.mma issue — S(g+1) = Q K(g+1)^T ahead of softmax(g), then
+//     O += P(g) V(g) with P from TMEM once the softmax warps have stored it;
+//   warps 0-3 (thread = query row): online softmax in registers. The running max used by the
+//     exponentials is only raised when a row's max exceeds it by more than 2^8 (lazy rescale:
+//     O and l are multiplied in place then, warp-uniformly, after the previous PV has landed);
+//     P <= 2^8 stays well inside fp32 / TF32 range. Max and sum use four accumulators each.
+// smem: Q 32 KB + K 2 x 16 KB + V 2 x 16 KB (two CTAs per SM); TMEM: S 2 x 64, P 64, O 64.
+constexpr int kFwdSmem = 32768 + 2 * 16384 + 2 * 16384 + 128 + 1024;
+constexpr float kRescaleLog2 = 8.0f;
 
-__global__ void __launch_bounds__(128) attn_fwd_kernel(const __grid_constant__ CUtensorMap mq,
-                                                       const __grid_constant__ CUtensorMap mk,
-                                                       const __grid_constant__ CUtensorMap mv, int T, int H,
-                                                       float* __restrict__ out, float* __restrict__ lse2) {
+struct FwdUnits {
+  int nqt, BH, U, G;  // query tiles per (b, h), batch*heads, units, CTAs
+  // unit -> (bh, qt): longest tiles first
+  __device__ __forceinline__ void unit(int u, int& bh, int& qt) const {
+    qt = nqt - 1 - u / BH;
+    bh = u % BH;
+  }
+  // r-th unit of CTA c in snake order (-1 past the end)
+  __device__ __forceinline__ int nth(int c, int r) const {
+    const int u = r * G + ((r & 1) ? G - 1 - c : c);
+    return u < U ? u : -1;
+  }
+};
+
+__global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant__ CUtensorMap mq,
+                                                          const __grid_constant__ CUtensorMap mk,
+                                                          const __grid_constant__ CUtensorMap mv, int T, int H,
+                                                          int B, float* __restrict__ out, float* __restrict__ lse2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sQ = align1024(smem_raw);
   uint8_t* sK0 = sQ + 32768;
   uint8_t* sV0 = sK0 + 2 * 16384;
-  // barriers: 0 q, 1-2 k[2], 3-4 v[2], 5-6 s[2], 7 pv
+  // barriers: 0 q, 1-2 kfull, 3-4 vfull, 5-6 sdone, 7-8 pvdone, 9 pready (4 arrivals)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV0 + 2 * 16384);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 8);
-  const int tid = threadIdx.x;
-  const int nqt = (T + 127) / 128;
-  const int bh = blockIdx.x / nqt;
-  const int qt = nqt - 1 - blockIdx.x % nqt;  // longest (most keys) tiles first
-  const int b = bh / H, h = bh % H;
-  const int q0 = qt * 128, D = H * HD, row0 = b * T;
-  const int nkt = min((T + 63) / 64, (q0 + 128) / 64);
+  uint64_t *bq = bar, *bk = bar + 1, *bv = bar + 3, *bs = bar + 5, *bpv = bar + 7, *bp = bar + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  FwdUnits W;
+  W.nqt = (T + 127) / 128;
+  W.BH = B * H;
+  W.U = W.nqt * W.BH;
+  W.G = static_cast<int>(gridDim.x);
+  const int c = static_cast<int>(blockIdx.x);
+  const int D = H * HD;
+  auto nkt_of = [&](int qt) { return min((T + 63) / 64, (qt * 128 + 128) / 64); };
   if (tid == 0) {
     tma_prefetch_desc(&mq);
     tma_prefetch_desc(&mk);
     tma_prefetch_desc(&mv);
-    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 10; ++i) mbar_init(&bar[i], i == 9 ? 4 : 1);
     fence_barrier_init();
   }
-  if (tid < 32) tmem_alloc<256>(tslot);
+  if (warp == 0) tmem_alloc<256>(tslot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   pdl_wait_and_trigger();
   const uint32_t tbase = *tslot;
-  const uint32_t tP = tbase + 128, tPV = tbase + 192;
-  const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
-  auto load_k = [&](int j) {
-    uint8_t* dst = sK0 + (j & 1) * 16384;
-    mbar_expect_tx(&bar[1 + (j & 1)], 16384);
-    tma_load_2d(dst, &mk, &bar[1 + (j & 1)], D + h * HD, row0 + j * 64);
-    tma_load_2d(dst + 8192, &mk, &bar[1 + (j & 1)], D + h * HD + 32, row0 + j * 64);
-  };
-  auto load_v = [&](int j) {
-    uint8_t* dst = sV0 + (j & 1) * 16384;
-    mbar_expect_tx(&bar[3 + (j & 1)], 16384);
-    for (int kb = 0; kb < 2; ++kb)
-      for (int jn = 0; jn < 2; ++jn)
-        tma_load_2d(dst + kb * 8192 + jn * 4096, &mv, &bar[3 + (j & 1)], 2 * D + h * HD + 32 * jn, row0 + j * 64 + 32 * kb);
-  };
-  constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
-  constexpr uint32_t idPV = idesc_tf32(128, 64, false, true);
-  auto issue_s = [&](int j) {  // tid 0
-    mbar_wait(&bar[1 + (j & 1)], (j >> 1) & 1);
-    tc_fence_after();
-    const uint32_t tS = tbase + (j & 1) * 64;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sK0 + (j & 1) * 16384, kk, 8192), idS, kk > 0);
-    mma_commit(&bar[5 + (j & 1)]);
-  };
-  if (tid == 0) {
-    mbar_expect_tx(&bar[0], 32768);
-    tma_load_2d(sQ, &mq, &bar[0], h * HD, row0 + q0);
-    tma_load_2d(sQ + 16384, &mq, &bar[0], h * HD + 32, row0 + q0);
-    load_k(0);
-    load_v(0);
-    if (nkt > 1) {
-      load_k(1);
-      load_v(1);
-    }
-    mbar_wait(&bar[0], 0);
-    issue_s(0);
-  }
-  float o[64];
-#pragma unroll
-  for (int i = 0; i < 64; ++i) o[i] = 0.f;
-  float m_run = -FLT_MAX, l_run = 0.f, alpha_prev = 1.f;
-  const int q = q0 + tid;
-  for (int j = 0; j < nkt; ++j) {
-    const int k0 = j * 64;
-    mbar_wait(&bar[5 + (j & 1)], (j >> 1) & 1);  // S(j) landed (K(j) consumed)
-    tc_fence_after();
-    if (tid == 0) {
-      if (j + 2 < nkt) load_k(j + 2);  // into the buffer S(j) just released
-      if (j + 1 < nkt) issue_s(j + 1);
-    }
-    float s[64];
-    tmem_ld64(tbase + (j & 1) * 64 + lane_off, s);
-    float mx = m_run;
-    const bool full = k0 + 63 <= q0;  // every key of the tile visible to every row (CTA-uniform)
-    if (full) {
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        s[i] *= kScaleLog2;
-        mx = fmaxf(mx, s[i]);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        s[i] = (k0 + i <= q) ? s[i] * kScaleLog2 : -FLT_MAX;
-        mx = fmaxf(mx, s[i]);
+  const uint32_t tP = tbase + 128, tO = tbase + 192;
+  if (warp == 5) {
+    if (lane_id() == 0) {  // loader
+      int g = 0;
+      for (int r = 0;; ++r) {
+        const int u = W.nth(c, r);
+        if (u < 0) break;
+        int bh, qt;
+        W.unit(u, bh, qt);
+        const int b = bh / H, h = bh % H, row0 = b * T;
+        if (g > 0) mbar_wait(&bs[(g - 1) & 1], ((g - 1) >> 1) & 1);  // previous unit's last S: Q free
+        mbar_expect_tx(bq, 32768);
+        tma_load_2d(sQ, &mq, bq, h * HD, row0 + qt * 128);
+        tma_load_2d(sQ + 16384, &mq, bq, h * HD + 32, row0 + qt * 128);
+        const int nkt = nkt_of(qt);
+        for (int j = 0; j < nkt; ++j, ++g) {
+          const int s = g & 1;
+          if (g >= 2) mbar_wait(&bs[s], ((g - 2) >> 1) & 1);  // S(g-2) read K(g-2)
+          uint8_t* dk = sK0 + s * 16384;
+          mbar_expect_tx(&bk[s], 16384);
+          tma_load_2d(dk, &mk, &bk[s], D + h * HD, row0 + j * 64);
+          tma_load_2d(dk + 8192, &mk, &bk[s], D + h * HD + 32, row0 + j * 64);
+          if (g >= 2) mbar_wait(&bpv[s], ((g - 2) >> 1) & 1);  // PV(g-2) read V(g-2)
+          uint8_t* dv = sV0 + s * 16384;
+          mbar_expect_tx(&bv[s], 16384);
+          for (int kb = 0; kb < 2; ++kb)
+            for (int jn = 0; jn < 2; ++jn)
+              tma_load_2d(dv + kb * 8192 + jn * 4096, &mv, &bv[s], 2 * D + h * HD + 32 * jn, row0 + j * 64 + 32 * kb);
+        }
       }
     }
-    const float alpha = fast_exp2(m_run - mx);
-    float sum = 0.f;
-    if (full) {
+    __syncwarp();
+  } else if (warp == 4) {
+    if (lane_id() == 0) {  // MMA issuer
+      constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
+      constexpr uint32_t idPV = idesc_tf32(128, 64, false, true);
+      auto issue_s = [&](int g) {
+        const int s = g & 1;
+        mbar_wait(&bk[s], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tS = tbase + s * 64;
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        s[i] = fast_exp2(s[i] - mx);
-        sum += s[i];
-        s[i] = tf32_rna(s[i]);
+        for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sK0 + s * 16384, kk, 8192), idS, kk > 0);
+        mma_commit(&bs[s]);
+      };
+      int g = 0;
+      int r = 0;
+      int u = W.nth(c, 0);
+      if (u >= 0) {
+        mbar_wait(bq, 0);
+        issue_s(0);
       }
-    } else {
+      while (u >= 0) {
+        int bh, qt;
+        W.unit(u, bh, qt);
+        const int nkt = nkt_of(qt);
+        const int un = W.nth(c, r + 1);
+        for (int j = 0; j < nkt; ++j, ++g) {
+          const int s = g & 1;
+          if (j + 1 < nkt) issue_s(g + 1);
+          mbar_wait(bp, g & 1);  // P(g) stored (and O rescaled) by the softmax warps
+          mbar_wait(&bv[s], (g >> 1) & 1);
+          tc_fence_after();
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        s[i] = (k0 + i <= q) ? fast_exp2(s[i] - mx) : 0.f;
-        sum += s[i];
-        s[i] = tf32_rna(s[i]);
+          for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tO, tP + kk * 8, desc_mn(sV0 + s * 16384, kk), idPV, (j | kk) > 0);
+          mma_commit(&bpv[s]);
+          if (j + 1 == nkt && un >= 0) {  // next unit's first S once its Q has landed
+            mbar_wait(bq, (r + 1) & 1);
+            issue_s(g + 1);
+          }
+        }
+        ++r;
+        u = un;
       }
     }
-    l_run = l_run * alpha + sum;
-    m_run = mx;
-    if (j > 0) {  // PV(j-1) done: fold it into O, its P and V(j-1) buffers are free
-      mbar_wait(&bar[7], (j - 1) & 1);
+    __syncwarp();
+  } else {
+    const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
+    int g = 0;
+    for (int r = 0;; ++r) {
+      const int u = W.nth(c, r);
+      if (u < 0) break;
+      int bh, qt;
+      W.unit(u, bh, qt);
+      const int b = bh / H, h = bh % H, row0 = b * T, q0 = qt * 128;
+      const int nkt = nkt_of(qt);
+      const int q = q0 + tid;
+      float m_used = -FLT_MAX, l_run = 0.f;  // m_used: scaled (log2-domain) max the exponentials use
+      for (int j = 0; j < nkt; ++j, ++g) {
+        const int k0 = j * 64, s_ = g & 1;
+        mbar_wait(&bs[s_], (g >> 1) & 1);
+        tc_fence_after();
+        float s[64];
+        tmem_ld64(tbase + s_ * 64 + lane_off, s);
+        if (k0 + 63 > q0) {  // diagonal tile: mask keys past the row (CTA-uniform test)
+#pragma unroll
+          for (int i = 0; i < 64; ++i) s[i] = (k0 + i <= q) ? s[i] : -FLT_MAX;
+        }
+        float mx4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+        for (int i = 4; i < 64; i += 4) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) mx4[v] = fmaxf(mx4[v], s[i + v]);
+        }
+        const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * kScaleLog2;
+        float alpha = 1.f;
+        if (mx > m_used + kRescaleLog2 || j == 0) {
+          alpha = fast_exp2(m_used - mx);  // 0 on the first tile (m_used = -FLT_MAX)
+          m_used = mx;
+        }
+        float sum4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < 64; i += 4) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const float p = fast_exp2(fmaf(s[i + v], kScaleLog2, -m_used));  // masked: 2^-huge = 0
+            sum4[v] += p;
+            s[i + v] = tf32_round_add(p);
+          }
+        }
+        l_run = l_run * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+        if (j > 0) {  // PV(g-1) landed: P free, O final up to tile j-1
+          mbar_wait(&bpv[(g - 1) & 1], ((g - 1) >> 1) & 1);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {  // lazy rescale of this warp's O rows
+            float o[64];
+            tmem_ld64(tO + lane_off, o);
+#pragma unroll
+            for (int i = 0; i < 64; ++i) o[i] *= alpha;
+            tmem_st_x32(tO + lane_off, o);
+            tmem_st_x32(tO + lane_off + 32, o + 32);
+          }
+        }
+        tmem_st_x32(tP + lane_off, s);
+        tmem_st_x32(tP + lane_off + 32, s + 32);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(bp);
+      }
+      // unit epilogue: O / l once the last PV has landed (the next unit's first PV, which
+      // overwrites O, is only issued after these rows have stored its P, i.e. after this read)
+      mbar_wait(&bpv[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
-      if (tid == 0 && j + 1 < nkt) load_v(j + 1);
-      float pv[64];
-      tmem_ld64(tPV + lane_off, pv);
+      float o[64];
+      tmem_ld64(tO + lane_off, o);
+      if (q < T) {
+        const float inv = 1.f / l_run;
+        float4* dst = reinterpret_cast<float4*>(out + static_cast<long>(row0 + q) * D + h * HD);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) o[i] = o[i] * alpha_prev + pv[i];
+        for (int i = 0; i < 16; ++i)
+          dst[i] = make_float4(o[4 * i] * inv, o[4 * i + 1] * inv, o[4 * i + 2] * inv, o[4 * i + 3] * inv);
+        lse2[static_cast<long>(bh) * T + q] = m_used + log2f(l_run);
+      }
     }
-    tmem_st_x32(tP + lane_off, s);
-    tmem_st_x32(tP + lane_off + 32, s + 32);
-    tmem_st_wait();
-    tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc_fence_after();
-      mbar_wait(&bar[3 + (j & 1)], (j >> 1) & 1);
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tPV, tP + kk * 8, desc_mn(sV0 + (j & 1) * 16384, kk), idPV, kk > 0);
-      mma_commit(&bar[7]);
-    }
-    alpha_prev = alpha;
-  }
-  mbar_wait(&bar[7], (nkt - 1) & 1);
-  tc_fence_after();
-  {
-    float pv[64];
-    tmem_ld64(tPV + lane_off, pv);
-#pragma unroll
-    for (int i = 0; i < 64; ++i) o[i] = o[i] * alpha_prev + pv[i];
-  }
-  if (q < T) {
-    const float inv = 1.f / l_run;
-    float4* dst = reinterpret_cast<float4*>(out + static_cast<long>(row0 + q) * D + h * HD);
-#pragma unroll
-    for (int c = 0; c < 16; ++c) dst[c] = make_float4(o[4 * c] * inv, o[4 * c + 1] * inv, o[4 * c + 2] * inv, o[4 * c + 3] * inv);
-    lse2[static_cast<long>(bh) * T + q] = m_run + log2f(l_run);
   }
   tc_fence_before();
   __syncthreads();
-  if (tid < 32) {
+  if (warp == 0) {
     tc_fence_after();
     tmem_dealloc<256>(*tslot);
   }
@@ -347,7 +410,7 @@ __global__ void attn_di_kernel(long n, int T, int H, const float* __restrict__ o
 // tiles i (from the diagonal): warp 4 (one lane) streams Q / dO tiles (double-buffered, both
 // majors) and issues S^T(i) = K Q(i)^T, dP^T(i) = V dO(i)^T into double-buffered TMEM as soon
 // as they land, then dV += P^T(i) dO(i) and dK += dS^T(i) Q(i) with P^T, dS^T read from TMEM;
-// warps 0-3 (thread = key row) compute P^T = exp2(S^T c - lse2) and dS^T = P^T (dP^T - Di) / 8.
+// warps 0-3 (thread = key row) compute P^T = exp2(S^T c - lse2) and dS^T = P^T (dP^T - Di).
 // smem: K, V 32 KB each + 2 stages x (Q k, Q mn, dO k, dO mn) 64 KB = 192 KB;
 // TMEM: S^T 2 x 64, dP^T 2 x 64, P^T 64, dS^T 64, dV 64, dK 64 columns.
 constexpr int kDkvSmem = 32768 * 2 + 2 * 65536 + 256 + 1024 + 1024;  // + lse / Di staging
@@ -471,8 +534,8 @@ __global__ void __launch_bounds__(160) attn_dkdv_kernel(
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           const float p = fast_exp2(fmaf(s[c], kScaleLog2, -ld[c]));
-          s[c] = tf32_rna(p);
-          dp[c] = tf32_rna(p * (dp[c] - ld[64 + c]) * 0.125f);
+          s[c] = tf32_round_add(p);
+          dp[c] = tf32_round_add(p * (dp[c] - ld[64 + c]));  // the 1/8 of dS is applied to dK
         }
       } else {
 #pragma unroll
@@ -480,8 +543,8 @@ __global__ void __launch_bounds__(160) attn_dkdv_kernel(
           const int q = q0 + c;
           const bool valid = q >= key && q < T;
           const float p = valid ? fast_exp2(fmaf(s[c], kScaleLog2, -ld[c])) : 0.f;
-          s[c] = tf32_rna(p);
-          dp[c] = valid ? tf32_rna(p * (dp[c] - ld[64 + c]) * 0.125f) : 0.f;
+          s[c] = tf32_round_add(p);
+          dp[c] = valid ? tf32_round_add(p * (dp[c] - ld[64 + c])) : 0.f;
         }
       }
       if (i >= 1) mbar_wait(&bar[6 + ((i - 1) & 1)], ((i - 1) >> 1) & 1);  // P^T, dS^T(i-1) consumed
@@ -504,7 +567,7 @@ __global__ void __launch_bounds__(160) attn_dkdv_kernel(
       float4* gv = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + 2 * D + h * HD);
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        gk[c] = make_float4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]);
+        gk[c] = make_float4(0.125f * dk[4 * c], 0.125f * dk[4 * c + 1], 0.125f * dk[4 * c + 2], 0.125f * dk[4 * c + 3]);
         gv[c] = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
       }
     }
@@ -521,7 +584,7 @@ __global__ void __launch_bounds__(160) attn_dkdv_kernel(
 //   warp 4 (one lane) loads K/V tiles (double-buffered) and issues S(j) = Q K(j)^T and
 //   dP(j) = dO V(j)^T into TMEM (double-buffered) as soon as their tiles land, then
 //   dQ += dS(j) K(j) with dS read from TMEM (written there by the compute warps);
-//   warps 0-3 (thread = query row) turn S, dP into dS = P (dP - Di) / 8 while the tensor core
+//   warps 0-3 (thread = query row) turn S, dP into dS = P (dP - Di) while the tensor core
 //   works on the neighbouring tiles.
 // smem: Q, dO 32 KB each + 2 stages x (K K-major, V K-major, K MN-major) 48 KB = 160 KB;
 // TMEM: S 2 x 64, dP 2 x 64, dS 2 x 64, dQ 64 columns.
@@ -630,14 +693,14 @@ __global__ void __launch_bounds__(160) attn_dq_kernel(
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           const float p = fast_exp2(fmaf(s[c], kScaleLog2, -my_lse));
-          s[c] = tf32_rna(p * (dp[c] - my_di) * 0.125f);
+          s[c] = tf32_round_add(p * (dp[c] - my_di));  // the 1/8 of dS is applied to dQ
         }
       } else {
 #pragma unroll
         for (int c = 0; c < 64; ++c) {
           const bool valid = k0 + c <= q;
           const float p = valid ? fast_exp2(fmaf(s[c], kScaleLog2, -my_lse)) : 0.f;
-          s[c] = valid ? tf32_rna(p * (dp[c] - my_di) * 0.125f) : 0.f;
+          s[c] = valid ? tf32_round_add(p * (dp[c] - my_di)) : 0.f;
         }
       }
       if (j >= 2) {  // dQ(j-2) has finished reading this dS buffer
@@ -658,7 +721,8 @@ __global__ void __launch_bounds__(160) attn_dq_kernel(
     if (q < T) {
       float4* g = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + q) * 3 * D + h * HD);
 #pragma unroll
-      for (int c = 0; c < 16; ++c) g[c] = make_float4(dq[4 * c], dq[4 * c + 1], dq[4 * c + 2], dq[4 * c + 3]);
+      for (int c = 0; c < 16; ++c)
+        g[c] = make_float4(0.125f * dq[4 * c], 0.125f * dq[4 * c + 1], 0.125f * dq[4 * c + 2], 0.125f * dq[4 * c + 3]);
     }
   }
   tc_fence_before();
@@ -667,6 +731,13 @@ __global__ void __launch_bounds__(160) attn_dq_kernel(
     tc_fence_after();
     tmem_dealloc<512>(*tslot);
   }
+}
+
+int attn_sm_count() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+  return v > 0 ? v : 148;
 }
 
 }  // namespace
@@ -683,9 +754,10 @@ cudaError_t attention_fwd_fa(cudaStream_t st, int B, int T, int H, const float* 
     const cudaError_t e = ensure_smem_limit(attn_fwd_kernel, kFwdSmem);
     if (e != cudaSuccess) return e;
   }
-  const int grid = B * H * ((T + 127) / 128);
+  const int units = B * H * ((T + 127) / 128);
+  const int grid = std::min(units, 2 * attn_sm_count());  // persistent: two CTAs per SM
   count_launch();
-  return launch_pdl(attn_fwd_kernel, dim3(grid), dim3(128), kFwdSmem, st, mq, mk, mv, T, H, out, lse2);
+  return launch_pdl(attn_fwd_kernel, dim3(grid), dim3(192), kFwdSmem, st, mq, mk, mv, T, H, B, out, lse2);
 }
 
 cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* qkv, const float* out,
