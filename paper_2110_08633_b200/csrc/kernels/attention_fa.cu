@@ -120,6 +120,17 @@ __device__ __forceinline__ void tmem_ld64(uint32_t taddr, float (&x)[64]) {
   }
 }
 
+// Non-blocking mbarrier phase test (the MMA warp's event loop polls several barriers).
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
 __device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // TMEM <- registers: 32 lanes x 32 columns (thread t of the warp writes its lane's 32 values).
@@ -159,8 +170,9 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
 // TMA + TMEM start per 2-8 tiles of work).
 //   warp 5 (one lane): TMA loads — Q of each unit (single buffer, reloaded once the unit's last
 //     S has been computed), K(g) / V(g) double-buffered over the CTA's global tile sequence g;
-//   warp 4 (one lane): tcgen05.mma issue — S(g+1) = Q K(g+1)^T ahead of softmax(g), then
-//     O += P(g) V(g) with P from TMEM once the softmax warps have stored it;
+//   warp 4 (one lane): tcgen05.mma issue from an event loop — S(g) = Q K(g)^T as soon as its
+//     buffer is read out (up to two tiles ahead of the softmax), O += P(g) V(g) with P from
+//     TMEM once the softmax warps have stored it;
 //   warps 0-3 (thread = query row): online softmax in registers. The running max used by the
 //     exponentials is only raised when a row's max exceeds it by more than 2^8 (lazy rescale:
 //     O and l are multiplied in place then, warp-uniformly, after the previous PV has landed);
@@ -191,9 +203,10 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
   uint8_t* sQ = align1024(smem_raw);
   uint8_t* sK0 = sQ + 32768;
   uint8_t* sV0 = sK0 + 2 * 16384;
-  // barriers: 0 q, 1-2 kfull, 3-4 vfull, 5-6 sdone, 7-8 pvdone, 9 pready (4 arrivals)
+  // barriers: 0 q, 1-2 kfull, 3-4 vfull, 5-6 sdone, 7-8 pvdone, 9 pready (4 arrivals),
+  // 10-11 sfree (4 arrivals: the softmax warps have read S out of that buffer)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sV0 + 2 * 16384);
-  uint64_t *bq = bar, *bk = bar + 1, *bv = bar + 3, *bs = bar + 5, *bpv = bar + 7, *bp = bar + 9;
+  uint64_t *bq = bar, *bk = bar + 1, *bv = bar + 3, *bs = bar + 5, *bpv = bar + 7, *bp = bar + 9, *bsf = bar + 10;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 12);
   const int tid = threadIdx.x, warp = tid >> 5;
   FwdUnits W;
@@ -208,7 +221,7 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
     tma_prefetch_desc(&mq);
     tma_prefetch_desc(&mk);
     tma_prefetch_desc(&mv);
-    for (int i = 0; i < 10; ++i) mbar_init(&bar[i], i == 9 ? 4 : 1);
+    for (int i = 0; i < 12; ++i) mbar_init(&bar[i], i >= 9 ? 4 : 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<256>(tslot);
@@ -250,46 +263,69 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
     }
     __syncwarp();
   } else if (warp == 4) {
-    if (lane_id() == 0) {  // MMA issuer
+    if (lane_id() == 0) {  // MMA issuer: an event loop over two cursors, S ahead of PV
       constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
       constexpr uint32_t idPV = idesc_tf32(128, 64, false, true);
-      auto issue_s = [&](int g) {
-        const int s = g & 1;
-        mbar_wait(&bk[s], (g >> 1) & 1);
-        tc_fence_after();
-        const uint32_t tS = tbase + s * 64;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sK0 + s * 16384, kk, 8192), idS, kk > 0);
-        mma_commit(&bs[s]);
+      // cursor over this CTA's tile sequence: global tile g, unit ordinal r, tile j of nkt
+      struct Cur {
+        int g, r, j, nkt;
       };
-      int g = 0;
-      int r = 0;
-      int u = W.nth(c, 0);
-      if (u >= 0) {
-        mbar_wait(bq, 0);
-        issue_s(0);
-      }
-      while (u >= 0) {
+      auto start = [&](Cur& x) {
+        x.g = 0;
+        x.r = 0;
+        x.j = 0;
+        const int u = W.nth(c, 0);
         int bh, qt;
-        W.unit(u, bh, qt);
-        const int nkt = nkt_of(qt);
-        const int un = W.nth(c, r + 1);
-        for (int j = 0; j < nkt; ++j, ++g) {
-          const int s = g & 1;
-          if (j + 1 < nkt) issue_s(g + 1);
-          mbar_wait(bp, g & 1);  // P(g) stored (and O rescaled) by the softmax warps
-          mbar_wait(&bv[s], (g >> 1) & 1);
-          tc_fence_after();
+        if (u >= 0) W.unit(u, bh, qt);
+        x.nkt = u >= 0 ? nkt_of(qt) : 0;
+      };
+      auto advance = [&](Cur& x) {
+        ++x.g;
+        if (++x.j == x.nkt) {
+          x.j = 0;
+          ++x.r;
+          const int u = W.nth(c, x.r);
+          int bh, qt;
+          if (u >= 0) W.unit(u, bh, qt);
+          x.nkt = u >= 0 ? nkt_of(qt) : 0;
+        }
+      };
+      Cur cs, cp;
+      start(cs);
+      start(cp);
+      // S(g) = Q K(g)^T may run two tiles ahead of the softmax: it needs K(g) and its unit's Q
+      // landed and the softmax warps to have read S(g-2) out of the buffer (sfree), so it is
+      // issued while softmax(g-1) still runs, ahead of PV(g-1) in the tensor pipe when it can be.
+      // PV(g) needs P(g) stored (pready) and V(g) landed.
+      while (cp.nkt > 0) {
+        bool progressed = false;
+        if (cs.nkt > 0) {
+          const int g = cs.g, sb = g & 1;
+          if ((g < 2 || mbar_test(&bsf[sb], ((g - 2) >> 1) & 1)) && mbar_test(bq, cs.r & 1) &&
+              mbar_test(&bk[sb], (g >> 1) & 1)) {
+            tc_fence_after();
+            const uint32_t tS = tbase + sb * 64;
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tO, tP + kk * 8, desc_mn(sV0 + s * 16384, kk), idPV, (j | kk) > 0);
-          mma_commit(&bpv[s]);
-          if (j + 1 == nkt && un >= 0) {  // next unit's first S once its Q has landed
-            mbar_wait(bq, (r + 1) & 1);
-            issue_s(g + 1);
+            for (int kk = 0; kk < 8; ++kk)
+              mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sK0 + sb * 16384, kk, 8192), idS, kk > 0);
+            mma_commit(&bs[sb]);
+            advance(cs);
+            progressed = true;
           }
         }
-        ++r;
-        u = un;
+        {
+          const int g = cp.g, sb = g & 1;
+          if (cp.g < cs.g && mbar_test(bp, g & 1) && mbar_test(&bv[sb], (g >> 1) & 1)) {
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk)
+              mma_tf32_ts(tO, tP + kk * 8, desc_mn(sV0 + sb * 16384, kk), idPV, (cp.j | kk) > 0);
+            mma_commit(&bpv[sb]);
+            advance(cp);
+            progressed = true;
+          }
+        }
+        if (!progressed) __nanosleep(20);
       }
     }
     __syncwarp();
@@ -311,6 +347,9 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
         tc_fence_after();
         float s[64];
         tmem_ld64(tbase + s_ * 64 + lane_off, s);
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&bsf[s_]);  // S buffer free for S(g+2)
         if (k0 + 63 > q0) {  // diagonal tile: mask keys past the row (CTA-uniform test)
 #pragma unroll
           for (int i = 0; i < 64; ++i) s[i] = (k0 + i <= q) ? s[i] : -FLT_MAX;
