@@ -1,6 +1,7 @@
 """Execute the per-device shares of a G-GPU SHARP plan one after another on ONE B200.
 
 python tools/run_shares.py CONFIG.json G [devices,comma,separated|all] ['{"opt_state": "bf16"}']
+   extra keys also: "strategy" ("sharp" | "task-parallel"), "mem_bytes" (override every device's cap)
 
 With double buffering a job never leaves the device it first lands on, so the
 G devices of a plan share nothing but host DRAM / PCIe-switch bandwidth: device r's share
@@ -22,8 +23,13 @@ cfg_path, G = sys.argv[1], int(sys.argv[2])
 devs = sys.argv[3] if len(sys.argv) > 3 else "all"
 extra = json.loads(sys.argv[4]) if len(sys.argv) > 4 else {}
 warm = int(extra.pop("warmup_passes", 1))
+strategy = extra.pop("strategy", "sharp")
 cfg = json.load(open(cfg_path))
-plan = P.plan(cfg, gpus=G)
+if "mem_bytes" in extra:  # e.g. the task-parallel comparison leg, run uncapped
+    mem = float(extra.pop("mem_bytes"))
+    for d in cfg["cluster"]["devices"]:
+        d["mem_bytes"] = mem
+plan = P.plan(cfg, strategy=strategy, gpus=G)
 devices = list(range(G)) if devs == "all" else [int(x) for x in devs.split(",")]
 shares = []
 for r in devices:
@@ -32,7 +38,7 @@ for r in devices:
     if not mine:
         continue
     t0 = time.time()
-    ex = P.Executor(cfg, strategy="sharp", gpus=G, run_devices=[r], device_ids=[0] * G, passes=1,
+    ex = P.Executor(cfg, strategy=strategy, gpus=G, run_devices=[r], device_ids=[0] * G, passes=1,
                     warmup_passes=warm, **extra)
     setup = time.time() - t0
     if warm:
@@ -41,7 +47,7 @@ for r in devices:
     ex.close()
     st = res["stats"]
     sec = res["pass_seconds"][0]
-    line = {"config": os.path.basename(cfg_path), "G": G, "device": r, "jobs": jobs, "tasks": len(mine),
+    line = {"config": os.path.basename(cfg_path), "strategy": strategy, "G": G, "device": r, "jobs": jobs, "tasks": len(mine),
             "samples": res["samples_per_pass"], "makespan_s": round(sec, 3),
             "samples_per_s": round(res["samples_per_pass"] / sec, 2),
             "h2d_GB": round(st["h2d_bytes_per_pass"] / 1e9, 2), "d2h_GB": round(st["d2h_bytes_per_pass"] / 1e9, 2),
@@ -52,7 +58,7 @@ for r in devices:
 if shares:
     total = sum(s["samples"] for s in shares)
     mk = max(s["makespan_s"] for s in shares)
-    print(json.dumps({"summary": True, "config": os.path.basename(cfg_path), "G": G,
+    print(json.dumps({"summary": True, "config": os.path.basename(cfg_path), "strategy": strategy, "G": G,
                       "devices_measured": [s["device"] for s in shares], "samples": total,
                       "emulated_makespan_s": mk, "emulated_samples_per_s": round(total / mk, 2),
                       "sum_of_share_makespans_s": round(sum(s["makespan_s"] for s in shares), 3),
