@@ -94,9 +94,6 @@ long hy_kernel_launches(void);
  * split ("fp32", ~fp32 accuracy), 0 plain TF32; splitk_ws (device, may be NULL) lets
  * low-occupancy GEMMs split K. */
 int hy_gemm_config(int precision_fp32, float* splitk_ws, long splitk_floats);
-/* Diagnostics / tests: 0 = two-way split-K GEMMs reduce in a separate kernel instead of in
- * the CTA-pair kernel's epilogue (bit-identical results either way). Per host thread. */
-int hy_gemm_splitk_fixup(int on);
 
 /* C[M,N] = beta*C + op(A) op(B)^T (+bias[N]) (+R[M,N]) with tcgen05 kind::tf32.
  * a_mn=0: A is [M][lda] (K contiguous); a_mn=1: A is [K][lda] (M contiguous). Same for B

@@ -28,7 +28,6 @@ _SIGS = {
     "hy_kernel_launches": (ctypes.c_long, []),
     "hy_host_launch_us": (ctypes.c_double, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                             ctypes.c_void_p, ctypes.c_void_p]),
-    "hy_gemm_splitk_fixup": (ctypes.c_int, [ctypes.c_int]),
     "hy_gemm_config": (ctypes.c_int, [ctypes.c_int, ctypes.c_void_p, ctypes.c_long]),
     "hy_gemm": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,
                                ctypes.c_int, ctypes.c_void_p, ctypes.c_long, ctypes.c_int, ctypes.c_void_p, ctypes.c_long,

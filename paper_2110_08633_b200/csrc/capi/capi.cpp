@@ -160,11 +160,6 @@ double hy_host_launch_us(void* stream, int kind, int n, float* a, float* b, floa
   return std::chrono::duration<double, std::micro>(t1 - t0).count() / n;
 }
 
-int hy_gemm_splitk_fixup(int on) {
-  hy::gemm_set_splitk_fixup(on != 0);
-  return HY_OK;
-}
-
 int hy_gemm_config(int precision_fp32, float* splitk_ws, long splitk_floats) {
   hy::gemm_set_precision_fp32(precision_fp32 != 0);
   hy::gemm_set_splitk_workspace(splitk_ws, splitk_floats);

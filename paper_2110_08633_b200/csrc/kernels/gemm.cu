@@ -25,24 +25,6 @@ constexpr int BK = 32;
 thread_local float* t_splitk_ws = nullptr;
 thread_local bool t_prec3 = false;
 thread_local long t_splitk_floats = 0;
-// the in-kernel split-K's tile flags live in the last kFlagWords words of the workspace
-constexpr long kFlagWords = 1024;
-thread_local unsigned* t_flags_zeroed = nullptr;
-thread_local bool t_fixup = true;
-// share of K for slice 0 of an in-kernel two-way split: its main loop + partial store finish
-// before slice 1's main loop, so slice 1's epilogue does not wait
-constexpr double kSlice0Frac = 0.44;  // in-kernel two-way split-K reduce (off: separate reduce kernel)
-
-// floats of the workspace the partials may use (the flags take the tail)
-long splitk_capacity() { return t_splitk_floats > kFlagWords ? t_splitk_floats - kFlagWords : 0; }
-
-bool pair_path_enabled() {  // mirrors use_pairs() of gemm_kernels.cuh (HY_GEMM_PAIR=0: one-CTA tiles)
-  static const bool on = [] {
-    const char* e = std::getenv("HY_GEMM_PAIR");
-    return !e || std::atoi(e) != 0;
-  }();
-  return on;
-}
 
 // C = alpha * sum_s part[s] + beta * C   (fixed summation order: deterministic). Rows over
 // grid.y (grid-stride), columns over grid.x, float4 when N and ldc allow; PDL-chained behind the
@@ -127,18 +109,9 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
     const char* v = std::getenv("HY_GEMM_SPLIT");
     return v ? std::atoi(v) : 0;
   }();
-  // partial slices the workspace holds; a two-way split that reduces in-kernel (CTA-pair
-  // kernel, alpha 1) stores one partial instead of two
-  const long cap = splitk_capacity() / (static_cast<long>(M) * N);
-  const long pair_tiles = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + 127) / 128);
-  const bool fixup_ok = t_fixup && e.alpha == 1.f && M > BM && !t_prec3 && pair_path_enabled() && 2 * pair_tiles <= kFlagWords &&
-                        cap >= 1;
-  auto fit = [&](long s) {  // largest usable split <= s
-    if (s >= 2 && cap < 2 && fixup_ok) return 2L;
-    return std::min(s, cap);
-  };
   if (plain && t_splitk_ws && tiles * 2 <= sm_count_host() && kb_all >= 32) {
-    split = static_cast<int>(fit(std::min<long>(sm_count_host() / tiles, kb_all / 16)));
+    split = static_cast<int>(std::min<long>(sm_count_host() / tiles, kb_all / 16));
+    split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
   // Long-K GEMMs whose 256-wide CTA-pair tiles cover under half the pairs (the weight gradients,
   // K = tokens): split K so 256-wide tiles fill the GPU (BN 256 halves the operand traffic per
@@ -149,12 +122,14 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   }();
   const long tiles256 = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
   const long pairs = sm_count_host() / 2;
-  if (split256 && split <= 1 && plain && t_splitk_ws && !t_prec3 && M > BM && N > 128 && kb_all >= 64 &&
+  if (split256 && split == 1 && plain && t_splitk_ws && !t_prec3 && M > BM && N > 128 && kb_all >= 64 &&
       tiles256 * 2 <= pairs) {
-    split = static_cast<int>(fit(std::min<long>(pairs / tiles256, kb_all / 32)));
+    split = static_cast<int>(std::min<long>(pairs / tiles256, kb_all / 32));
+    split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
-  if (forced_split >= 2 && plain && t_splitk_ws) split = static_cast<int>(fit(forced_split));
-  if (split < 1) split = 1;
+  if (forced_split >= 2 && plain && t_splitk_ws) {
+    split = static_cast<int>(std::min<long>(forced_split, t_splitk_floats / (static_cast<long>(M) * N)));
+  }
   if (split >= 2) {
     bat.nb1 = split;
     bat.causal = kSplitK;
@@ -162,26 +137,6 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
     GemmEpilogue pe;
     pe.C = t_splitk_ws;
     pe.ldc = N;
-    // Two-way splits on the CTA-pair kernel reduce in-kernel (GemmBatch::flags): slice 1's
-    // epilogue adds slice 0's partial — no second launch, one partial instead of two.
-    if (split == 2 && fixup_ok) {
-      unsigned* flags = reinterpret_cast<unsigned*>(t_splitk_ws + (t_splitk_floats - kFlagWords));
-      if (t_flags_zeroed != flags) {  // once per workspace: consumers return every flag to 0
-        const cudaError_t z = cudaMemsetAsync(flags, 0, sizeof(unsigned) * kFlagWords, stream);
-        if (z != cudaSuccess) return z;
-        t_flags_zeroed = flags;
-      }
-      bat.flags = flags;
-      static const double frac = [] {  // diagnostics: HY_GEMM_SLICE0=f overrides slice 0's share of K
-        const char* v = std::getenv("HY_GEMM_SLICE0");
-        return v ? std::atof(v) : kSlice0Frac;
-      }();
-      bat.kb_split = std::max(1, static_cast<int>(kb_all * frac));
-      bat.fin_C = e.C;
-      bat.fin_ldc = e.ldc;
-      bat.fin_beta = e.beta;
-      return dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, pe, bat);
-    }
     const cudaError_t r = dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, pe, bat);
     if (r != cudaSuccess) return r;
     const bool vec = (N % 4 == 0) && (e.ldc % 4 == 0) && (reinterpret_cast<uintptr_t>(e.C) % 16 == 0);
@@ -196,8 +151,6 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   }
   return dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
 }
-
-void gemm_set_splitk_fixup(bool on) { t_fixup = on; }
 
 void gemm_set_splitk_workspace(float* ws, long floats) {
   t_splitk_ws = ws;

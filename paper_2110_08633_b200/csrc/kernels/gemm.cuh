@@ -41,18 +41,6 @@ struct GemmBatch {
   // set by the launcher: TMA dimension order {inner, b2, outer, b1} when b2's stride is
   // smaller than the row stride (e.g. heads interleaved inside a row)
   int a_perm = 0, b_perm = 0;
-  // In-kernel two-way split-K (CTA-pair kernel, kSplitK with nb1 == 2, alpha 1): slice 0
-  // stores its partial (C + 0) and counts its stored 32-column chunks into flags[tile]; slice
-  // 1 waits for all of them and stores partial + acc + fin_beta * fin_C into fin_C — the sum
-  // order of the separate reduce kernel, so results are bit-identical and deterministic. The
-  // consumers return each flag to 0, so the array stays zeroed between launches.
-  unsigned* flags = nullptr;
-  float* fin_C = nullptr;
-  long fin_ldc = 0;
-  float fin_beta = 0.f;
-  // K blocks of slice 0 in that mode (0: even split): slice 0 gets the shorter part so its
-  // partial is stored while slice 1 is still in its main loop
-  int kb_split = 0;
 };
 
 // C[M,N] = op(A)[M,K] * op(B)[N,K]^T.
@@ -65,8 +53,6 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
 // Split-K scratch for low-occupancy GEMMs (few output tiles, long K). Per host thread
 // (each executor worker drives one GPU); without one, GEMMs never split.
 void gemm_set_splitk_workspace(float* ws, long floats);
-// Per host thread (tests / diagnostics): false = two-way splits reduce in a separate kernel.
-void gemm_set_splitk_fixup(bool on);
 // Per host thread: true = "fp32" precision (3xTF32 split on the tensor cores, ~fp32
 // accuracy at 3x the MMA work), false = plain TF32 (default).
 void gemm_set_precision_fp32(bool three_pass);

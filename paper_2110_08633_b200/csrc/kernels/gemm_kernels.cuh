@@ -81,7 +81,7 @@ struct TileInfo {
 
 template <int BN>
 __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n, int M, int N, int K, int nb2,
-                                              int causal, int nb1 = 1, int kb_split = 0) {
+                                              int causal, int nb1 = 1) {
   TileInfo t;
   const int per_batch = tiles_m * tiles_n;
   const int z = tile / per_batch;
@@ -104,14 +104,9 @@ __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n
     t.nkb = max(0, kb_all - t.kb0);
   } else if (causal == kSplitK) {
     // z1 indexes the K slice; the operands themselves are not batched (TMA z = 0)
-    if (nb1 == 2 && kb_split > 0) {  // uneven two-way split (in-kernel reduce): slice 0 ends first
-      t.kb0 = t.z1 == 0 ? 0 : kb_split;
-      t.nkb = t.z1 == 0 ? kb_split : kb_all - kb_split;
-    } else {
-      const int per = (kb_all + nb1 - 1) / nb1;
-      t.kb0 = t.z1 * per;
-      t.nkb = max(0, min(per, kb_all - t.kb0));
-    }
+    const int per = (kb_all + nb1 - 1) / nb1;
+    t.kb0 = t.z1 * per;
+    t.nkb = max(0, min(per, kb_all - t.kb0));
   }
   (void)M;
   (void)N;
@@ -193,7 +188,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
         const long grow = x0.row0 + r;
         av[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         pv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (x0.src && ok) av[i] = __ldcg(reinterpret_cast<const float4*>(x0.src + grow * x0.lds + col));
+        if (x0.src && ok) av[i] = *reinterpret_cast<const float4*>(x0.src + grow * x0.lds + col);
         if (MODE == kEpiStore && x0.use_beta && ok) pv[i] = *reinterpret_cast<const float4*>(x0.Cb + grow * epi.ldc + col);
       }
 #pragma unroll
@@ -349,7 +344,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
         if (ti.skip) continue;
         if (bat.causal == kSplitK) ti.z1 = ti.z2 = 0;  // K slices read the same operands
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
@@ -391,7 +386,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     uint32_t phase = 0;
     int local = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -456,7 +451,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       for (int kb = 0; kb < ti.nkb; ++kb) {
         mbar_wait(&full[stage], phase);
@@ -488,7 +483,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const uint32_t q = warp - 4;  // TMEM lane quarter this warp may access
     int local = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
@@ -526,55 +521,6 @@ struct SmemPair {
   static constexpr int kEpi = 4 * 32 * 36 * 4;
   static constexpr int kTotal = kRing + kEpi + 1024 + 256;
 };
-
-// Epilogue of one pair-kernel tile (this warp's 32 rows, chunks [c_begin, c_end)), with the
-// in-kernel two-way split-K of GemmBatch::flags: slice 0 stores its partial and counts the
-// chunks it stored; slice 1 waits until slice 0's whole CTA tile is stored (4 quarters x
-// BN/32 chunks), adds it as the residual operand and stores the final C, then counts itself
-// as a consumer — the last of the tile's consumer warps resets the flag to 0.
-template <int BN, int MODE>
-__device__ __forceinline__ void pair_epilogue(const TileInfo& ti, int tile, int per_batch, uint32_t rank, int acc,
-                                              uint32_t q, uint32_t tmem_base, float* epi_smem, const GemmEpilogue& epi,
-                                              const GemmBatch& bat, int M, int N, int c_begin, int c_end,
-                                              int consumers) {
-  if (MODE != kEpiStore || bat.causal != kSplitK || bat.flags == nullptr) {
-    epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N, c_begin, c_end);
-    return;
-  }
-  unsigned* flag = bat.flags + (tile % per_batch) * 2 + rank;
-  const unsigned target = 4u * (BN / 32);
-  if (ti.z1 == 0) {
-    epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N, c_begin, c_end);
-    __threadfence();
-    __syncwarp();
-    if (lane_id() == 0) atomicAdd(flag, static_cast<unsigned>(c_end - c_begin));
-    return;
-  }
-  if (lane_id() == 0) {
-    unsigned v;
-    while (true) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-      if (v >= target) break;
-      __nanosleep(64);
-    }
-  }
-  __syncwarp();
-  GemmEpilogue e2 = epi;
-  e2.C = bat.fin_C;
-  e2.ldc = bat.fin_ldc;
-  e2.R = epi.C;  // slice 0's partial
-  e2.ldr = epi.ldc;
-  e2.beta = bat.fin_beta;
-  GemmBatch b2 = bat;
-  b2.c_s1 = 0;
-  b2.c_s2 = 0;
-  epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, e2, b2, M, N, c_begin, c_end);
-  __syncwarp();
-  if (lane_id() == 0) {
-    const unsigned old = atomicAdd(flag, 1u);
-    if (old == target + static_cast<unsigned>(consumers) - 1u) atomicExch(flag, 0u);
-  }
-}
 
 template <int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
@@ -630,7 +576,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
         // tile_info counts 128-row tiles; rescale to this CTA's half of the 256-row pair tile
         ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
         if (bat.causal == kSplitK) ti.z1 = ti.z2 = 0;
@@ -675,7 +621,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       uint32_t phase = 0;
       int local = 0;
       for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-        const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+        const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         ++local;
@@ -719,7 +665,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     const uint32_t q = warp - 4;
     int local = 0;
     for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-      TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+      TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
       const int acc = local & 1;
       mbar_wait(&tfull[acc], (local >> 1) & 1);
@@ -732,8 +678,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(lastbar);
       }
-      pair_epilogue<BN, MODE>(ti, tile, tiles_m * tiles_n, rank, acc, q, tmem_base, epi_smem, epi, bat, M, N, 0,
-                              last ? kHalfChunks : BN / 32, last ? 8 : 4);
+      epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N, 0, last ? kHalfChunks : BN / 32);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) {
@@ -747,15 +692,15 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     __syncwarp();
     const int cnt = (n_tiles - 1 - pair) / n_pairs + 1;  // tiles of this CTA
     const int tile = pair + (cnt - 1) * n_pairs;
-    TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1, bat.kb_split);
+    TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
     ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
     const int acc = (cnt - 1) & 1;
     // not tfull itself: an early parity test on it could pass for an earlier phase
     mbar_wait(lastbar, 0);
     tc_fence_after();
     // the pipeline ring is idle now (every TMA landed, every MMA read it): per-warp transposes
-    pair_epilogue<BN, MODE>(ti, tile, tiles_m * tiles_n, rank, acc, warp, tmem_base, reinterpret_cast<float*>(smem),
-                            epi, bat, M, N, kHalfChunks, BN / 32, 8);
+    epilogue_tile_m<BN, MODE>(ti, acc, warp, tmem_base, reinterpret_cast<float*>(smem), epi, bat, M, N, kHalfChunks,
+                              BN / 32);
   }
 
   tc_fence_before();

@@ -26,11 +26,6 @@ def gemm_config(precision_fp32=False, splitk_ws=None):
     check(lib().hy_gemm_config(int(precision_fp32), _p(splitk_ws), 0 if splitk_ws is None else splitk_ws.numel()))
 
 
-def gemm_splitk_fixup(on=True):
-    """Two-way split-K reduced in the CTA-pair kernel's epilogue (default) or by a separate kernel."""
-    check(lib().hy_gemm_splitk_fixup(int(on)))
-
-
 def gemm(A, B, *, a_mn=False, b_mn=False, M=None, N=None, K=None, C=None, bias=None, R=None, beta=0.0,
          mode=0, H=None, lda=None, ldb=None, ldc=None):
     """C = op(A) op(B)^T. a_mn=False: A is [M,K]; True: A is [K,M]. Likewise B with N."""

@@ -119,17 +119,6 @@ def test_gemm_split256_weight_grads(shape, a_mn, b_mn):
     assert rel(C1, ref) < 3e-3, rel(C1, ref)
     assert rel(C1 - C0, Cu - C0) < 1e-4  # same TF32 operands, fp32 partial sums in another order
     assert torch.equal(C1, C2)
-    # the in-kernel two-way reduce (default) against the separate reduce kernel: same sum order
-    # (that path stores every partial, so it gets a workspace with room for all of them)
-    ws2 = torch.empty(8 * M * N + 2048, device=dev)
-    try:
-        K.gemm_config(splitk_ws=ws2)
-        K.gemm_splitk_fixup(False)
-        C3 = K.gemm(Ain, Bin, a_mn=a_mn, b_mn=b_mn, M=M, N=N, K=Kd, C=C0.clone(), beta=1.0)
-    finally:
-        K.gemm_splitk_fixup(True)
-        K.gemm_config()
-    assert torch.equal(C1, C3)
 
 
 def test_gemm_epilogues():

@@ -1,16 +1,13 @@
 """dW(fc) GEMM at the C2 shape as bench.py times it (token-major operands, split-K workspace),
-50 launches back to back behind a GPU spin, CUDA events: us per launch. HY_FIXUP=0 selects the
-separate reduce kernel (with a workspace for two partials)."""
+50 launches back to back behind a GPU spin, CUDA events: us per launch."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2110_08633_b200 import kernels as K
 d, M = 768, 4096
 dev = torch.device("cuda")
-fix = os.environ.get("HY_FIXUP", "1") != "0"
-ws = torch.empty(2 * 4 * d * d + (0 if fix else 4096), device=dev)
+ws = torch.empty(2 * 4 * d * d, device=dev)
 K.gemm_config(splitk_ws=ws)
-K.gemm_splitk_fixup(fix)
 dY = torch.randn(M, 4 * d, device=dev)
 X = torch.randn(M, d, device=dev)
 W = torch.empty(4 * d, d, device=dev)
@@ -26,4 +23,4 @@ for _ in range(50):
 e1.record()
 torch.cuda.synchronize()
 t = e0.elapsed_time(e1) / 50 * 1e3
-print(f"fixup={int(fix)} slice0={os.environ.get('HY_GEMM_SLICE0', 'default')} {t:.2f} us {2 * M * 4 * d * d / t / 1e6:.0f} TFLOP/s")
+print(f"dW(fc) {t:.2f} us {2 * M * 4 * d * d / t / 1e6:.0f} TFLOP/s")

@@ -15,7 +15,6 @@ d, M = 768, 4096
 dev = torch.device("cuda")
 ws = torch.empty(2 * 4 * d * d, device=dev)
 K.gemm_config(splitk_ws=ws)
-K.gemm_splitk_fixup(os.environ.get("HY_FIXUP", "1") != "0")
 dY = torch.randn(M, 4 * d, device=dev)
 X = torch.randn(M, d, device=dev)
 W = torch.empty(4 * d, d, device=dev)
