@@ -104,6 +104,9 @@ struct LinkStats {
   double exposed_s = 0;                   // link busy while no compute op runs
   double h2d_bytes = 0, d2h_bytes = 0;    // bytes of the logged copies
   long copies = 0, ops = 0;
+  // HY_LINK_DUMP=1 (diagnostics): every logged interval {lane 0 compute / 1 H2D / 2 D2H,
+  // stream 0 comp 1 down 2 up 3 opt 4 opt2 5 optin 6 other, start s, end s, bytes}
+  std::vector<std::vector<double>> raw;
 };
 
 struct ExecResult {

@@ -213,6 +213,7 @@ ojson session_result(Session& S, bool with_trace) {
                     {"compute_busy_s", l.compute_busy_s}, {"exposed_s", l.exposed_s},
                     {"overlap_frac", l.link_busy_s > 0 ? 1.0 - l.exposed_s / l.link_busy_s : 1.0},
                     {"h2d_bytes", l.h2d_bytes}, {"d2h_bytes", l.d2h_bytes}, {"copies", l.copies}, {"ops", l.ops}});
+      if (!l.raw.empty()) ls.back()["raw"] = l.raw;
     }
     out["links"] = ls;
   }

@@ -683,8 +683,15 @@ void ExecutorImpl::collect(int pass, ExecResult& res, bool interval_log) {
       ls.plan_device = w.plan_dev;
       ls.pass_s = ms * 1e-3;
       Spans lane[3];
+      static const bool dump = std::getenv("HY_LINK_DUMP") != nullptr;
       for (const hy::IntervalLog::Rec& r : w.ilog.recs) {
         lane[r.lane].emplace_back(rel(r.a), rel(r.b));
+        if (dump) {
+          const cudaStream_t ss[6] = {w.comp, w.down, w.up, w.opt, w.opt2, w.optin};
+          int code = 6;
+          for (int i = 0; i < 6; ++i) code = (r.st == ss[i] && code == 6) ? i : code;
+          ls.raw.push_back({static_cast<double>(r.lane), static_cast<double>(code), rel(r.a), rel(r.b), r.bytes});
+        }
         if (r.lane == hy::IntervalLog::kH2D) ls.h2d_bytes += r.bytes, ++ls.copies;
         if (r.lane == hy::IntervalLog::kD2H) ls.d2h_bytes += r.bytes, ++ls.copies;
         if (r.lane == hy::IntervalLog::kCompute) ++ls.ops;

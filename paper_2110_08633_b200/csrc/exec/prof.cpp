@@ -49,7 +49,7 @@ cudaEvent_t IntervalLog::take() {
 }
 
 size_t IntervalLog::begin(int lane, double bytes, cudaStream_t st) {
-  Rec r{lane, bytes, take(), take()};
+  Rec r{lane, bytes, take(), take(), st};
   cudaEventRecord(r.a, st);
   recs.push_back(r);
   return recs.size() - 1;

@@ -45,6 +45,7 @@ struct IntervalLog {
     int lane;
     double bytes;
     cudaEvent_t a, b;
+    cudaStream_t st;
   };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;

@@ -619,41 +619,46 @@ __global__ void __launch_bounds__(160) attn_dkdv_kernel(
   }
 }
 
-// dQ of one (batch, head, 128-query tile), warp-specialised and pipelined over 64-key tiles j:
-//   warp 4 (one lane) loads K/V tiles (double-buffered) and issues S(j) = Q K(j)^T and
-//   dP(j) = dO V(j)^T into TMEM (double-buffered) as soon as their tiles land, then
-//   dQ += dS(j) K(j) with dS read from TMEM (written there by the compute warps);
-//   warps 0-3 (thread = query row) turn S, dP into dS = P (dP - Di) while the tensor core
-//   works on the neighbouring tiles.
-// smem: Q, dO 32 KB each + 2 stages x (K K-major, V K-major, K MN-major) 48 KB = 160 KB;
+// dQ, persistent and warp-specialised like the forward: units (batch, head, 128-query tile),
+// longest first in snake order over one CTA per SM; the key tiles of all a CTA's units stream
+// through one pipeline (global tile index g):
+//   warp 5 (one lane): TMA — Q and dO of each unit (reloaded once its last S / dP landed),
+//     K (K-major), V (K-major), K (MN-major) of tile g into stage g & 1;
+//   warp 4 (one lane): tcgen05.mma from an event loop — S(g) = Q K(g)^T and dP(g) = dO V(g)^T
+//     into TMEM buffer g & 1 as soon as the softmax warps have read that buffer out, and
+//     dQ += dS(g) K(g) (dS from TMEM) once dS(g) is stored;
+//   warps 0-3 (thread = query row): dS = P (dP - Di), P = exp2(S c - lse2), TF32-rounded.
+// smem: Q, dO 32 KB each + 2 stages x (K k, V k, K mn) 48 KB = 160 KB;
 // TMEM: S 2 x 64, dP 2 x 64, dS 2 x 64, dQ 64 columns.
 constexpr int kDqSmem = 32768 * 2 + 2 * 49152 + 256 + 1024;
 
-__global__ void __launch_bounds__(160) attn_dq_kernel(
+__global__ void __launch_bounds__(192, 1) attn_dq_kernel(
     const __grid_constant__ CUtensorMap mq128, const __grid_constant__ CUtensorMap mdo128,
-    const __grid_constant__ CUtensorMap mk64, const __grid_constant__ CUtensorMap mkmn, int T, int H,
+    const __grid_constant__ CUtensorMap mk64, const __grid_constant__ CUtensorMap mkmn, int T, int H, int B,
     const float* __restrict__ lse2, const float* __restrict__ Di, float* __restrict__ dqkv) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sQ = align1024(smem_raw);
   uint8_t* sG = sQ + 32768;
   uint8_t* sKV = sG + 32768;  // stage s: Kk at +0, Vk at +16K, Km at +32K
-  // barriers: 0 q/do, 1-2 kv[2], 3-4 sp[2] (S, dP landed), 5-6 ds[2] (dS written), 7-8 dq[2]
+  // barriers: 0 q/do, 1-2 kv, 3-4 spdone, 5-6 sfree (4), 7-8 dsready (4), 9-10 dqdone
   uint64_t* bar = reinterpret_cast<uint64_t*>(sKV + 2 * 49152);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 10);
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int nqt = (T + 127) / 128;
-  const int bh = blockIdx.x / nqt;
-  const int qt = nqt - 1 - blockIdx.x % nqt;
-  const int b = bh / H, h = bh % H;
-  const int q0 = qt * 128, D = H * HD, row0 = b * T;
-  const int nkt = min((T + 63) / 64, (q0 + 128) / 64);
+  uint64_t *bq = bar, *bkv = bar + 1, *bsp = bar + 3, *bsf = bar + 5, *bds = bar + 7, *bdq = bar + 9;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  FwdUnits W;
+  W.nqt = (T + 127) / 128;
+  W.BH = B * H;
+  W.U = W.nqt * W.BH;
+  W.G = static_cast<int>(gridDim.x);
+  const int c = static_cast<int>(blockIdx.x);
+  const int D = H * HD;
+  auto nkt_of = [&](int qt) { return min((T + 63) / 64, (qt * 128 + 128) / 64); };
   if (tid == 0) {
     tma_prefetch_desc(&mq128);
     tma_prefetch_desc(&mdo128);
     tma_prefetch_desc(&mk64);
     tma_prefetch_desc(&mkmn);
-    for (int i = 0; i < 9; ++i) mbar_init(&bar[i], i == 5 || i == 6 ? 4 : 1);
+    for (int i = 0; i < 11; ++i) mbar_init(&bar[i], (i >= 5 && i <= 8) ? 4 : 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tslot);
@@ -663,105 +668,155 @@ __global__ void __launch_bounds__(160) attn_dq_kernel(
   pdl_wait_and_trigger();
   const uint32_t tb = *tslot;  // S: tb + 64s, dP: tb + 128 + 64s, dS: tb + 256 + 64s, dQ: tb + 384
   const uint32_t tdQ = tb + 384;
-  if (warp == 4) {
-    if (lane_id() == 0) {
-      auto load_kv = [&](int j) {
-        uint8_t* st = sKV + (j & 1) * 49152;
-        uint64_t* bb = &bar[1 + (j & 1)];
-        const int k0 = 64 * j;
-        mbar_expect_tx(bb, 3 * 16384);
+  if (warp == 5) {
+    if (lane_id() == 0) {  // loader
+      int g = 0;
+      for (int r = 0;; ++r) {
+        const int u = W.nth(c, r);
+        if (u < 0) break;
+        int bh, qt;
+        W.unit(u, bh, qt);
+        const int b = bh / H, h = bh % H, row0 = b * T, q0 = qt * 128;
+        if (g > 0) mbar_wait(&bsp[(g - 1) & 1], ((g - 1) >> 1) & 1);  // last S / dP of the previous unit
+        mbar_expect_tx(bq, 65536);
         for (int kb = 0; kb < 2; ++kb) {
-          tma_load_2d(st + kb * 8192, &mk64, bb, D + h * HD + 32 * kb, row0 + k0);
-          tma_load_2d(st + 16384 + kb * 8192, &mk64, bb, 2 * D + h * HD + 32 * kb, row0 + k0);
-          for (int jn = 0; jn < 2; ++jn)
-            tma_load_2d(st + 32768 + kb * 8192 + jn * 4096, &mkmn, bb, D + h * HD + 32 * jn, row0 + k0 + 32 * kb);
+          tma_load_2d(sQ + kb * 16384, &mq128, bq, h * HD + 32 * kb, row0 + q0);
+          tma_load_2d(sG + kb * 16384, &mdo128, bq, h * HD + 32 * kb, row0 + q0);
         }
-      };
+        const int nkt = nkt_of(qt);
+        for (int j = 0; j < nkt; ++j, ++g) {
+          const int s = g & 1;
+          if (g >= 2) mbar_wait(&bdq[s], ((g - 2) >> 1) & 1);  // dQ(g-2) read stage s (after S / dP did)
+          uint8_t* st = sKV + s * 49152;
+          const int k0 = 64 * j;
+          mbar_expect_tx(&bkv[s], 3 * 16384);
+          for (int kb = 0; kb < 2; ++kb) {
+            tma_load_2d(st + kb * 8192, &mk64, &bkv[s], D + h * HD + 32 * kb, row0 + k0);
+            tma_load_2d(st + 16384 + kb * 8192, &mk64, &bkv[s], 2 * D + h * HD + 32 * kb, row0 + k0);
+            for (int jn = 0; jn < 2; ++jn)
+              tma_load_2d(st + 32768 + kb * 8192 + jn * 4096, &mkmn, &bkv[s], D + h * HD + 32 * jn, row0 + k0 + 32 * kb);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    if (lane_id() == 0) {  // MMA issuer: S / dP ahead of dQ
       constexpr uint32_t idS = idesc_tf32(128, 64, false, false);
       constexpr uint32_t idQ = idesc_tf32(128, 64, false, true);
-      auto issue_sp = [&](int j) {
-        uint8_t* st = sKV + (j & 1) * 49152;
-        mbar_wait(&bar[1 + (j & 1)], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t tS = tb + (j & 1) * 64, tP = tb + 128 + (j & 1) * 64;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(st, kk, 8192), idS, kk > 0);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sG, kk, 16384), desc_k(st + 16384, kk, 8192), idS, kk > 0);
-        mma_commit(&bar[3 + (j & 1)]);
+      struct Cur {
+        int g, r, j, nkt;
       };
-      mbar_expect_tx(&bar[0], 65536);
-      for (int kb = 0; kb < 2; ++kb) {
-        tma_load_2d(sQ + kb * 16384, &mq128, &bar[0], h * HD + 32 * kb, row0 + q0);
-        tma_load_2d(sG + kb * 16384, &mdo128, &bar[0], h * HD + 32 * kb, row0 + q0);
-      }
-      load_kv(0);
-      if (nkt > 1) load_kv(1);
-      mbar_wait(&bar[0], 0);
-      issue_sp(0);
-      for (int j = 0; j < nkt; ++j) {
-        // S/dP(j+1) into the TMEM buffers the compute warps released with dS(j-1)
-        if (j + 1 < nkt) issue_sp(j + 1);  // its buffers held tile j-1, whose dS was waited for
-        mbar_wait(&bar[5 + (j & 1)], (j >> 1) & 1);  // dS(j) in TMEM
-        tc_fence_after();
-        const uint32_t tdS = tb + 256 + (j & 1) * 64;
-        uint8_t* km = sKV + (j & 1) * 49152 + 32768;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdQ, tdS + kk * 8, desc_mn(km, kk), idQ, (j | kk) > 0);
-        mma_commit(&bar[7 + (j & 1)]);
-        if (j + 2 < nkt) {  // stage j&1 is free once dQ(j) has read K(j)
-          mbar_wait(&bar[7 + (j & 1)], (j >> 1) & 1);
-          load_kv(j + 2);
+      auto set_unit = [&](Cur& x) {
+        const int u = W.nth(c, x.r);
+        int bh, qt;
+        if (u >= 0) W.unit(u, bh, qt);
+        x.nkt = u >= 0 ? nkt_of(qt) : 0;
+      };
+      auto advance = [&](Cur& x) {
+        ++x.g;
+        if (++x.j == x.nkt) {
+          x.j = 0;
+          ++x.r;
+          set_unit(x);
         }
+      };
+      Cur cs{0, 0, 0, 0}, cp{0, 0, 0, 0};
+      set_unit(cs);
+      set_unit(cp);
+      while (cp.nkt > 0) {
+        bool progressed = false;
+        if (cs.nkt > 0) {
+          const int g = cs.g, sb = g & 1;
+          if ((g < 2 || mbar_test(&bsf[sb], ((g - 2) >> 1) & 1)) && mbar_test(bq, cs.r & 1) &&
+              mbar_test(&bkv[sb], (g >> 1) & 1)) {
+            tc_fence_after();
+            uint8_t* st = sKV + sb * 49152;
+            const uint32_t tS = tb + sb * 64, tP = tb + 128 + sb * 64;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(st, kk, 8192), idS, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sG, kk, 16384), desc_k(st + 16384, kk, 8192), idS, kk > 0);
+            mma_commit(&bsp[sb]);
+            advance(cs);
+            progressed = true;
+          }
+        }
+        {
+          const int g = cp.g, sb = g & 1;
+          if (cp.g < cs.g && mbar_test(&bds[sb], (g >> 1) & 1)) {
+            tc_fence_after();
+            const uint32_t tdS = tb + 256 + sb * 64;
+            uint8_t* km = sKV + sb * 49152 + 32768;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdQ, tdS + kk * 8, desc_mn(km, kk), idQ, (cp.j | kk) > 0);
+            mma_commit(&bdq[sb]);
+            advance(cp);
+            progressed = true;
+          }
+        }
+        if (!progressed) __nanosleep(20);
       }
     }
     __syncwarp();
   } else {
     const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
-    const int q = q0 + tid;
-    const long li = static_cast<long>(bh) * T + min(q, T - 1);
-    const float my_lse = lse2[li], my_di = Di[li];
-    for (int j = 0; j < nkt; ++j) {
-      const int k0 = 64 * j;
-      mbar_wait(&bar[3 + (j & 1)], (j >> 1) & 1);
+    int g = 0;
+    for (int r = 0;; ++r) {
+      const int u = W.nth(c, r);
+      if (u < 0) break;
+      int bh, qt;
+      W.unit(u, bh, qt);
+      const int b = bh / H, h = bh % H, row0 = b * T, q0 = qt * 128;
+      const int nkt = nkt_of(qt);
+      const int q = q0 + tid;
+      const long li = static_cast<long>(bh) * T + min(q, T - 1);
+      const float my_lse = lse2[li], my_di = Di[li];
+      for (int j = 0; j < nkt; ++j, ++g) {
+        const int k0 = 64 * j, sb = g & 1;
+        mbar_wait(&bsp[sb], (g >> 1) & 1);
+        tc_fence_after();
+        float s[64], dp[64];
+        tmem_ld64(tb + sb * 64 + lane_off, s);
+        tmem_ld64(tb + 128 + sb * 64 + lane_off, dp);
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&bsf[sb]);  // S / dP buffer free for S(g+2) / dP(g+2)
+        if (k0 + 63 <= q0) {  // whole tile visible (CTA-uniform)
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            const float p = fast_exp2(fmaf(s[i], kScaleLog2, -my_lse));
+            s[i] = tf32_round_add(p * (dp[i] - my_di));  // the 1/8 of dS is applied to dQ
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            const bool valid = k0 + i <= q;
+            const float p = valid ? fast_exp2(fmaf(s[i], kScaleLog2, -my_lse)) : 0.f;
+            s[i] = valid ? tf32_round_add(p * (dp[i] - my_di)) : 0.f;
+          }
+        }
+        if (g >= 2) mbar_wait(&bdq[sb], ((g - 2) >> 1) & 1);  // dQ(g-2) read this dS buffer
+        const uint32_t tdS = tb + 256 + sb * 64 + lane_off;
+        tmem_st_x32(tdS, s);
+        tmem_st_x32(tdS + 32, s + 32);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&bds[sb]);
+      }
+      // unit epilogue (the next unit's first dQ MMA overwrites dQ only after these rows have
+      // stored that unit's first dS, i.e. after this read)
+      mbar_wait(&bdq[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
-      float s[64], dp[64];
-      tmem_ld64(tb + (j & 1) * 64 + lane_off, s);
-      tmem_ld64(tb + 128 + (j & 1) * 64 + lane_off, dp);
-      if (k0 + 63 <= q0) {  // whole tile visible (CTA-uniform)
+      float dq[64];
+      tmem_ld64(tdQ + lane_off, dq);
+      if (q < T) {
+        float4* gq = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + q) * 3 * D + h * HD);
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p = fast_exp2(fmaf(s[c], kScaleLog2, -my_lse));
-          s[c] = tf32_round_add(p * (dp[c] - my_di));  // the 1/8 of dS is applied to dQ
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const bool valid = k0 + c <= q;
-          const float p = valid ? fast_exp2(fmaf(s[c], kScaleLog2, -my_lse)) : 0.f;
-          s[c] = valid ? tf32_round_add(p * (dp[c] - my_di)) : 0.f;
-        }
+        for (int i = 0; i < 16; ++i)
+          gq[i] = make_float4(0.125f * dq[4 * i], 0.125f * dq[4 * i + 1], 0.125f * dq[4 * i + 2], 0.125f * dq[4 * i + 3]);
       }
-      if (j >= 2) {  // dQ(j-2) has finished reading this dS buffer
-        mbar_wait(&bar[7 + (j & 1)], ((j - 2) >> 1) & 1);
-      }
-      const uint32_t tdS = tb + 256 + (j & 1) * 64 + lane_off;
-      tmem_st_x32(tdS, s);
-      tmem_st_x32(tdS + 32, s + 32);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&bar[5 + (j & 1)]);
-    }
-    mbar_wait(&bar[7 + ((nkt - 1) & 1)], ((nkt - 1) >> 1) & 1);
-    tc_fence_after();
-    float dq[64];
-    tmem_ld64(tdQ + lane_off, dq);
-    if (q < T) {
-      float4* g = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + q) * 3 * D + h * HD);
-#pragma unroll
-      for (int c = 0; c < 16; ++c)
-        g[c] = make_float4(0.125f * dq[4 * c], 0.125f * dq[4 * c + 1], 0.125f * dq[4 * c + 2], 0.125f * dq[4 * c + 3]);
     }
   }
   tc_fence_before();
@@ -830,7 +885,8 @@ cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* 
   }
   count_launch();
   {
-    const cudaError_t e = launch_pdl(attn_dq_kernel, dim3(B * H * tiles), dim3(160), kDqSmem, st, mq128, mdo128, mk64, mkmn, T, H, static_cast<const float*>(lse2), static_cast<const float*>(Di), dqkv);
+    const int grid = std::min(B * H * tiles, attn_sm_count());  // persistent: one CTA per SM
+    const cudaError_t e = launch_pdl(attn_dq_kernel, dim3(grid), dim3(192), kDqSmem, st, mq128, mdo128, mk64, mkmn, T, H, B, static_cast<const float*>(lse2), static_cast<const float*>(Di), dqkv);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
