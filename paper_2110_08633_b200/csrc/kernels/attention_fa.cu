@@ -420,67 +420,90 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
   }
 }
 
-// Di[bh*T + q] = sum_c dO[q, h*64 + c] * O[q, h*64 + c]; one thread per (row, head): 32
-// independent 128-bit loads in flight per thread (the 256-byte head slices are fully used).
+// Di[bh*T + q] = sum_c dO[q, h*64 + c] * O[q, h*64 + c]; 16 lanes per (row, head), one
+// float4 of O and of dO each (fully coalesced 256-byte head slices), then a 16-lane shuffle sum.
 __global__ void attn_di_kernel(long n, int T, int H, const float* __restrict__ out, const float* __restrict__ dout,
                                float* __restrict__ Di) {
   pdl_wait_and_trigger();
-  const long w = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (w >= n) return;
-  const long row = w / H;
-  const int h = static_cast<int>(w % H);
-  const long D = static_cast<long>(H) * HD;
-  const float4* a = reinterpret_cast<const float4*>(out + row * D + h * HD);
-  const float4* g = reinterpret_cast<const float4*>(dout + row * D + h * HD);
-  float4 av[16], gv[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    av[c] = __ldg(a + c);
-    gv[c] = __ldg(g + c);
-  }
+  const long t = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long w = t >> 4;  // (row, head) pair
+  const int sub = static_cast<int>(t & 15);
   float v = 0.f;
+  if (w < n) {
+    const long row = w / H;
+    const int h = static_cast<int>(w % H);
+    const long off = row * static_cast<long>(H) * HD + h * HD + 4 * sub;
+    const float4 a = __ldg(reinterpret_cast<const float4*>(out + off));
+    const float4 g = __ldg(reinterpret_cast<const float4*>(dout + off));
+    v = (a.x * g.x + a.y * g.y) + (a.z * g.z + a.w * g.w);
+  }
 #pragma unroll
-  for (int c = 0; c < 16; ++c) v += (av[c].x * gv[c].x + av[c].y * gv[c].y) + (av[c].z * gv[c].z + av[c].w * gv[c].w);
-  const long b = row / T, q = row % T;
-  Di[(b * H + h) * T + q] = v;
+  for (int m = 8; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  if (w < n && sub == 0) {
+    const long row = w / H;
+    const int h = static_cast<int>(w % H);
+    const long b = row / T, q = row % T;
+    Di[(b * H + h) * T + q] = v;
+  }
 }
 
-// dK, dV of one (batch, head, 128-key tile), warp-specialised and pipelined over 64-query
-// tiles i (from the diagonal): warp 4 (one lane) streams Q / dO tiles (double-buffered, both
-// majors) and issues S^T(i) = K Q(i)^T, dP^T(i) = V dO(i)^T into double-buffered TMEM as soon
-// as they land, then dV += P^T(i) dO(i) and dK += dS^T(i) Q(i) with P^T, dS^T read from TMEM;
-// warps 0-3 (thread = key row) compute P^T = exp2(S^T c - lse2) and dS^T = P^T (dP^T - Di).
+// dK, dV, persistent and warp-specialised: units (batch, head, 128-key tile), those near the
+// start of the sequence (the most query tiles) first, in snake order over one CTA per SM; the
+// query tiles of all a CTA's units stream through one pipeline (global tile index g):
+//   warp 5 (one lane): TMA — K and V of each unit (reloaded once its last S^T / dP^T landed),
+//     Q and dO of tile g in both majors into stage g & 1;
+//   warp 4 (one lane): tcgen05.mma from an event loop — S^T(g) = K Q(g)^T and dP^T(g) = V dO(g)^T
+//     into TMEM buffer g & 1 once the compute warps have read it out, then dV += P^T(g) dO(g) and
+//     dK += dS^T(g) Q(g) with P^T, dS^T from TMEM once they are stored;
+//   warps 0-3 (thread = key row): P^T = exp2(S^T c - lse2), dS^T = P^T (dP^T - Di), TF32-rounded
+//     (the softmax scale 1/8 is applied to dK once at the end).
 // smem: K, V 32 KB each + 2 stages x (Q k, Q mn, dO k, dO mn) 64 KB = 192 KB;
 // TMEM: S^T 2 x 64, dP^T 2 x 64, P^T 64, dS^T 64, dV 64, dK 64 columns.
 constexpr int kDkvSmem = 32768 * 2 + 2 * 65536 + 256 + 1024 + 1024;  // + lse / Di staging
 
-__global__ void __launch_bounds__(160) attn_dkdv_kernel(
+struct KvUnits {
+  int nkt, BH, U, G;
+  // unit -> (bh, kt): key tiles near the start (most queries) first
+  __device__ __forceinline__ void unit(int u, int& bh, int& kt) const {
+    kt = u / BH;
+    bh = u % BH;
+  }
+  __device__ __forceinline__ int nth(int c, int r) const {
+    const int u = r * G + ((r & 1) ? G - 1 - c : c);
+    return u < U ? u : -1;
+  }
+};
+
+__global__ void __launch_bounds__(192, 1) attn_dkdv_kernel(
     const __grid_constant__ CUtensorMap mkv128, const __grid_constant__ CUtensorMap mq64,
     const __grid_constant__ CUtensorMap mqmn, const __grid_constant__ CUtensorMap mdo64,
-    const __grid_constant__ CUtensorMap mdomn, int T, int H, const float* __restrict__ lse2,
+    const __grid_constant__ CUtensorMap mdomn, int T, int H, int B, const float* __restrict__ lse2,
     const float* __restrict__ Di, float* __restrict__ dqkv) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sK = align1024(smem_raw);
   uint8_t* sV = sK + 32768;
   uint8_t* sQG = sV + 32768;  // stage s: Q k at +0, Q mn at +16K, dO k at +32K, dO mn at +48K
-  // barriers: 0 k/v, 1-2 qg[2], 3-4 sp[2], 5 pds (P^T, dS^T written), 6-7 g[2] (dV, dK MMAs done)
+  // barriers: 0 kv, 1-2 qg, 3-4 spdone, 5-6 sfree (4), 7 pds (4), 8-9 gdone
   uint64_t* bar = reinterpret_cast<uint64_t*>(sQG + 2 * 65536);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 8);
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5;
-  const int nkt = (T + 127) / 128;
-  const int bh = blockIdx.x / nkt;
-  const int kt = blockIdx.x % nkt;  // tiles near the start see the most queries: schedule them first
-  const int b = bh / H, h = bh % H;
-  const int k0 = kt * 128, D = H * HD, row0 = b * T;
-  const int nq = (T - k0 + 63) / 64;
+  uint64_t *bkv = bar, *bqg = bar + 1, *bsp = bar + 3, *bsf = bar + 5, *bpd = bar + 7, *bgd = bar + 8;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 10);
+  float* sLD = reinterpret_cast<float*>(bar + 16);  // [2][lse 64 | Di 64] per query tile
+  const int tid = threadIdx.x, warp = tid >> 5;
+  KvUnits W;
+  W.nkt = (T + 127) / 128;
+  W.BH = B * H;
+  W.U = W.nkt * W.BH;
+  W.G = static_cast<int>(gridDim.x);
+  const int c = static_cast<int>(blockIdx.x);
+  const int D = H * HD;
+  auto nq_of = [&](int kt) { return (T - kt * 128 + 63) / 64; };
   if (tid == 0) {
     tma_prefetch_desc(&mkv128);
     tma_prefetch_desc(&mq64);
     tma_prefetch_desc(&mqmn);
     tma_prefetch_desc(&mdo64);
     tma_prefetch_desc(&mdomn);
-    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], i == 5 ? 4 : 1);
+    for (int i = 0; i < 10; ++i) mbar_init(&bar[i], (i >= 5 && i <= 7) ? 4 : 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<512>(tslot);
@@ -491,123 +514,173 @@ __global__ void __launch_bounds__(160) attn_dkdv_kernel(
   // S^T: tb + 64s, dP^T: tb + 128 + 64s, P^T: tb + 256, dS^T: tb + 320, dV: tb + 384, dK: tb + 448
   const uint32_t tb = *tslot;
   const uint32_t tPT = tb + 256, tDST = tb + 320, tdV = tb + 384, tdK = tb + 448;
-  if (warp == 4) {
-    if (lane_id() == 0) {
-      auto load_q = [&](int i) {
-        uint8_t* st = sQG + (i & 1) * 65536;
-        uint64_t* bb = &bar[1 + (i & 1)];
-        const int q0 = k0 + 64 * i;
-        mbar_expect_tx(bb, 4 * 16384);
+  if (warp == 5) {
+    if (lane_id() == 0) {  // loader
+      int g = 0;
+      for (int r = 0;; ++r) {
+        const int u = W.nth(c, r);
+        if (u < 0) break;
+        int bh, kt;
+        W.unit(u, bh, kt);
+        const int b = bh / H, h = bh % H, row0 = b * T, k0 = kt * 128;
+        if (g > 0) mbar_wait(&bsp[(g - 1) & 1], ((g - 1) >> 1) & 1);  // last S^T / dP^T of the previous unit
+        mbar_expect_tx(bkv, 65536);
         for (int kb = 0; kb < 2; ++kb) {
-          tma_load_2d(st + kb * 8192, &mq64, bb, h * HD + 32 * kb, row0 + q0);
-          tma_load_2d(st + 32768 + kb * 8192, &mdo64, bb, h * HD + 32 * kb, row0 + q0);
-          for (int jn = 0; jn < 2; ++jn) {
-            tma_load_2d(st + 16384 + kb * 8192 + jn * 4096, &mqmn, bb, h * HD + 32 * jn, row0 + q0 + 32 * kb);
-            tma_load_2d(st + 49152 + kb * 8192 + jn * 4096, &mdomn, bb, h * HD + 32 * jn, row0 + q0 + 32 * kb);
+          tma_load_2d(sK + kb * 16384, &mkv128, bkv, D + h * HD + 32 * kb, row0 + k0);
+          tma_load_2d(sV + kb * 16384, &mkv128, bkv, 2 * D + h * HD + 32 * kb, row0 + k0);
+        }
+        const int nq = nq_of(kt);
+        for (int i = 0; i < nq; ++i, ++g) {
+          const int sb = g & 1;
+          if (g >= 2) mbar_wait(&bgd[sb], ((g - 2) >> 1) & 1);  // dV / dK(g-2) read stage sb
+          uint8_t* st = sQG + sb * 65536;
+          const int q0 = k0 + 64 * i;
+          mbar_expect_tx(&bqg[sb], 4 * 16384);
+          for (int kb = 0; kb < 2; ++kb) {
+            tma_load_2d(st + kb * 8192, &mq64, &bqg[sb], h * HD + 32 * kb, row0 + q0);
+            tma_load_2d(st + 32768 + kb * 8192, &mdo64, &bqg[sb], h * HD + 32 * kb, row0 + q0);
+            for (int jn = 0; jn < 2; ++jn) {
+              tma_load_2d(st + 16384 + kb * 8192 + jn * 4096, &mqmn, &bqg[sb], h * HD + 32 * jn, row0 + q0 + 32 * kb);
+              tma_load_2d(st + 49152 + kb * 8192 + jn * 4096, &mdomn, &bqg[sb], h * HD + 32 * jn, row0 + q0 + 32 * kb);
+            }
           }
         }
-      };
+      }
+    }
+    __syncwarp();
+  } else if (warp == 4) {
+    if (lane_id() == 0) {  // MMA issuer: S^T / dP^T ahead of dV / dK
       constexpr uint32_t idT = idesc_tf32(128, 64, false, false);  // S^T, dP^T
       constexpr uint32_t idG = idesc_tf32(128, 64, false, true);   // dV, dK (B MN-major)
-      auto issue_sp = [&](int i) {
-        uint8_t* st = sQG + (i & 1) * 65536;
-        mbar_wait(&bar[1 + (i & 1)], (i >> 1) & 1);
-        tc_fence_after();
-        const uint32_t tS = tb + (i & 1) * 64, tP = tb + 128 + (i & 1) * 64;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sK, kk, 16384), desc_k(st, kk, 8192), idT, kk > 0);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sV, kk, 16384), desc_k(st + 32768, kk, 8192), idT, kk > 0);
-        mma_commit(&bar[3 + (i & 1)]);
+      struct Cur {
+        int g, r, j, n;
       };
-      mbar_expect_tx(&bar[0], 65536);
-      for (int kb = 0; kb < 2; ++kb) {
-        tma_load_2d(sK + kb * 16384, &mkv128, &bar[0], D + h * HD + 32 * kb, row0 + k0);
-        tma_load_2d(sV + kb * 16384, &mkv128, &bar[0], 2 * D + h * HD + 32 * kb, row0 + k0);
-      }
-      load_q(0);
-      if (nq > 1) load_q(1);
-      mbar_wait(&bar[0], 0);
-      issue_sp(0);
-      for (int i = 0; i < nq; ++i) {
-        // S^T/dP^T(i+1) overwrite the buffers of tile i-1, released with its P^T, dS^T (waited
-        // for in the previous iteration; bar[5] must not be re-waited on an old phase)
-        if (i + 1 < nq) issue_sp(i + 1);
-        mbar_wait(&bar[5], i & 1);  // P^T(i), dS^T(i) in TMEM
-        tc_fence_after();
-        uint8_t* st = sQG + (i & 1) * 65536;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdV, tPT + kk * 8, desc_mn(st + 49152, kk), idG, (i | kk) > 0);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdK, tDST + kk * 8, desc_mn(st + 16384, kk), idG, (i | kk) > 0);
-        mma_commit(&bar[6 + (i & 1)]);
-        if (i + 2 < nq) {  // stage i&1 is free once dV/dK(i) have read it
-          mbar_wait(&bar[6 + (i & 1)], (i >> 1) & 1);
-          load_q(i + 2);
+      auto set_unit = [&](Cur& x) {
+        const int u = W.nth(c, x.r);
+        int bh, kt;
+        if (u >= 0) W.unit(u, bh, kt);
+        x.n = u >= 0 ? nq_of(kt) : 0;
+      };
+      auto advance = [&](Cur& x) {
+        ++x.g;
+        if (++x.j == x.n) {
+          x.j = 0;
+          ++x.r;
+          set_unit(x);
         }
+      };
+      Cur cs{0, 0, 0, 0}, cp{0, 0, 0, 0};
+      set_unit(cs);
+      set_unit(cp);
+      while (cp.n > 0) {
+        bool progressed = false;
+        if (cs.n > 0) {
+          const int g = cs.g, sb = g & 1;
+          if ((g < 2 || mbar_test(&bsf[sb], ((g - 2) >> 1) & 1)) && mbar_test(bkv, cs.r & 1) &&
+              mbar_test(&bqg[sb], (g >> 1) & 1)) {
+            tc_fence_after();
+            uint8_t* st = sQG + sb * 65536;
+            const uint32_t tS = tb + sb * 64, tP = tb + 128 + sb * 64;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_tf32(tS, desc_k(sK, kk, 16384), desc_k(st, kk, 8192), idT, kk > 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_tf32(tP, desc_k(sV, kk, 16384), desc_k(st + 32768, kk, 8192), idT, kk > 0);
+            mma_commit(&bsp[sb]);
+            advance(cs);
+            progressed = true;
+          }
+        }
+        {
+          const int g = cp.g, sb = g & 1;
+          if (cp.g < cs.g && mbar_test(bpd, g & 1)) {
+            tc_fence_after();
+            uint8_t* st = sQG + sb * 65536;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdV, tPT + kk * 8, desc_mn(st + 49152, kk), idG, (cp.j | kk) > 0);
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) mma_tf32_ts(tdK, tDST + kk * 8, desc_mn(st + 16384, kk), idG, (cp.j | kk) > 0);
+            mma_commit(&bgd[sb]);
+            advance(cp);
+            progressed = true;
+          }
+        }
+        if (!progressed) __nanosleep(20);
       }
     }
     __syncwarp();
   } else {
     const uint32_t lane_off = static_cast<uint32_t>((tid & ~31) << 16);
-    const int key = k0 + tid;
-    const float* lse_bh = lse2 + static_cast<long>(bh) * T;
-    const float* di_bh = Di + static_cast<long>(bh) * T;
-    float* sLD = reinterpret_cast<float*>(bar + 10);  // [2][lse 64 | Di 64] per query tile
-    for (int i = 0; i < nq; ++i) {
-      const int q0 = k0 + 64 * i;
-      // the tile's 64 lse / Di values, one per compute thread, staged for broadcast reads
-      float* ld = sLD + (i & 1) * 128;
-      {
-        const int q = q0 + (tid & 63);
-        ld[tid] = q < T ? (tid < 64 ? lse_bh[q] : di_bh[q]) : 0.f;
+    int g = 0;
+    for (int r = 0;; ++r) {
+      const int u = W.nth(c, r);
+      if (u < 0) break;
+      int bh, kt;
+      W.unit(u, bh, kt);
+      const int b = bh / H, h = bh % H, row0 = b * T, k0 = kt * 128;
+      const int nq = nq_of(kt);
+      const int key = k0 + tid;
+      const float* lse_bh = lse2 + static_cast<long>(bh) * T;
+      const float* di_bh = Di + static_cast<long>(bh) * T;
+      for (int i = 0; i < nq; ++i, ++g) {
+        const int q0 = k0 + 64 * i, sb = g & 1;
+        // the tile's 64 lse / Di values, one per compute thread, staged for broadcast reads
+        float* ld = sLD + sb * 128;
+        {
+          const int q = q0 + (tid & 63);
+          ld[tid] = q < T ? (tid < 64 ? lse_bh[q] : di_bh[q]) : 0.f;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        mbar_wait(&bsp[sb], (g >> 1) & 1);
+        tc_fence_after();
+        float s[64], dp[64];
+        tmem_ld64(tb + sb * 64 + lane_off, s);
+        tmem_ld64(tb + 128 + sb * 64 + lane_off, dp);
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(&bsf[sb]);  // S^T / dP^T buffer free for g + 2
+        const bool full = q0 >= k0 + 127 && q0 + 63 < T;  // no masked (query, key) pair in the tile
+        if (full) {
+#pragma unroll
+          for (int cc = 0; cc < 64; ++cc) {
+            const float p = fast_exp2(fmaf(s[cc], kScaleLog2, -ld[cc]));
+            s[cc] = tf32_round_add(p);
+            dp[cc] = tf32_round_add(p * (dp[cc] - ld[64 + cc]));  // the 1/8 of dS is applied to dK
+          }
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < 64; ++cc) {
+            const int q = q0 + cc;
+            const bool valid = q >= key && q < T;
+            const float p = valid ? fast_exp2(fmaf(s[cc], kScaleLog2, -ld[cc])) : 0.f;
+            s[cc] = tf32_round_add(p);
+            dp[cc] = valid ? tf32_round_add(p * (dp[cc] - ld[64 + cc])) : 0.f;
+          }
+        }
+        if (g >= 1) mbar_wait(&bgd[(g - 1) & 1], ((g - 1) >> 1) & 1);  // P^T, dS^T(g-1) consumed
+        tmem_st_x32(tPT + lane_off, s);
+        tmem_st_x32(tPT + lane_off + 32, s + 32);
+        tmem_st_x32(tDST + lane_off, dp);
+        tmem_st_x32(tDST + lane_off + 32, dp + 32);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane_id() == 0) mbar_arrive(bpd);
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      mbar_wait(&bar[3 + (i & 1)], (i >> 1) & 1);
+      // unit epilogue (the next unit's first dV / dK MMAs overwrite them only after these rows
+      // have stored that unit's first P^T / dS^T, i.e. after this read)
+      mbar_wait(&bgd[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
-      float s[64], dp[64];
-      tmem_ld64(tb + (i & 1) * 64 + lane_off, s);
-      tmem_ld64(tb + 128 + (i & 1) * 64 + lane_off, dp);
-      const bool full = q0 >= k0 + 127 && q0 + 63 < T;  // no masked (query, key) pair in the tile
-      if (full) {
+      float dv[64], dk[64];
+      tmem_ld64(tdV + lane_off, dv);
+      tmem_ld64(tdK + lane_off, dk);
+      if (key < T) {
+        float4* gk = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + D + h * HD);
+        float4* gv = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + 2 * D + h * HD);
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p = fast_exp2(fmaf(s[c], kScaleLog2, -ld[c]));
-          s[c] = tf32_round_add(p);
-          dp[c] = tf32_round_add(p * (dp[c] - ld[64 + c]));  // the 1/8 of dS is applied to dK
+        for (int cc = 0; cc < 16; ++cc) {
+          gk[cc] = make_float4(0.125f * dk[4 * cc], 0.125f * dk[4 * cc + 1], 0.125f * dk[4 * cc + 2], 0.125f * dk[4 * cc + 3]);
+          gv[cc] = make_float4(dv[4 * cc], dv[4 * cc + 1], dv[4 * cc + 2], dv[4 * cc + 3]);
         }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const int q = q0 + c;
-          const bool valid = q >= key && q < T;
-          const float p = valid ? fast_exp2(fmaf(s[c], kScaleLog2, -ld[c])) : 0.f;
-          s[c] = tf32_round_add(p);
-          dp[c] = valid ? tf32_round_add(p * (dp[c] - ld[64 + c])) : 0.f;
-        }
-      }
-      if (i >= 1) mbar_wait(&bar[6 + ((i - 1) & 1)], ((i - 1) >> 1) & 1);  // P^T, dS^T(i-1) consumed
-      tmem_st_x32(tPT + lane_off, s);
-      tmem_st_x32(tPT + lane_off + 32, s + 32);
-      tmem_st_x32(tDST + lane_off, dp);
-      tmem_st_x32(tDST + lane_off + 32, dp + 32);
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane_id() == 0) mbar_arrive(&bar[5]);
-    }
-    mbar_wait(&bar[6 + ((nq - 1) & 1)], ((nq - 1) >> 1) & 1);
-    tc_fence_after();
-    float dv[64], dk[64];
-    tmem_ld64(tdV + lane_off, dv);
-    tmem_ld64(tdK + lane_off, dk);
-    if (key < T) {
-      float4* gk = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + D + h * HD);
-      float4* gv = reinterpret_cast<float4*>(dqkv + static_cast<long>(row0 + key) * 3 * D + 2 * D + h * HD);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        gk[c] = make_float4(0.125f * dk[4 * c], 0.125f * dk[4 * c + 1], 0.125f * dk[4 * c + 2], 0.125f * dk[4 * c + 3]);
-        gv[c] = make_float4(dv[4 * c], dv[4 * c + 1], dv[4 * c + 2], dv[4 * c + 3]);
       }
     }
   }
@@ -874,13 +947,14 @@ cudaError_t attention_bwd_fa(cudaStream_t st, int B, int T, int H, const float* 
   const long n = rows * H;
   count_launch();
   {
-    const cudaError_t e = launch_pdl(attn_di_kernel, dim3(static_cast<unsigned>((n + 127) / 128)), dim3(128), 0, st, n, T, H, out, dout, Di);
+    const cudaError_t e = launch_pdl(attn_di_kernel, dim3(static_cast<unsigned>((16 * n + 255) / 256)), dim3(256), 0, st, n, T, H, out, dout, Di);
     if (e != cudaSuccess) return e;
   }
   const int tiles = (T + 127) / 128;
   count_launch();
   {
-    const cudaError_t e = launch_pdl(attn_dkdv_kernel, dim3(B * H * tiles), dim3(160), kDkvSmem, st, mkv128, mq64, mqmn, mdo64, mdomn, T, H, static_cast<const float*>(lse2), static_cast<const float*>(Di), dqkv);
+    const int grid = std::min(B * H * tiles, attn_sm_count());  // persistent: one CTA per SM
+    const cudaError_t e = launch_pdl(attn_dkdv_kernel, dim3(grid), dim3(192), kDkvSmem, st, mkv128, mq64, mqmn, mdo64, mdomn, T, H, B, static_cast<const float*>(lse2), static_cast<const float*>(Di), dqkv);
     if (e != cudaSuccess) return e;
   }
   count_launch();
