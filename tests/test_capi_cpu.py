@@ -103,3 +103,25 @@ def test_execute_request_validation_without_gpu(field, value, msg):
     with pytest.raises(P.HydraError) as e:
         P.execute(cfg, **{field: value})
     assert e.value.code == -1 and msg in str(e.value), (e.value.code, str(e.value))
+
+
+def test_pinned_shard_boundaries():
+    """Boundary reuse (partitioner.cpp:157-231) through the request: a list of starts or the
+    boundary text of boundaries_to_text; validated against the cap like the reference does."""
+    with open(os.path.join(ROOT, "configs", "c3_gpt2xl_x16.json")) as f:
+        cfg = json.load(f)
+    model = dict(cfg["models"][0])
+    model["generator"] = dict(model["generator"], batch_size=2)
+    cfg["models"] = [model]
+    cfg["jobs"] = [dict(cfg["jobs"][0], batch_size=2, minibatches_per_epoch=2)]
+    assert P.plan(cfg)["partitions"][0]["shard_starts"] == [0]  # b2 fits the 24e9 cap whole
+    cfg["options"] = dict(cfg["options"], buffer_policy={"kind": "absolute", "value": 5359724800.0})
+    for pin in ([0, 24, 48], "0\n24\n48\n"):
+        r = P.call_json("hy_plan_json", {"config": cfg, "shard_boundaries": [pin]})
+        assert r["partitions"][0]["shard_starts"] == [0, 24, 48]
+        assert len(r["tasks"]) == 2 * 2 * 3  # minibatches x (F + B) x shards
+    with pytest.raises(P.HydraError) as e:  # not strictly increasing
+        P.call_json("hy_plan_json", {"config": cfg, "shard_boundaries": [[0, 24, 24]]})
+    assert e.value.code == -1 and "strictly increasing" in str(e.value)
+    with pytest.raises(P.HydraError):  # only SHARP partitions spilled shards
+        P.call_json("hy_plan_json", {"config": cfg, "strategy": "task-parallel", "shard_boundaries": [[0, 24]]})
