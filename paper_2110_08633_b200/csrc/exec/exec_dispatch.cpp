@@ -146,6 +146,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       ain = 0;
       // don't clobber a resident buffer that the forward output will need: pick the older
       if (w.abuf_tag[0].job >= 0 && w.abuf_tag[1].job < 0) ain = 1;
+      if (w.abuf_dirty[ain] && !w.abuf_dirty[1 - ain]) ain = 1 - ain;  // keep live content resident
+      spill_boundary(w, ain, false);
       std::lock_guard<std::mutex> lk(peer_mu);
       w.abuf_tag[ain] = Tag{};
       w.abuf_tr[ain].before_write(w.down);
@@ -170,7 +172,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     const Tag gt{j, gmb, s, 1};
     gin = find_tag(w.gbd_tag, 2, gt);
     if (gin < 0) {
-      gin = 0;
+      gin = w.gbd_dirty[0] && !w.gbd_dirty[1] ? 1 : 0;
+      spill_boundary(w, gin, true);
       std::lock_guard<std::mutex> lk(peer_mu);
       w.gbd_tag[gin] = Tag{};
       w.gbd_tr[gin].before_write(w.down);
@@ -232,6 +235,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     io.act_in = ain >= 0 ? w.abuf[ain] : nullptr;
     if (!g.has_head) {
       aout = ain >= 0 ? 1 - ain : (w.abuf_tag[0].job < 0 ? 0 : (w.abuf_tag[1].job < 0 ? 1 : 0));
+      if (ain < 0 && w.abuf_dirty[aout] && !w.abuf_dirty[1 - aout]) aout = 1 - aout;
+      spill_boundary(w, aout, false);
       std::lock_guard<std::mutex> lk(peer_mu);
       w.abuf_tag[aout] = Tag{};  // being overwritten: no peer may copy the old content now
       w.abuf_tr[aout].before_write(w.comp);
@@ -242,7 +247,8 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     io.act_in = ain >= 0 ? w.abuf[ain] : nullptr;
     io.grad_in = gin >= 0 ? w.gbd[gin] : nullptr;
     if (s > 0) {
-      gout = gin >= 0 ? 1 - gin : 0;
+      gout = gin >= 0 ? 1 - gin : (w.gbd_dirty[0] && !w.gbd_dirty[1] ? 1 : 0);
+      spill_boundary(w, gout, true);
       std::lock_guard<std::mutex> lk(peer_mu);
       w.gbd_tag[gout] = Tag{};
       w.gbd_tr[gout].before_write(w.comp);
@@ -359,6 +365,28 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   }
 
   // ---- ActDemote + GradOffload (up) ---------------------------------------------------
+  // Write-back jobs (every task on this GPU) keep boundary activations / gradients resident
+  // and demote them only if their buffer is reused before the last consumer (spill_boundary):
+  // B(s+1) reads activation s from here, B(s-1) gradient s-1. With two buffers per kind, the
+  // activations of all but the last two boundaries are reused by the forward before their
+  // backward, so those still go out eagerly right behind their producer (no stall later).
+  // The reference's transfers (the plan) are unchanged; only physical copies are elided.
+  if (!fwd) {  // B(s) was the last consumer of activation s-1 and of gradient s: dead now
+    for (int i = 0; i < 2; ++i) {
+      if (w.abuf_tag[i] == Tag{j, gmb, s - 1, 0}) w.abuf_dirty[i] = false;
+      if (w.gbd_tag[i] == Tag{j, gmb, s, 1}) w.gbd_dirty[i] = false;
+    }
+  }
+  if (aout >= 0 && hj.write_back && s >= k - 3) {
+    w.abuf_dirty[aout] = true;
+    w.st.elided_act_bytes += static_cast<double>(act_bytes);
+    aout = -1;
+  }
+  if (gout >= 0 && hj.write_back) {
+    w.gbd_dirty[gout] = true;
+    w.st.elided_act_bytes += static_cast<double>(act_bytes);
+    gout = -1;
+  }
   if (aout >= 0) {  // forward boundary activation -> checkpoint store
     Tracked& host = *hj.ckpt_tr[static_cast<size_t>(s)];
     w.abuf_tr[aout].before_read(w.up);
@@ -501,6 +529,28 @@ void ExecutorImpl::dynamic_dispatch(Worker& w, int pass) {
     }
     dyn.cv.notify_all();
   }
+}
+
+void ExecutorImpl::spill_boundary(Worker& w, int i, bool grad) {
+  bool& dirty = grad ? w.gbd_dirty[i] : w.abuf_dirty[i];
+  if (!dirty) return;
+  dirty = false;
+  const Tag t = grad ? w.gbd_tag[i] : w.abuf_tag[i];
+  if (t.job < 0) return;
+  HostJob& oj = jobs.at(t.job);
+  const size_t bytes = sizeof(float) * static_cast<size_t>(oj.n_act);
+  Tracked& dev = grad ? w.gbd_tr[i] : w.abuf_tr[i];
+  Tracked& host = grad ? *oj.grad_tr[static_cast<size_t>(t.idx)] : *oj.ckpt_tr[static_cast<size_t>(t.idx)];
+  float* dst = grad ? oj.grad[static_cast<size_t>(t.idx)] : oj.ckpt[static_cast<size_t>(t.idx)];
+  dev.before_read(w.up);
+  host.before_write(w.up);
+  check_cuda(xfer(dst, grad ? w.gbd[i] : w.abuf[i], bytes, cudaMemcpyDeviceToHost, w.up),
+             grad ? "grad spill d2h" : "act spill d2h");
+  host.after_write(w.up);
+  dev.after_read(w.up);
+  w.st.act_d2h_bytes += static_cast<double>(bytes);
+  w.st.d2h_bytes += static_cast<double>(bytes);
+  w.st.elided_act_bytes -= static_cast<double>(bytes);
 }
 
 }  // namespace spillsim

@@ -205,6 +205,10 @@ struct Worker {
   float* gbd[2] = {nullptr, nullptr};
   Tag gbd_tag[2];
   Tracked gbd_tr[2];
+  // write-back boundary buffers (write-back jobs): the content is live and not yet in the
+  // host checkpoint store; it is demoted only if the buffer is reused before its last consumer
+  bool abuf_dirty[2] = {false, false};
+  bool gbd_dirty[2] = {false, false};
   float* zbuf = nullptr;
   Tag z_tag;
   Tracked z_tr;
@@ -301,6 +305,9 @@ struct ExecutorImpl {
   // on the producer's GPU are copied device to device (NVLink) instead of through the host.
   std::mutex peer_mu;  // guards the act/grad buffer tags of every worker
   bool peer_fetch(Worker& w, float* dst, const Tag& want, bool grad, size_t bytes);
+  // demote a dirty boundary buffer (activation: grad = false, gradient: true) to the host
+  // checkpoint store of the job / boundary in its tag before the buffer is overwritten
+  void spill_boundary(Worker& w, int i, bool grad);
   // dynamic-time scheduling state (one scheduler per pass, shared by the GPU workers)
   struct Dynamic {
     std::mutex mu;
