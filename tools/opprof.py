@@ -6,7 +6,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2110_08633_b200 as P
 cfg = json.load(open(sys.argv[1]))
 extra = json.loads(sys.argv[2]) if len(sys.argv) > 2 else {}
-ex = P.Executor(cfg, gpus=1, passes=1, warmup_passes=1, **extra)
+extra.setdefault("gpus", 1)
+ex = P.Executor(cfg, passes=1, warmup_passes=1, **extra)
 ex.run(1, timed=False)
 r = ex.run(1)
 prof = r.get("op_profile_ms", {})
