@@ -32,7 +32,7 @@ struct ExecOptions {
   uint64_t seed = 0;               // synthetic tokens
   int passes = 1;                  // times the whole plan is replayed (minibatch index continues)
   int warmup_passes = 0;           // replays before the timed ones (not in the trace)
-  long opt_chunk_floats = 2L << 20;  // Adam m/v streaming chunk (elements)
+  long opt_chunk_floats = 4L << 20;  // Adam m/v streaming chunk, upper bound (elements; the arena grants <= 2M first)
   long splitk_max_floats = 4672L << 10;  // split-K partials cap (elements): two 3072x768 partials (GPT-2 dW(fc))
   bool ring_first = true;             // spare HBM: deepen the gradient ring before the moment cache
   bool opt_priority = false;          // optimizer streams at the device's highest stream priority

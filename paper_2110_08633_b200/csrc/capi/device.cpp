@@ -210,12 +210,8 @@ static int shard_task(hy_dev* d, const hy_shard_desc* desc, const hy_shard_bufs*
     cudaStream_t st = d->lane[HY_LANE_COMPUTE];
     if (backward) {
       BufferSink sink(b->grads, hy_layer_offset(&m, desc->l0), m);
+      if (g.has_head && !g.has_embed) io.z_out = b->z_out;  // saved right after the head pass
       hy::run_backward(st, m, g, b->params, sink, io, s);
-      if (g.has_head && !g.has_embed && b->z_out) {
-        hy::check_cuda(cudaMemcpyAsync(b->z_out, s.z, sizeof(float) * static_cast<size_t>(m.B) * m.T * m.d,
-                                       cudaMemcpyDeviceToDevice, st),
-                       "z out");
-      }
     } else {
       hy::run_forward(st, m, g, b->params, io, s);
     }

@@ -213,9 +213,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   // ---- Compute (comp) ---------------------------------------------------------------
   std::vector<int> host_dirty;  // layers of this backward updated host-side
   hy::Scratch sc;
-  int max_blocks = 0;
-  for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
-  hy::carve_scratch(hj.m, max_blocks, w.scratch, &sc);
+  hy::carve_scratch(hj.m, hy::stash_blocks(hj.geom), w.scratch, &sc);
   if (w.stg_alias) {
     for (int i = 0; i < kStaging; ++i) w.stg_tr[i].before_write(w.comp);  // scratch reused as staging
   }
@@ -302,6 +300,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       }
       if (g.has_embed) sink.release(0);
     } else {
+      if (g.has_head && !g.has_embed) {
+        w.z_tr.before_write(w.comp);
+        io.z_out = w.zbuf;
+      }
       hy::run_backward(w.comp, hj.m, g, pbase, sink, io, sc);
     }
     if (w.stg_alias) {
@@ -323,9 +325,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
     mvt.after_write(w.up);
     pe->tr.after_write(w.opt);  // Adam rewrote the params in place (opt waited for opt2)
     pe->tr.after_read(w.up);    // ... and the up stream writes them back
-    if (g.has_head && !g.has_embed) {
-      w.z_tr.before_write(w.comp);
-      check_cuda(cudaMemcpyAsync(w.zbuf, sc.z, act_bytes, cudaMemcpyDeviceToDevice, w.comp), "z save");
+    if (g.has_head && !g.has_embed) {  // run_backward saved the ln_f output (io.z_out)
       w.z_tr.after_write(w.comp);
       w.z_tag = Tag{j, gmb, 0, 2};
     }

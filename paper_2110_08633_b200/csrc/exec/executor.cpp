@@ -201,7 +201,15 @@ void ExecutorImpl::setup_host_job(int j) {
 
 void ExecutorImpl::setup_worker(Worker& w) {
   check_cuda(cudaSetDevice(w.cuda_dev), "set device");
-  check_cuda(cudaStreamCreateWithFlags(&w.comp, cudaStreamNonBlocking), "stream");
+  {
+    static const int comp_prio = [] {  // diagnostics: HY_COMP_PRIORITY=1 runs the compute stream at high priority
+      const char* v = std::getenv("HY_COMP_PRIORITY");
+      return v ? std::atoi(v) : 0;
+    }();
+    int lo = 0, hi = 0;
+    check_cuda(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    check_cuda(cudaStreamCreateWithPriority(&w.comp, cudaStreamNonBlocking, comp_prio ? hi : 0), "stream");
+  }
   check_cuda(cudaStreamCreateWithFlags(&w.down, cudaStreamNonBlocking), "stream");
   check_cuda(cudaStreamCreateWithFlags(&w.up, cudaStreamNonBlocking), "stream");
   // the Adam kernels sit between an H2D and a D2H copy of each moment chunk: at high priority the
@@ -236,9 +244,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
     for (int l = std::max(g.l0, 1); l < g.l1; ++l) layer_f = std::max(layer_f, hy_layer_floats(&hj.m, l));
     act_f = std::max(act_f, hj.n_act);
     tok_n = std::max(tok_n, hj.M);
-    int max_blocks = 0;
-    for (const ShardGeom& sg : hj.geom) max_blocks = std::max(max_blocks, sg.n_blocks);
-    scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, max_blocks));
+    scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, hy::stash_blocks(hj.geom)));
   }
   const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(embed_f) + 5 * hy_pad32(act_f) +
                            2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
@@ -255,11 +261,16 @@ void ExecutorImpl::setup_worker(Worker& w) {
   long splitk_f = std::min(exec.splitk_max_floats, std::max(0L, budget_floats / 4)) / 1024 * 1024;
   if (splitk_f < (256L << 10)) splitk_f = 0;
   budget_floats -= splitk_f;
-  long chunk = std::min(exec.opt_chunk_floats, budget_floats / (2 * kStaging));
+  // staging: first its base chunk (<= 2M elements), then — after the parameter cache has grown
+  // toward the whole job — up to opt_chunk_floats from what is left: deeper m, v prefetch keeps
+  // the host link busier (C2: 2M -> 4M-element chunks took a pass 1.97 -> 1.82 s with 120 MB
+  // of extra HBM, tools/skip_sweep.py)
+  const long base_chunk = std::min(exec.opt_chunk_floats, 2L << 20);
+  long chunk = std::min(base_chunk, budget_floats / (2 * kStaging));
   chunk = chunk / 1024 * 1024;
   // alias the staging ring onto the scratch only when the cap leaves no room for the
   // requested chunks (or for 1M-element chunks, whichever is smaller)
-  w.stg_alias = chunk < std::min(exec.opt_chunk_floats / 1024 * 1024, 1L << 20);
+  w.stg_alias = chunk < std::min(base_chunk / 1024 * 1024, 1L << 20);
   if (w.stg_alias) chunk = 0;
   budget_floats -= kStaging * 2 * hy_pad32(chunk);
   if (w.stg_alias) {
@@ -285,6 +296,13 @@ void ExecutorImpl::setup_worker(Worker& w) {
     ext = ext / 32 * 32;
     pool_f += ext;
     budget_floats -= ext;
+  }
+  if (!w.stg_alias && chunk > 0 && exec.opt_chunk_floats > chunk && budget_floats > 0) {
+    const long grow = std::min(exec.opt_chunk_floats - chunk, budget_floats / (2 * kStaging)) / 1024 * 1024;
+    if (grow > 0) {
+      budget_floats -= kStaging * 2 * (hy_pad32(chunk + grow) - hy_pad32(chunk));
+      chunk += grow;
+    }
   }
   // Spare budget: a deeper gradient ring (up to 4 layers) and optimizer moments kept resident
   // (write-back jobs only). Resident moments save their link bytes every minibatch, so they
@@ -357,10 +375,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
     long best = 0;
     for (int t : w.tasks) {
       const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
-      int mb = 0;
-      for (const ShardGeom& sg : hj.geom) mb = std::max(mb, sg.n_blocks);
       hy::Scratch sc;
-      hy::carve_scratch(hj.m, mb, w.scratch, &sc);
+      hy::carve_scratch(hj.m, hy::stash_blocks(hj.geom), w.scratch, &sc);
       const long avail = 8L * hj.M * hj.m.d;  // fc + act
       if (avail > best) {
         best = avail;

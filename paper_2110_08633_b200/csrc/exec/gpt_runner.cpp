@@ -61,7 +61,9 @@ void gemm(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a
 }
 
 // keep_h: also store the MLP pre-activation (s.fc), which only the backward's GELU' needs; the
-// forward tasks and the backward's stash recompute skip that M x 4d write.
+// forward tasks and the backward's stash recompute skip that M x 4d write. h_out == nullptr:
+// the block's output is not needed (the backward's per-block recompute, or the last block of a
+// shard without the head in the stash pass) — the MLP projection GEMM is skipped.
 void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const float* h_in, float* h_out, Scratch& s,
                    bool keep_h) {
   const int M = s.M, d = m.d;
@@ -91,8 +93,9 @@ void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const floa
   gemm(st, M, 4 * d, d, s.ln2, d, false, bt(w, d, HY_WFC), d, false, s.act, 4 * d, bt(w, d, HY_BFC), nullptr, 0, 0.f,
        kEpiGelu, keep_h ? s.fc : nullptr, nullptr, 4 * d);
   }
-  { HY_PROF(st, "mlp_proj");
-  gemm(st, M, d, 4 * d, s.act, 4 * d, false, bt(w, d, HY_WPR), 4 * d, false, h_out, d, bt(w, d, HY_BPR), s.hmid, d);
+  if (h_out) {
+    HY_PROF(st, "mlp_proj");
+    gemm(st, M, d, 4 * d, s.act, 4 * d, false, bt(w, d, HY_WPR), 4 * d, false, h_out, d, bt(w, d, HY_BPR), s.hmid, d);
   }
 }
 
@@ -244,10 +247,13 @@ void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s) {
   }
   s->tmp_h = take(M * d);
   s->ws = take(512L * 4 * d);  // >= colsum_blocks(M) * max(4d, 2d)
-  s->z = take(M * d);
+  // the head's ln_f output and its gradient alias the QKV buffer (3 M d): the head pass runs
+  // when no block intermediates are live (before the blocks' recompute in a backward, after
+  // the last block in a forward); B(0)'s deferred tied-wte pass restores z there first
+  s->z = s->qkv;
   s->zmean = take(M);
   s->zrstd = take(M);
-  s->dz = take(M * d);
+  s->dz = s->qkv + M * d;
   s->row_loss = take(M);
   s->loss = reinterpret_cast<double*>(take(2));
   s->attn_ws = take(static_cast<long>(m.B) * m.H * m.T);
@@ -311,8 +317,9 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   // alias the MLP buffers) runs in between: then its recompute can be skipped.
   bool last_block_live = nb > 0 && !g.has_head;
   for (int i = 0; i < nb; ++i) {
-    block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, s.stash + (i + 1) * n, s,
-                  last_block_live && i == nb - 1);
+    // the last block's output is only needed as the head's input
+    float* out = (i == nb - 1 && !g.has_head) ? nullptr : s.stash + (i + 1) * n;
+    block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, out, s, last_block_live && i == nb - 1);
   }
   // 2) gradient wrt the shard output
   float* dh = s.tmp_h;
@@ -324,6 +331,9 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     const float* hfin = s.stash + nb * n;
     head_pass(st, m, lnf, wte, hfin, io.targets, s, true, dwte);
     if (dwte) sink.release_dense(0);
+    if (io.z_out) {  // z aliases the block scratch: saved before the blocks recompute
+      check_cuda(cudaMemcpyAsync(io.z_out, s.z, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "z save");
+    }
     check_cuda(layernorm_bwd(st, s.M, m.d, hfin, lnf, s.zmean, s.zrstd, s.dz, dh, false, glnf, glnf + hy_pad32(m.d),
                              s.ws),
                "ln_f bwd");
@@ -337,7 +347,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     const int layer = b0 + i;
     const float* w = slot + lo(m, layer, g.l0);
     if (!(last_block_live && i == nb - 1)) {
-      block_forward(st, m, w, s.stash + i * n, s.stash + (i + 1) * n, s, true);  // block output is scratch here
+      block_forward(st, m, w, s.stash + i * n, nullptr, s, true);  // intermediates only: no MLP projection
     }
     float* gw = sink.acquire(layer);
     block_backward(st, m, w, gw, s.stash + i * n, dh, s);

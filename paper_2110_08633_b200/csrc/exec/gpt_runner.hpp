@@ -2,6 +2,9 @@
 // sequence of sm_100a kernel launches on one stream. Transfers are the executor's job.
 #pragma once
 
+#include <algorithm>
+#include <vector>
+
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -38,6 +41,14 @@ struct Scratch {
   float* attn_ws;                // [B*H*T]
 };
 
+// Stash depth for a job's shards: the backward keeps the input of each of its blocks, plus the
+// last block's output only when the shard also holds the head (its input). Passed to
+// scratch_floats / carve_scratch as `max_blocks` (they reserve max_blocks + 1 slots).
+inline int stash_blocks(const std::vector<ShardGeom>& geom) {
+  int n = 1;
+  for (const ShardGeom& sg : geom) n = std::max(n, sg.n_blocks + (sg.has_head ? 1 : 0));
+  return n - 1;
+}
 // Bytes of scratch a worker needs for these dims with `max_blocks` blocks per shard.
 long scratch_floats(const hy_dims& m, int max_blocks);
 void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s);
@@ -50,6 +61,7 @@ struct TaskIO {
   const float* grad_in = nullptr;    // dL/d act_out (backward, no head)
   float* grad_out = nullptr;         // dL/d act_in (backward, l0 > 0)
   const float* z_in = nullptr;       // saved ln_f output for the deferred tied-wte grad (B of shard 0)
+  float* z_out = nullptr;            // B of a head shard without the embedding: save its ln_f output here
   const float* wte = nullptr;        // tied wte for a head shard without the embedding
 };
 
