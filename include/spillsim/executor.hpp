@@ -90,6 +90,7 @@ struct ExecStats {
   std::vector<double> pinned_bytes;
   int kernel_launches = 0;
   int elided_compute_tasks = 0;  // head-shard forwards folded into their backward
+  int stash_reuses = 0;          // backwards that skipped the recompute pass (their forward's stash survived)
   double setup_s = 0;
 };
 

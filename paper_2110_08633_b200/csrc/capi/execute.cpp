@@ -198,6 +198,7 @@ ojson session_result(Session& S, bool with_trace) {
   st["mv_resident_updates_per_pass"] = r.stats.mv_resident_updates / np;
   st["mv_cache_bytes"] = r.stats.mv_cache_bytes;
   st["p2p_bytes_per_pass"] = r.stats.p2p_bytes / np;
+  st["stash_reuses_per_pass"] = r.stats.stash_reuses / np;
   st["arena_bytes"] = r.stats.arena_bytes;
   st["pinned_bytes"] = r.stats.pinned_bytes;
   st["device_busy_s_last_pass"] = r.stats.device_busy_s.empty() ? 0.0 : r.stats.device_busy_s.back();

@@ -267,8 +267,11 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
                nx.direction == Direction::kBackward;
   }
   if (g_debug_skip == 2) skip_fwd = true;
+  const Tag my_stash{j, gmb, s, 4};
   if (fwd && !skip_fwd) {
+    io.keep_stash = !g.has_head && g.n_blocks > 0 && g_debug_skip == 0;
     hy::run_forward(w.comp, hj.m, g, pbase, io, sc);
+    if (g.n_blocks > 0 || g.has_embed) w.stash_tag = io.keep_stash ? my_stash : Tag{};
     if (g.has_head) {
       check_cuda(cudaMemcpyAsync(w.loss_dev + local, sc.loss, sizeof(double), cudaMemcpyDeviceToDevice, w.comp),
                  "loss copy");
@@ -304,7 +307,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
         w.z_tr.before_write(w.comp);
         io.z_out = w.zbuf;
       }
+      io.stash_ready = g.n_blocks > 0 && w.stash_tag == my_stash;
+      if (io.stash_ready) w.st.stash_reuses += 1;
       hy::run_backward(w.comp, hj.m, g, pbase, sink, io, sc);
+      if (g.n_blocks > 0 || g.has_embed) w.stash_tag = Tag{};  // the backward rewrote the stash
     }
     if (w.stg_alias) {
       for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // staging = scratch: after the backward

@@ -772,6 +772,7 @@ void Executor::run(int passes, bool timed, bool interval_log) {
       a.p2p_bytes += b.p2p_bytes;
       a.elided_act_bytes += b.elided_act_bytes;
       a.kernel_launches += b.kernel_launches;
+      a.stash_reuses += b.stash_reuses;
     }
   }
   double total = 0;

@@ -265,6 +265,22 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
   const int b0 = std::max(g.l0, 1);
   const int b1 = std::min(g.l1, m.L + 1);
   const bool write_out = !g.has_head && io.act_out != nullptr;
+  if (io.keep_stash && write_out && g.n_blocks > 0) {
+    // the backward's stash pass, done here: stash[i] = input of block b0+i, so this shard's
+    // backward can skip recomputing the forward if the stash survives until then
+    if (g.has_embed) {
+      check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d),
+                           s.stash),
+                 "embed");
+    } else {
+      check_cuda(cudaMemcpyAsync(s.stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
+    }
+    for (int i = 0; i < g.n_blocks; ++i) {
+      float* out = i == g.n_blocks - 1 ? io.act_out : s.stash + (i + 1) * n;
+      block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, out, s, false);
+    }
+    return;
+  }
   const float* cur = io.act_in;
   if (g.has_embed) {
     float* dst = (write_out && g.n_blocks == 0) ? io.act_out : s.tmp_h;
@@ -306,20 +322,25 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     s.dz = saved_dz;
     sink.release_dense(0);
   }
-  // 1) recompute: stash[i] = input of block b0+i; stash[nb] = shard output.
-  if (g.has_embed) {
-    check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), s.stash),
-               "embed");
-  } else {
-    check_cuda(cudaMemcpyAsync(s.stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
-  }
+  // 1) recompute: stash[i] = input of block b0+i; stash[nb] = shard output (head shards) —
+  //    unless this shard's forward left its block inputs there (io.stash_ready).
   // The last block's intermediates survive in scratch unless the head pass (whose logits
   // alias the MLP buffers) runs in between: then its recompute can be skipped.
-  bool last_block_live = nb > 0 && !g.has_head;
-  for (int i = 0; i < nb; ++i) {
-    // the last block's output is only needed as the head's input
-    float* out = (i == nb - 1 && !g.has_head) ? nullptr : s.stash + (i + 1) * n;
-    block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, out, s, last_block_live && i == nb - 1);
+  bool last_block_live = nb > 0 && !g.has_head && !io.stash_ready;
+  // a head-only shard reads its input in place (the stash keeps another shard's block inputs)
+  const bool head_only = nb == 0 && !g.has_embed;
+  if (!io.stash_ready && !head_only) {
+    if (g.has_embed) {
+      check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), s.stash),
+                 "embed");
+    } else {
+      check_cuda(cudaMemcpyAsync(s.stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
+    }
+    for (int i = 0; i < nb; ++i) {
+      // the last block's output is only needed as the head's input
+      float* out = (i == nb - 1 && !g.has_head) ? nullptr : s.stash + (i + 1) * n;
+      block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, out, s, last_block_live && i == nb - 1);
+    }
   }
   // 2) gradient wrt the shard output
   float* dh = s.tmp_h;
@@ -328,7 +349,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     float* glnf = sink.acquire(m.L + 1);
     const float* wte = g.has_embed ? slot : (io.wte ? io.wte : slot + g.wte_offset);
     float* dwte = g.has_embed ? gembed : nullptr;  // otherwise deferred to shard 0 via z
-    const float* hfin = s.stash + nb * n;
+    const float* hfin = head_only ? io.act_in : s.stash + nb * n;
     head_pass(st, m, lnf, wte, hfin, io.targets, s, true, dwte);
     if (dwte) sink.release_dense(0);
     if (io.z_out) {  // z aliases the block scratch: saved before the blocks recompute

@@ -62,6 +62,8 @@ struct TaskIO {
   float* grad_out = nullptr;         // dL/d act_in (backward, l0 > 0)
   const float* z_in = nullptr;       // saved ln_f output for the deferred tied-wte grad (B of shard 0)
   float* z_out = nullptr;            // B of a head shard without the embedding: save its ln_f output here
+  bool keep_stash = false;           // forward (no head): leave each block's input in the stash
+  bool stash_ready = false;          // backward: the stash holds this shard's block inputs (its forward's)
   const float* wte = nullptr;        // tied wte for a head shard without the embedding
 };
 
