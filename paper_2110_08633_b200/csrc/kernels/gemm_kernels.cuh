@@ -113,6 +113,29 @@ __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n
   return t;
 }
 
+// L2 prefetch of the global operands a tile's epilogue reads (the residual R, GELU's
+// pre-activation Hin, C when beta != 0): each epilogue warp issues one bulk prefetch per lane
+// for its 32 rows as soon as it is waiting for the tile's accumulator, so the loads hit L2
+// instead of HBM once the main loop is done.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(p)), "r"(bytes)
+               : "memory");
+}
+template <int BN, int MODE>
+__device__ __forceinline__ void prefetch_epilogue_rows(const GemmEpilogue& epi, const GemmBatch& bat,
+                                                       const TileInfo& ti, int row, int M, int N) {
+  if (row >= M) return;
+  const int cols = min(BN, N - ti.n0);
+  const uint32_t bytes = static_cast<uint32_t>(cols * 4) & ~15u;
+  if (cols <= 0 || bytes == 0) return;
+  if (MODE == kEpiGeluBwd && epi.Hin) bulk_prefetch_l2(epi.Hin + static_cast<long>(row) * epi.ldhi + ti.n0, bytes);
+  if (MODE == kEpiStore && epi.R) bulk_prefetch_l2(epi.R + static_cast<long>(row) * epi.ldr + ti.n0, bytes);
+  if (MODE == kEpiStore && epi.beta != 0.f) {
+    const float* c = epi.C + ti.z1 * bat.c_s1 + ti.z2 * bat.c_s2;
+    bulk_prefetch_l2(c + static_cast<long>(row) * epi.ldc + ti.n0, bytes);
+  }
+}
+
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
@@ -486,6 +509,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       const int acc = local & 1;
+      prefetch_epilogue_rows<BN, MODE>(epi, bat, ti, ti.m0 + static_cast<int>(q * 32 + lane_id()), M, N);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       ++local;
       tc_fence_after();
@@ -668,6 +692,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
       const int acc = local & 1;
+      prefetch_epilogue_rows<BN, MODE>(epi, bat, ti, ti.m0 + static_cast<int>(q * 32 + lane_id()), M, N);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       ++local;
       tc_fence_after();
