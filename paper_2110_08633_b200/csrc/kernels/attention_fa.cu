@@ -181,6 +181,18 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
 constexpr int kFwdSmem = 32768 + 2 * 16384 + 2 * 16384 + 128 + 1024;
 constexpr float kRescaleLog2 = 8.0f;
 
+#ifdef HY_ATTN_TRACE  // diagnostics build (tools/attn_trace.cu): per-tile timestamps of CTA 0
+__device__ unsigned long long g_attn_trace[8][256];
+#define ATTN_TRACE(slot, g)                                                 \
+  do {                                                                      \
+    if (blockIdx.x == 0 && (g) < 256) g_attn_trace[slot][g] = clock64(); \
+  } while (0)
+#else
+#define ATTN_TRACE(slot, g) \
+  do {                      \
+  } while (0)
+#endif
+
 struct FwdUnits {
   int nqt, BH, U, G;  // query tiles per (b, h), batch*heads, units, CTAs
   // unit -> (bh, qt): longest tiles first
@@ -309,6 +321,7 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
             for (int kk = 0; kk < 8; ++kk)
               mma_tf32(tS, desc_k(sQ, kk, 16384), desc_k(sK0 + sb * 16384, kk, 8192), idS, kk > 0);
             mma_commit(&bs[sb]);
+            ATTN_TRACE(0, g);
             advance(cs);
             progressed = true;
           }
@@ -321,6 +334,7 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
             for (int kk = 0; kk < 8; ++kk)
               mma_tf32_ts(tO, tP + kk * 8, desc_mn(sV0 + sb * 16384, kk), idPV, (cp.j | kk) > 0);
             mma_commit(&bpv[sb]);
+            ATTN_TRACE(1, g);
             advance(cp);
             progressed = true;
           }
@@ -343,10 +357,13 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
       float m_used = -FLT_MAX, l_run = 0.f;  // m_used: scaled (log2-domain) max the exponentials use
       for (int j = 0; j < nkt; ++j, ++g) {
         const int k0 = j * 64, s_ = g & 1;
+        if (tid == 0) ATTN_TRACE(2, g);
         mbar_wait(&bs[s_], (g >> 1) & 1);
+        if (tid == 0) ATTN_TRACE(3, g);
         tc_fence_after();
         float s[64];
         tmem_ld64(tbase + s_ * 64 + lane_off, s);
+        if (tid == 0) ATTN_TRACE(4, g);
         tc_fence_before();
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(&bsf[s_]);  // S buffer free for S(g+2)
@@ -377,6 +394,7 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
           }
         }
         l_run = l_run * alpha + ((sum4[0] + sum4[1]) + (sum4[2] + sum4[3]));
+        if (tid == 0) ATTN_TRACE(5, g);
         if (j > 0) {  // PV(g-1) landed: P free, O final up to tile j-1
           mbar_wait(&bpv[(g - 1) & 1], ((g - 1) >> 1) & 1);
           tc_fence_after();
@@ -389,12 +407,14 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
             tmem_st_x32(tO + lane_off + 32, o + 32);
           }
         }
+        if (tid == 0) ATTN_TRACE(6, g);
         tmem_st_x32(tP + lane_off, s);
         tmem_st_x32(tP + lane_off + 32, s + 32);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane_id() == 0) mbar_arrive(bp);
+        if (tid == 0) ATTN_TRACE(7, g);
       }
       // unit epilogue: O / l once the last PV has landed (the next unit's first PV, which
       // overwrites O, is only issued after these rows have stored its P, i.e. after this read)
