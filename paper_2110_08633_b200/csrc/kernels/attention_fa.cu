@@ -244,7 +244,11 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
   const uint32_t tbase = *tslot;
   const uint32_t tP = tbase + 128, tO = tbase + 192;
   if (warp == 5) {
-    if (lane_id() == 0) {  // loader
+    // two independent loader lanes: lane 0 streams Q and K (K(g) once S(g-2) has read its
+    // buffer), lane 1 streams V (V(g) once PV(g-2) has) — one lane for both made every K wait
+    // behind the previous V's PV, which left S(g+2) without its K (tools/attn_trace.cu)
+    const int ln = lane_id();
+    if (ln < 2) {
       int g = 0;
       for (int r = 0;; ++r) {
         const int u = W.nth(c, r);
@@ -252,24 +256,29 @@ __global__ void __launch_bounds__(192, 2) attn_fwd_kernel(const __grid_constant_
         int bh, qt;
         W.unit(u, bh, qt);
         const int b = bh / H, h = bh % H, row0 = b * T;
-        if (g > 0) mbar_wait(&bs[(g - 1) & 1], ((g - 1) >> 1) & 1);  // previous unit's last S: Q free
-        mbar_expect_tx(bq, 32768);
-        tma_load_2d(sQ, &mq, bq, h * HD, row0 + qt * 128);
-        tma_load_2d(sQ + 16384, &mq, bq, h * HD + 32, row0 + qt * 128);
+        if (ln == 0) {
+          if (g > 0) mbar_wait(&bs[(g - 1) & 1], ((g - 1) >> 1) & 1);  // previous unit's last S: Q free
+          mbar_expect_tx(bq, 32768);
+          tma_load_2d(sQ, &mq, bq, h * HD, row0 + qt * 128);
+          tma_load_2d(sQ + 16384, &mq, bq, h * HD + 32, row0 + qt * 128);
+        }
         const int nkt = nkt_of(qt);
         for (int j = 0; j < nkt; ++j, ++g) {
           const int s = g & 1;
-          if (g >= 2) mbar_wait(&bs[s], ((g - 2) >> 1) & 1);  // S(g-2) read K(g-2)
-          uint8_t* dk = sK0 + s * 16384;
-          mbar_expect_tx(&bk[s], 16384);
-          tma_load_2d(dk, &mk, &bk[s], D + h * HD, row0 + j * 64);
-          tma_load_2d(dk + 8192, &mk, &bk[s], D + h * HD + 32, row0 + j * 64);
-          if (g >= 2) mbar_wait(&bpv[s], ((g - 2) >> 1) & 1);  // PV(g-2) read V(g-2)
-          uint8_t* dv = sV0 + s * 16384;
-          mbar_expect_tx(&bv[s], 16384);
-          for (int kb = 0; kb < 2; ++kb)
-            for (int jn = 0; jn < 2; ++jn)
-              tma_load_2d(dv + kb * 8192 + jn * 4096, &mv, &bv[s], 2 * D + h * HD + 32 * jn, row0 + j * 64 + 32 * kb);
+          if (ln == 0) {
+            if (g >= 2) mbar_wait(&bs[s], ((g - 2) >> 1) & 1);  // S(g-2) read K(g-2)
+            uint8_t* dk = sK0 + s * 16384;
+            mbar_expect_tx(&bk[s], 16384);
+            tma_load_2d(dk, &mk, &bk[s], D + h * HD, row0 + j * 64);
+            tma_load_2d(dk + 8192, &mk, &bk[s], D + h * HD + 32, row0 + j * 64);
+          } else {
+            if (g >= 2) mbar_wait(&bpv[s], ((g - 2) >> 1) & 1);  // PV(g-2) read V(g-2)
+            uint8_t* dv = sV0 + s * 16384;
+            mbar_expect_tx(&bv[s], 16384);
+            for (int kb = 0; kb < 2; ++kb)
+              for (int jn = 0; jn < 2; ++jn)
+                tma_load_2d(dv + kb * 8192 + jn * 4096, &mv, &bv[s], 2 * D + h * HD + 32 * jn, row0 + j * 64 + 32 * kb);
+          }
         }
       }
     }
