@@ -309,8 +309,11 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
       }
       io.stash_ready = g.n_blocks > 0 && w.stash_tag == my_stash;
       if (io.stash_ready) w.st.stash_reuses += 1;
+      const hy::StashPlan sp = hy::stash_plan(hj.geom);
+      const bool own_region = g.has_head && sp.head_offset > 0;  // the head's stash after the others'
+      if (own_region) io.head_stash = sc.stash + static_cast<long>(sp.head_offset) * hj.n_act;
       hy::run_backward(w.comp, hj.m, g, pbase, sink, io, sc);
-      if (g.n_blocks > 0 || g.has_embed) w.stash_tag = Tag{};  // the backward rewrote the stash
+      if ((g.n_blocks > 0 || g.has_embed) && !own_region) w.stash_tag = Tag{};  // the backward rewrote the stash
     }
     if (w.stg_alias) {
       for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // staging = scratch: after the backward

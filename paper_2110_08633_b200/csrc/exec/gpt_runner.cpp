@@ -329,17 +329,18 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   bool last_block_live = nb > 0 && !g.has_head && !io.stash_ready;
   // a head-only shard reads its input in place (the stash keeps another shard's block inputs)
   const bool head_only = nb == 0 && !g.has_embed;
+  float* const stash = io.head_stash ? io.head_stash : s.stash;
   if (!io.stash_ready && !head_only) {
     if (g.has_embed) {
-      check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), s.stash),
+      check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), stash),
                  "embed");
     } else {
-      check_cuda(cudaMemcpyAsync(s.stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
+      check_cuda(cudaMemcpyAsync(stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
     }
     for (int i = 0; i < nb; ++i) {
       // the last block's output is only needed as the head's input
-      float* out = (i == nb - 1 && !g.has_head) ? nullptr : s.stash + (i + 1) * n;
-      block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, out, s, last_block_live && i == nb - 1);
+      float* out = (i == nb - 1 && !g.has_head) ? nullptr : stash + (i + 1) * n;
+      block_forward(st, m, slot + lo(m, b0 + i, g.l0), stash + i * n, out, s, last_block_live && i == nb - 1);
     }
   }
   // 2) gradient wrt the shard output
@@ -349,7 +350,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     float* glnf = sink.acquire(m.L + 1);
     const float* wte = g.has_embed ? slot : (io.wte ? io.wte : slot + g.wte_offset);
     float* dwte = g.has_embed ? gembed : nullptr;  // otherwise deferred to shard 0 via z
-    const float* hfin = head_only ? io.act_in : s.stash + nb * n;
+    const float* hfin = head_only ? io.act_in : stash + nb * n;
     head_pass(st, m, lnf, wte, hfin, io.targets, s, true, dwte);
     if (dwte) sink.release_dense(0);
     if (io.z_out) {  // z aliases the block scratch: saved before the blocks recompute
@@ -368,10 +369,10 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     const int layer = b0 + i;
     const float* w = slot + lo(m, layer, g.l0);
     if (!(last_block_live && i == nb - 1)) {
-      block_forward(st, m, w, s.stash + i * n, nullptr, s, true);  // intermediates only: no MLP projection
+      block_forward(st, m, w, stash + i * n, nullptr, s, true);  // intermediates only: no MLP projection
     }
     float* gw = sink.acquire(layer);
-    block_backward(st, m, w, gw, s.stash + i * n, dh, s);
+    block_backward(st, m, w, gw, stash + i * n, dh, s);
     sink.release(layer);
   }
   // 4) embedding: token rows of wte and wpe

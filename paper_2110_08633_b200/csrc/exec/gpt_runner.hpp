@@ -41,14 +41,32 @@ struct Scratch {
   float* attn_ws;                // [B*H*T]
 };
 
-// Stash depth for a job's shards: the backward keeps the input of each of its blocks, plus the
-// last block's output only when the shard also holds the head (its input). Passed to
-// scratch_floats / carve_scratch as `max_blocks` (they reserve max_blocks + 1 slots).
-inline int stash_blocks(const std::vector<ShardGeom>& geom) {
-  int n = 1;
-  for (const ShardGeom& sg : geom) n = std::max(n, sg.n_blocks + (sg.has_head ? 1 : 0));
-  return n - 1;
+// Stash layout for a job's shards: a backward keeps the input of each of its blocks (plus, for
+// the head shard, its last block's output: the head's input). The head shard's stash sits after
+// the deepest other shard's (when it has blocks and no embedding), so the forward stash of the
+// shard whose backward follows the head's survives it (StashPlan::head_offset; TaskIO::head_stash).
+struct StashPlan {
+  int head_offset = 0;  // slot where the head shard's stash starts (0: shared with the others)
+  int slots = 1;
+};
+inline StashPlan stash_plan(const std::vector<ShardGeom>& geom) {
+  StashPlan p;
+  int nohead = 0, head = 0;
+  bool separate = false;
+  for (const ShardGeom& sg : geom) {
+    if (sg.has_head) {
+      head = sg.n_blocks + 1;
+      separate = sg.n_blocks > 0 && !sg.has_embed;
+    } else {
+      nohead = std::max(nohead, sg.n_blocks);
+    }
+  }
+  p.head_offset = separate ? nohead : 0;
+  p.slots = std::max(1, separate ? nohead + head : std::max(nohead, head));
+  return p;
 }
+// Passed to scratch_floats / carve_scratch as `max_blocks` (they reserve max_blocks + 1 slots).
+inline int stash_blocks(const std::vector<ShardGeom>& geom) { return stash_plan(geom).slots - 1; }
 // Bytes of scratch a worker needs for these dims with `max_blocks` blocks per shard.
 long scratch_floats(const hy_dims& m, int max_blocks);
 void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s);
@@ -63,6 +81,7 @@ struct TaskIO {
   const float* z_in = nullptr;       // saved ln_f output for the deferred tied-wte grad (B of shard 0)
   float* z_out = nullptr;            // B of a head shard without the embedding: save its ln_f output here
   bool keep_stash = false;           // forward (no head): leave each block's input in the stash
+  float* head_stash = nullptr;       // backward of the head shard: its own stash region (StashPlan)
   bool stash_ready = false;          // backward: the stash holds this shard's block inputs (its forward's)
   const float* wte = nullptr;        // tied wte for a head shard without the embedding
 };
