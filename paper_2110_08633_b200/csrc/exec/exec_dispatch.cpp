@@ -268,10 +268,28 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   }
   if (g_debug_skip == 2) skip_fwd = true;
   const Tag my_stash{j, gmb, s, 4};
+  // this shard's stash region: its own slice of stash_ext when the arena has room for one per
+  // shard (shards 1.., not the head), the head shard's after the others' (StashPlan), else the
+  // scratch's shared stash (region 0)
+  int stash_region = 0;
+  float* stash_base = sc.stash;
+  {
+    const hy::StashPlan sp = hy::stash_plan(hj.geom);
+    if (g.has_head && sp.head_offset > 0) {
+      stash_region = 1;
+      stash_base = sc.stash + static_cast<long>(sp.head_offset) * hj.n_act;
+    } else if (!g.has_head && s > 0 && w.stash_ext &&
+               static_cast<long>(hy::ext_stash_offset(hj.geom, s) + g.n_blocks) * hj.n_act <= w.stash_ext_floats) {
+      stash_region = 2 + s;
+      stash_base = w.stash_ext + static_cast<long>(hy::ext_stash_offset(hj.geom, s)) * hj.n_act;
+    }
+  }
+  io.stash = stash_base;
   if (fwd && !skip_fwd) {
     io.keep_stash = !g.has_head && g.n_blocks > 0 && g_debug_skip == 0;
     hy::run_forward(w.comp, hj.m, g, pbase, io, sc);
-    if (g.n_blocks > 0 || g.has_embed) w.stash_tag = io.keep_stash ? my_stash : Tag{};
+    // a forward without the kept stash ping-pongs through the shared stash's first slot
+    if (g.n_blocks > 0 || g.has_embed) w.stash_tags[io.keep_stash ? stash_region : 0] = io.keep_stash ? my_stash : Tag{};
     if (g.has_head) {
       check_cuda(cudaMemcpyAsync(w.loss_dev + local, sc.loss, sizeof(double), cudaMemcpyDeviceToDevice, w.comp),
                  "loss copy");
@@ -307,13 +325,10 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
         w.z_tr.before_write(w.comp);
         io.z_out = w.zbuf;
       }
-      io.stash_ready = g.n_blocks > 0 && w.stash_tag == my_stash;
+      io.stash_ready = g.n_blocks > 0 && w.stash_tags[stash_region] == my_stash;
       if (io.stash_ready) w.st.stash_reuses += 1;
-      const hy::StashPlan sp = hy::stash_plan(hj.geom);
-      const bool own_region = g.has_head && sp.head_offset > 0;  // the head's stash after the others'
-      if (own_region) io.head_stash = sc.stash + static_cast<long>(sp.head_offset) * hj.n_act;
       hy::run_backward(w.comp, hj.m, g, pbase, sink, io, sc);
-      if ((g.n_blocks > 0 || g.has_embed) && !own_region) w.stash_tag = Tag{};  // the backward rewrote the stash
+      if (g.n_blocks > 0 || g.has_embed) w.stash_tags[stash_region] = Tag{};  // consumed / rewritten
     }
     if (w.stg_alias) {
       for (int i = 0; i < kStaging; ++i) w.stg_tr[i].after_write(w.comp);  // staging = scratch: after the backward

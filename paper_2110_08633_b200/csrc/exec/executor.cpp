@@ -304,6 +304,17 @@ void ExecutorImpl::setup_worker(Worker& w) {
       chunk += grow;
     }
   }
+  // Per-shard stash regions (a forward's block inputs then survive until its shard's backward,
+  // which skips its recompute pass): next in line, ahead of the deeper ring and the moment cache —
+  // a shard's recompute costs a block forward per block, its moments only link time.
+  long stash_ext_f = 0;
+  for (int t : w.tasks) {
+    const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
+    stash_ext_f = std::max(stash_ext_f, static_cast<long>(hy::ext_stash_slots(hj.geom)) * hj.n_act);
+  }
+  stash_ext_f = hy_pad32(stash_ext_f);
+  if (stash_ext_f <= 0 || stash_ext_f > budget_floats || g_debug_skip != 0) stash_ext_f = 0;
+  budget_floats -= stash_ext_f;
   // Spare budget: a deeper gradient ring (up to 4 layers) and optimizer moments kept resident
   // (write-back jobs only). Resident moments save their link bytes every minibatch, so they
   // come first when the budget is tight (exec.ring_first = false); the ring takes the rest.
@@ -332,14 +343,15 @@ void ExecutorImpl::setup_worker(Worker& w) {
   if (std::getenv("HY_DEBUG_ARENA")) {  // diagnostics: where the capped HBM goes (MB)
     std::fprintf(stderr,
                  "arena dev %d: slots %.1f embed %.1f act %.1f scratch %.1f crow %.1f | ring %.1f splitk %.1f "
-                 "staging %.1f pool+ %.1f mv %.1f | left %.1f\n",
+                 "staging %.1f pool+ %.1f stash+ %.1f mv %.1f | left %.1f\n",
                  w.plan_dev, 8.0 * hy_pad32(slot_f) / 1e6, 4.0 * hy_pad32(embed_f) / 1e6, 20.0 * hy_pad32(act_f) / 1e6,
                  4.0 * hy_pad32(scratch_f) / 1e6, 4.0 * (all_write_back ? 2 : 3) * crow / 1e6, 4.0 * ring_f / 1e6,
                  4.0 * splitk_f / 1e6, 4.0 * kStaging * 2 * hy_pad32(chunk) / 1e6,
-                 4.0 * (pool_f - 2 * hy_pad32(slot_f)) / 1e6, 4.0 * mv_f / 1e6, 4.0 * budget_floats / 1e6);
+                 4.0 * (pool_f - 2 * hy_pad32(slot_f)) / 1e6, 4.0 * stash_ext_f / 1e6, 4.0 * mv_f / 1e6,
+                 4.0 * budget_floats / 1e6);
   }
   const long floats = base_floats + ring_f + splitk_f + kStaging * 2 * hy_pad32(chunk) + (pool_f - 2 * hy_pad32(slot_f)) +
-                      mv_f;
+                      stash_ext_f + mv_f;
   w.arena_bytes = floats * 4 + 4096;
   if (static_cast<double>(w.arena_bytes) > cap) {
     throw InfeasibleOOM("sharp-executor", "(all jobs on this device)", dev.device_id,
@@ -370,6 +382,8 @@ void ExecutorImpl::setup_worker(Worker& w) {
   w.scratch = take(scratch_f);
   w.splitk = splitk_f > 0 ? take(splitk_f) : nullptr;
   w.splitk_floats = splitk_f;
+  w.stash_ext = stash_ext_f > 0 ? take(stash_ext_f) : nullptr;
+  w.stash_ext_floats = stash_ext_f;
   if (w.stg_alias) {
     // staging inside the scratch fc/act block of the largest job on this GPU
     long best = 0;

@@ -185,9 +185,12 @@ struct Worker {
   // head shard's tasks (a D2D copy instead of reloading V*d floats over the host link)
   Tag gembed_tag;
   Tracked gembed_tr;
-  // {job, gmb, shard, 4}: the scratch stash holds that forward's block inputs (its backward
-  // may skip the recompute pass); cleared by any task that rewrites the stash
-  Tag stash_tag;
+  // per stash region (0: the scratch's shared stash, 1: the head shard's, 2 + s: shard s's own
+  // in stash_ext): {job, gmb, shard, 4} when it holds that forward's block inputs (its backward
+  // may skip the recompute pass); cleared by any task that rewrites the region
+  std::map<int, Tag> stash_tags;
+  float* stash_ext = nullptr;  // per-shard stash regions, when the cap leaves room for them
+  long stash_ext_floats = 0;
   // Parameter gradients: the embedding's in its own buffer, every other layer in a ring
   // (FIFO, released as each layer's Adam finishes reading), so the optimizer streams a
   // layer's state while the backward is still working on earlier layers.

@@ -268,16 +268,17 @@ void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const fl
   if (io.keep_stash && write_out && g.n_blocks > 0) {
     // the backward's stash pass, done here: stash[i] = input of block b0+i, so this shard's
     // backward can skip recomputing the forward if the stash survives until then
+    float* const stash = io.stash ? io.stash : s.stash;
     if (g.has_embed) {
       check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d),
-                           s.stash),
+                           stash),
                  "embed");
     } else {
-      check_cuda(cudaMemcpyAsync(s.stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
+      check_cuda(cudaMemcpyAsync(stash, io.act_in, n * sizeof(float), cudaMemcpyDeviceToDevice, st), "stash in");
     }
     for (int i = 0; i < g.n_blocks; ++i) {
-      float* out = i == g.n_blocks - 1 ? io.act_out : s.stash + (i + 1) * n;
-      block_forward(st, m, slot + lo(m, b0 + i, g.l0), s.stash + i * n, out, s, false);
+      float* out = i == g.n_blocks - 1 ? io.act_out : stash + (i + 1) * n;
+      block_forward(st, m, slot + lo(m, b0 + i, g.l0), stash + i * n, out, s, false);
     }
     return;
   }
@@ -329,7 +330,7 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
   bool last_block_live = nb > 0 && !g.has_head && !io.stash_ready;
   // a head-only shard reads its input in place (the stash keeps another shard's block inputs)
   const bool head_only = nb == 0 && !g.has_embed;
-  float* const stash = io.head_stash ? io.head_stash : s.stash;
+  float* const stash = io.stash ? io.stash : s.stash;
   if (!io.stash_ready && !head_only) {
     if (g.has_embed) {
       check_cuda(embed_fwd(st, s.M, m.T, m.d, io.tokens, slot, slot + hy_pad32(static_cast<long>(m.V) * m.d), stash),

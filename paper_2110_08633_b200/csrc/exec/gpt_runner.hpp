@@ -67,6 +67,16 @@ inline StashPlan stash_plan(const std::vector<ShardGeom>& geom) {
 }
 // Passed to scratch_floats / carve_scratch as `max_blocks` (they reserve max_blocks + 1 slots).
 inline int stash_blocks(const std::vector<ShardGeom>& geom) { return stash_plan(geom).slots - 1; }
+// Stash slots of shard s in the optional extension region (shards 1.., not the head) when
+// every shard keeps its own stash; ext_stash_slots(geom) is the region's size.
+inline int ext_stash_offset(const std::vector<ShardGeom>& geom, int s) {
+  int off = 0;
+  for (int t = 1; t < s; ++t) off += geom[static_cast<size_t>(t)].has_head ? 0 : geom[static_cast<size_t>(t)].n_blocks;
+  return off;
+}
+inline int ext_stash_slots(const std::vector<ShardGeom>& geom) {
+  return ext_stash_offset(geom, static_cast<int>(geom.size()));
+}
 // Bytes of scratch a worker needs for these dims with `max_blocks` blocks per shard.
 long scratch_floats(const hy_dims& m, int max_blocks);
 void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s);
@@ -81,7 +91,7 @@ struct TaskIO {
   const float* z_in = nullptr;       // saved ln_f output for the deferred tied-wte grad (B of shard 0)
   float* z_out = nullptr;            // B of a head shard without the embedding: save its ln_f output here
   bool keep_stash = false;           // forward (no head): leave each block's input in the stash
-  float* head_stash = nullptr;       // backward of the head shard: its own stash region (StashPlan)
+  float* stash = nullptr;            // this shard's stash region (default: the scratch's shared stash)
   bool stash_ready = false;          // backward: the stash holds this shard's block inputs (its forward's)
   const float* wte = nullptr;        // tied wte for a head shard without the embedding
 };
