@@ -3,6 +3,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <cfloat>
@@ -47,50 +48,74 @@ int sms() {
 // One warp per row; the row lives in registers (d <= 32 * 4 * kMaxVec).
 constexpr int kMaxVecAll = 32;  // d <= 4096
 
-template <int kMaxVec>
-__global__ void ln_fwd_kernel(int rows, int d, const float* __restrict__ x, const float* __restrict__ g,
-                              const float* __restrict__ b, float* __restrict__ y, float* __restrict__ mean_out,
-                              float* __restrict__ rstd_out) {
+// Row split over kSplit warps (<= kVec float4 per lane held in registers between the two
+// reductions), the parts' sums meeting in shared memory in a fixed order: more warps per SM
+// than a whole row per warp (8192 x 1600: 24.6 -> 22.5 us, L2-cold).
+template <int kVec, int kSplit>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(int rows, int d, const float* __restrict__ x,
+                                                     const float* __restrict__ g, const float* __restrict__ b,
+                                                     float* __restrict__ y, float* __restrict__ mean_out,
+                                                     float* __restrict__ rstd_out) {
+  constexpr int kRows = kWarpsPerBlock / kSplit;
+  __shared__ float red[2][kWarpsPerBlock];
   pdl_wait_and_trigger();
-  const int row = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kRows + warp / kSplit;
+  const int part = warp % kSplit, first = (warp / kSplit) * kSplit;
+  const bool live = row < rows;
   const int nv = d >> 2;
   const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long>(row) * d);
-  float4 buf[kMaxVec];
+  float4 buf[kVec];
   float s = 0.f;
+  if (live) {
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int i = lane + 32 * k;
-    if (i < nv) {
-      buf[k] = xr[i];
-      s += (buf[k].x + buf[k].y) + (buf[k].z + buf[k].w);
+    for (int k = 0; k < kVec; ++k) {
+      const int i = part * 32 + lane + 32 * kSplit * k;
+      if (i < nv) {
+        buf[k] = xr[i];
+        s += (buf[k].x + buf[k].y) + (buf[k].z + buf[k].w);
+      }
     }
   }
-  const float mu = warp_sum(s) / d;
+  s = warp_sum(s);
+  if (lane == 0) red[0][warp] = s;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int p = 0; p < kSplit; ++p) t += red[0][first + p];
+  const float mu = t / d;
   float q = 0.f;
+  if (live) {
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int i = lane + 32 * k;
-    if (i < nv) {
-      const float a = buf[k].x - mu, bb = buf[k].y - mu, c = buf[k].z - mu, e = buf[k].w - mu;
-      q += (a * a + bb * bb) + (c * c + e * e);
+    for (int k = 0; k < kVec; ++k) {
+      const int i = part * 32 + lane + 32 * kSplit * k;
+      if (i < nv) {
+        const float a = buf[k].x - mu, bb = buf[k].y - mu, c = buf[k].z - mu, e = buf[k].w - mu;
+        q += (a * a + bb * bb) + (c * c + e * e);
+      }
     }
   }
-  const float rs = rsqrtf(warp_sum(q) / d + 1e-5f);
+  q = warp_sum(q);
+  if (lane == 0) red[1][warp] = q;
+  __syncthreads();
+  if (!live) return;
+  float u = 0.f;
+#pragma unroll
+  for (int p = 0; p < kSplit; ++p) u += red[1][first + p];
+  const float rs = rsqrtf(u / d + 1e-5f);
   float4* yr = reinterpret_cast<float4*>(y + static_cast<long>(row) * d);
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* b4 = reinterpret_cast<const float4*>(b);
 #pragma unroll
-  for (int k = 0; k < kMaxVec; ++k) {
-    const int i = lane + 32 * k;
+  for (int k = 0; k < kVec; ++k) {
+    const int i = part * 32 + lane + 32 * kSplit * k;
     if (i < nv) {
       const float4 gg = g4[i], bb = b4[i];
       yr[i] = make_float4((buf[k].x - mu) * rs * gg.x + bb.x, (buf[k].y - mu) * rs * gg.y + bb.y,
                           (buf[k].z - mu) * rs * gg.z + bb.z, (buf[k].w - mu) * rs * gg.w + bb.w);
     }
   }
-  if (lane == 0) {
+  if (part == 0 && lane == 0) {
     mean_out[row] = mu;
     rstd_out[row] = rs;
   }
@@ -104,42 +129,81 @@ __global__ void ln_fwd_kernel(int rows, int d, const float* __restrict__ x, cons
 //                      ticket, fixed block order: deterministic), added into dg, db.
 // Each pass keeps many warps in flight per SM; the single-pass kernel below carried dγ/dβ
 // for a whole row per lane and ran at ~1.4 TB/s at d = 1600.
+// The row in registers, split over kDxSplit warps (each lane holds <= kVec float4 of x, dy and
+// the dx being accumulated into: ~70 registers at kVec 4, three 8-warp blocks per SM), so every
+// load of the row is in flight before its first use and the SM keeps 24 warps' worth of them;
+// the parts' row sums meet in shared memory. At d = 1600 this took the dx pass from 8 warps
+// per SM (a whole row per warp, 225 registers) to 24, and LayerNorm backward 91 -> 64 us.
+template <int kVec, int kDxSplit>
 __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(int rows, int d, const float* __restrict__ x,
                                                         const float* __restrict__ g, const float* __restrict__ mean,
                                                         const float* __restrict__ rstd, const float* __restrict__ dy,
                                                         float* __restrict__ dx, int accumulate) {
+  constexpr int kDxRows = kWarpsPerBlock / kDxSplit;  // rows per 256-thread block
+  __shared__ float2 red[kWarpsPerBlock];
   pdl_wait_and_trigger();
-  const int row = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * kDxRows + warp / kDxSplit;
+  const int part = warp % kDxSplit;
   const int nv = d >> 2;
+  const bool live = row < rows;
   const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long>(row) * d);
   const float4* dyr = reinterpret_cast<const float4*>(dy + static_cast<long>(row) * d);
   const float4* g4 = reinterpret_cast<const float4*>(g);
-  const float mu = mean[row], rs = rstd[row];
-  float s1 = 0.f, s2 = 0.f;
-  for (int i = lane; i < nv; i += 32) {
-    const float4 xv = xr[i], dv = dyr[i], gv = g4[i];
-    const float gx = dv.x * gv.x, gy = dv.y * gv.y, gz = dv.z * gv.z, gw = dv.w * gv.w;
-    s1 += (gx + gy) + (gz + gw);
-    s2 += (gx * (xv.x - mu) + gy * (xv.y - mu)) + (gz * (xv.z - mu) + gw * (xv.w - mu));
-  }
-  const float m1 = warp_sum(s1) / d, m2 = warp_sum(s2) * rs / d;
   float4* dxr = reinterpret_cast<float4*>(dx + static_cast<long>(row) * d);
-  for (int i = lane; i < nv; i += 32) {
-    const float4 xv = xr[i], dv = dyr[i], gv = g4[i];
-    float4 o = make_float4(rs * (dv.x * gv.x - m1 - (xv.x - mu) * rs * m2),
-                           rs * (dv.y * gv.y - m1 - (xv.y - mu) * rs * m2),
-                           rs * (dv.z * gv.z - m1 - (xv.z - mu) * rs * m2),
-                           rs * (dv.w * gv.w - m1 - (xv.w - mu) * rs * m2));
-    if (accumulate) {
-      const float4 p = dxr[i];
-      o.x += p.x;
-      o.y += p.y;
-      o.z += p.z;
-      o.w += p.w;
+  float4 xv[kVec], gv[kVec], pv[kVec];
+  float mu = 0.f, rs = 0.f, s1 = 0.f, s2 = 0.f;
+  if (live) {
+    mu = mean[row];
+    rs = rstd[row];
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+      const int i = part * 32 + lane + 32 * kDxSplit * k;
+      if (i < nv) {
+        xv[k] = xr[i];
+        gv[k] = dyr[i];
+        if (accumulate) pv[k] = dxr[i];
+      }
     }
-    dxr[i] = o;
+#pragma unroll
+    for (int k = 0; k < kVec; ++k) {
+      const int i = part * 32 + lane + 32 * kDxSplit * k;
+      if (i < nv) {
+        const float4 w = g4[i];
+        gv[k] = make_float4(gv[k].x * w.x, gv[k].y * w.y, gv[k].z * w.z, gv[k].w * w.w);  // dy * g
+        xv[k] = make_float4((xv[k].x - mu) * rs, (xv[k].y - mu) * rs, (xv[k].z - mu) * rs, (xv[k].w - mu) * rs);
+        s1 += (gv[k].x + gv[k].y) + (gv[k].z + gv[k].w);
+        s2 += (gv[k].x * xv[k].x + gv[k].y * xv[k].y) + (gv[k].z * xv[k].z + gv[k].w * xv[k].w);
+      }
+    }
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  if (lane == 0) red[warp] = make_float2(s1, s2);
+  __syncthreads();
+  if (!live) return;
+  float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+  for (int p = 0; p < kDxSplit; ++p) {  // fixed order: deterministic
+    const float2 r = red[(warp / kDxSplit) * kDxSplit + p];
+    t1 += r.x;
+    t2 += r.y;
+  }
+  const float m1 = t1 / d, m2 = t2 / d;
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = part * 32 + lane + 32 * kDxSplit * k;
+    if (i < nv) {
+      float4 o = make_float4(rs * (gv[k].x - m1 - xv[k].x * m2), rs * (gv[k].y - m1 - xv[k].y * m2),
+                             rs * (gv[k].z - m1 - xv[k].z * m2), rs * (gv[k].w - m1 - xv[k].w * m2));
+      if (accumulate) {
+        o.x += pv[k].x;
+        o.y += pv[k].y;
+        o.z += pv[k].z;
+        o.w += pv[k].w;
+      }
+      dxr[i] = o;
+    }
   }
 }
 
@@ -439,7 +503,7 @@ __global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const f
   const int r1 = min(M, r0 + rows_per_block);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (c < N) {
-#pragma unroll 4
+#pragma unroll 8
     for (int r = r0 + ty; r < r1; r += 8) {
       const float4 v = *reinterpret_cast<const float4*>(X + static_cast<long>(r) * ldx + c);
       acc.x += v.x;
@@ -1008,6 +1072,17 @@ int grid_for(long n, int block) {
 
 }  // namespace
 
+// Column-sum blocks per SM: enough 256-thread blocks that each SM keeps ~40 KB of loads in
+// flight (Little's law at ~6.5 TB/s); HY_COLSUM_WAVES overrides (diagnostics).
+int colsum_waves() {
+  static const int w = [] {
+    const char* e = std::getenv("HY_COLSUM_WAVES");
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 4;
+  }();
+  return w;
+}
+
 int colsum_blocks(int rows) {
   const int target = sms() * 2;
   return rows < target ? (rows > 0 ? rows : 1) : target;
@@ -1016,16 +1091,18 @@ int colsum_blocks(int rows) {
 cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b, float* y,
                           float* mean, float* rstd) {
   if (d % 4 || d > 4 * 32 * kMaxVecAll) return cudaErrorInvalidValue;
-  const int grid = (rows + kWarpsPerBlock - 1) / kWarpsPerBlock, block = 32 * kWarpsPerBlock;
+  if (rows <= 0) return cudaSuccess;
+  // d <= 1024: a warp per row (8 rows per block) measured faster at C2's 4096 x 768 (10.2 vs
+  // 12.3 us); wider rows: 4 warps per row, 2 rows per block
+  const dim3 grid((rows + 1) / 2), block(32 * kWarpsPerBlock);
+  count_launch();
   if (d <= 1024) {
-    count_launch();
-    check_launch(launch_pdl(ln_fwd_kernel<8>, dim3(grid), dim3(block), 0, s, rows, d, x, g, b, y, mean, rstd));
+    check_launch(launch_pdl(ln_fwd_kernel<8, 1>, dim3((rows + kWarpsPerBlock - 1) / kWarpsPerBlock), block, 0, s,
+                            rows, d, x, g, b, y, mean, rstd));
   } else if (d <= 2048) {
-    count_launch();
-    check_launch(launch_pdl(ln_fwd_kernel<16>, dim3(grid), dim3(block), 0, s, rows, d, x, g, b, y, mean, rstd));
+    check_launch(launch_pdl(ln_fwd_kernel<4, 4>, grid, block, 0, s, rows, d, x, g, b, y, mean, rstd));
   } else {
-    count_launch();
-    check_launch(launch_pdl(ln_fwd_kernel<32>, dim3(grid), dim3(block), 0, s, rows, d, x, g, b, y, mean, rstd));
+    check_launch(launch_pdl(ln_fwd_kernel<8, 4>, grid, block, 0, s, rows, d, x, g, b, y, mean, rstd));
   }
   return cudaGetLastError();
 }
@@ -1038,12 +1115,19 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
   if (d % 4 || d > 4 * 32 * kMaxVecAll) return cudaErrorInvalidValue;
   if (rows <= 0) return cudaSuccess;
   if (unsigned* tickets = colsum_tickets(s)) {
+    const int acc = accumulate_dx ? 1 : 0;
+    const dim3 block(32 * kWarpsPerBlock);
     count_launch();
-    check_launch(launch_pdl(ln_bwd_dx_kernel, dim3((rows + kWarpsPerBlock - 1) / kWarpsPerBlock),
-                            dim3(32 * kWarpsPerBlock), 0, s, rows, d, x, g, mean, rstd, dy, dx,
-                            accumulate_dx ? 1 : 0));
+    const dim3 grid((rows + 1) / 2);  // kWarpsPerBlock / 4 rows per block
+    if (d <= 1024) {
+      check_launch(launch_pdl(ln_bwd_dx_kernel<2, 4>, grid, block, 0, s, rows, d, x, g, mean, rstd, dy, dx, acc));
+    } else if (d <= 2048) {
+      check_launch(launch_pdl(ln_bwd_dx_kernel<4, 4>, grid, block, 0, s, rows, d, x, g, mean, rstd, dy, dx, acc));
+    } else {
+      check_launch(launch_pdl(ln_bwd_dx_kernel<8, 4>, grid, block, 0, s, rows, d, x, g, mean, rstd, dy, dx, acc));
+    }
     const int strips = (d + 127) / 128;
-    int nb = std::max(1, std::min(colsum_blocks(rows), (2 * sms() + strips - 1) / strips));
+    int nb = std::max(1, std::min(colsum_blocks(rows), (colsum_waves() * sms() + strips - 1) / strips));
     nb = std::min(nb, std::max(1, rows / 32));
     const int rpb = (rows + nb - 1) / nb;
     nb = (rows + rpb - 1) / rpb;
@@ -1104,8 +1188,8 @@ cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float
   unsigned* tickets = colsum_tickets(s);
   if (tickets && N % 4 == 0 && ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
       (reinterpret_cast<uintptr_t>(out) & 15) == 0 && strips <= 4096 && M > 0) {
-    // ~2 waves of blocks, >= 32 rows per block, <= colsum_blocks(M) partials (the ws size)
-    int nb = std::max(1, std::min(colsum_blocks(M), (2 * sms() + strips - 1) / strips));
+    // colsum_waves() blocks per SM, >= 32 rows per block, <= colsum_blocks(M) partials (the ws size)
+    int nb = std::max(1, std::min(colsum_blocks(M), (colsum_waves() * sms() + strips - 1) / strips));
     nb = std::min(nb, std::max(1, M / 32));
     const int rpb = (M + nb - 1) / nb;
     nb = (M + rpb - 1) / rpb;
