@@ -481,7 +481,12 @@ def run_hydra(args, cfg):
         # BASELINE shape (tests/test_baseline_shapes_gpu.py)
         out["variants"] = {}
         other = "bf16" if args.opt_state == "fp32" else "fp32"
-        for name, over in ((f"opt_state_{other}", {"opt_state": other}), ("precision_fp32", {"precision": "fp32"})):
+        # and (c) the "bf16" precision: block GEMMs on bf16 operands (tcgen05 kind::f16), parity
+        # against the bf16-emulating oracle in tests/test_baseline_shapes_gpu.py — alone and with
+        # bf16 Adam moments
+        for name, over in ((f"opt_state_{other}", {"opt_state": other}), ("precision_fp32", {"precision": "fp32"}),
+                           ("precision_bf16", {"precision": "bf16"}),
+                           ("precision_bf16_opt_state_bf16", {"precision": "bf16", "opt_state": "bf16"})):
             vex = P.Executor(cfg, **dict(req, **over))
             vex.run(args.warmup, timed=False)
             torch.cuda.synchronize()

@@ -102,6 +102,15 @@ int hy_gemm(void* stream, int M, int N, int K, const float* A, long lda, int a_m
             int b_mn, float* C, long ldc, const float* bias, const float* R, long ldr, float beta, int mode,
             float* Hout, const float* Hin, long ldh);
 
+/* Same with bf16 operands (bit patterns, uint16) on tcgen05 kind::f16, fp32 accumulate; leading
+ * dims multiples of 8. c_bf16 = 1 stores C as bf16 (beta must be 0). The "bf16" precision's
+ * block GEMMs. */
+int hy_gemm_bf16(void* stream, int M, int N, int K, const uint16_t* A, long lda, int a_mn, const uint16_t* B,
+                 long ldb, int b_mn, void* C, long ldc, int c_bf16, const float* bias, const float* R, long ldr,
+                 float beta, int mode, float* Hout, const float* Hin, long ldh);
+/* y = bf16(x) (round to nearest even), n % 8 == 0. */
+int hy_to_bf16(void* stream, long n, const float* x, uint16_t* y);
+
 int hy_layernorm_fwd(void* stream, int rows, int d, const float* x, const float* g, const float* b, float* y,
                      float* mean, float* rstd);
 int hy_layernorm_bwd(void* stream, int rows, int d, const float* x, const float* g, const float* mean,

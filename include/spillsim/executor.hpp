@@ -40,6 +40,7 @@ struct ExecOptions {
   bool opt_state_bf16 = false;       // Adam moments stored/streamed as bf16 (halves their link bytes)
   std::string params_out_dir;      // if set: final params of every executed job as job<j>.f32
   bool precision_fp32 = false;     // GEMMs as 3xTF32 (~fp32) instead of TF32
+  bool precision_bf16 = false;     // block GEMMs on bf16 operands (kind::f16), fp32 accumulate / residual / head
   double hbm_slack_bytes = 0;      // physical arena may exceed mem_bytes by this much (toy configs
                                    // whose cost model leaves no room for real activations)
   int debug_skip = 0;              // diagnostics: 1 skip host<->device copies, 2 skip shard compute

@@ -64,6 +64,26 @@ static void ukern_generic(int kc, const double* restrict a, const double* restri
   for (int r = 0; r < MR; ++r) for (int j = 0; j < NR; ++j) c[r * ldc + j] += acc[r][j];
 }
 
+/* round-to-nearest-even to bfloat16, kept in a float */
+static float bf16_rne(float x) {
+  uint32_t u;
+  memcpy(&u, &x, 4);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  u &= 0xFFFF0000u;
+  memcpy(&x, &u, 4);
+  return x;
+}
+
+/* "bf16" precision (oracle_set_bf16): the transformer blocks' GEMM operands are rounded to bf16
+ * (RNE) as they are packed — the operands the GPU's bf16 block path stores as bf16 (weights, LN
+ * outputs, attention output, GELU output, dh, dact, dqkv); accumulation stays fp64. g_round is
+ * set only inside block_fwd / block_bwd, so the head GEMMs and attention are unrounded, as on
+ * the GPU (paper_2110_08633_b200/csrc/exec/gpt_runner.cpp, block_forward_bf16). */
+static int g_bf16 = 0;
+static int g_round = 0;
+void oracle_set_bf16(int on) { g_bf16 = on != 0; }
+static inline double rd(float x) { return g_round ? (double)bf16_rne(x) : (double)x; }
+
 /* pack rows [0,n) x k [0,kc) of X (element (r,k) at X[r*sr + k*sk]) into panels of P rows:
  * out[(p*KC + k)*P + r], zero-padded to a multiple of P */
 static void pack(int n, int kc, const float* X, long sr, long sk, int P, int npanels, double* out) {
@@ -72,13 +92,13 @@ static void pack(int n, int kc, const float* X, long sr, long sk, int P, int npa
     if (sk == 1) {
       for (int r = 0; r < P; ++r) {
         const int i = p * P + r;
-        if (i < n) { const float* x = X + (long)i * sr; for (int k = 0; k < kc; ++k) o[k * P + r] = x[k]; }
+        if (i < n) { const float* x = X + (long)i * sr; for (int k = 0; k < kc; ++k) o[k * P + r] = rd(x[k]); }
         else for (int k = 0; k < kc; ++k) o[k * P + r] = 0.0;
       }
     } else {
       for (int k = 0; k < kc; ++k) {
         const float* x = X + (long)k * sk;
-        for (int r = 0; r < P; ++r) { const int i = p * P + r; o[k * P + r] = i < n ? x[(long)i * sr] : 0.0; }
+        for (int r = 0; r < P; ++r) { const int i = p * P + r; o[k * P + r] = i < n ? rd(x[(long)i * sr]) : 0.0; }
       }
     }
   }
@@ -381,6 +401,7 @@ static void cache_free(block_cache* c) {
 /* h_out = block(h_in); fills the cache */
 static void block_fwd(const hy_dims* m, const float* w, const float* h_in, float* h_out, block_cache* c) {
   const int R = m->B * m->T, d = m->d;
+  g_round = g_bf16;
   ln_fwd(R, d, h_in, BT(w, HY_LN1_G), BT(w, HY_LN1_B), c->ln1, c->mean1, c->rstd1);
   mm_nt(R, 3 * d, d, c->ln1, d, BT(w, HY_WQKV), d, c->qkv, 3 * d, BT(w, HY_BQKV), 0);
   attn_fwd(m, c->qkv, c->att);
@@ -394,6 +415,7 @@ static void block_fwd(const hy_dims* m, const float* w, const float* h_in, float
   mm_nt(R, d, 4 * d, c->act, 4 * d, BT(w, HY_WPR), 4 * d, h_out, d, BT(w, HY_BPR), 0);
 #pragma omp parallel for schedule(static)
   for (long i = 0; i < (long)R * d; ++i) h_out[i] += c->hmid[i];
+  g_round = 0;
 }
 
 /* dh (in: dL/dh_out, out: dL/dh_in); g: this block's gradient slice (+=) */
@@ -405,12 +427,16 @@ static void block_bwd(const hy_dims* m, const float* w, float* g, const float* h
   float* dln = falloc(n);
   float* datt = falloc(n);
   float* dqkv = falloc((long)R * 3 * d);
+  g_round = g_bf16;
   /* MLP: h_out = hmid + act W_pr^T + b_pr */
   mm_tn(d, 4 * d, R, dh, d, c->act, 4 * d, BT(g, HY_WPR), 4 * d, 1);
   colsum_acc(R, d, dh, BT(g, HY_BPR));
   mm_nn(R, 4 * d, d, dh, d, BT(w, HY_WPR), 4 * d, dact, 4 * d, 0);
 #pragma omp parallel for schedule(static)
-  for (long i = 0; i < (long)R * 4 * d; ++i) dact[i] = (float)(dact[i] * gelu_grad(c->fc[i]));
+  for (long i = 0; i < (long)R * 4 * d; ++i) {
+    const float v = (float)(dact[i] * gelu_grad(c->fc[i]));
+    dact[i] = g_bf16 ? bf16_rne(v) : v; /* the GPU stores dact as bf16; the bias grad sums those */
+  }
   mm_tn(4 * d, d, R, dact, 4 * d, c->ln2, d, BT(g, HY_WFC), d, 1);
   colsum_acc(R, 4 * d, dact, BT(g, HY_BFC));
   mm_nn(R, d, 4 * d, dact, 4 * d, BT(w, HY_WFC), d, dln, d, 0);
@@ -426,6 +452,7 @@ static void block_bwd(const hy_dims* m, const float* w, float* g, const float* h
   mm_nn(R, d, 3 * d, dqkv, 3 * d, BT(w, HY_WQKV), d, dln, d, 0);
   memcpy(dh, dhm, sizeof(float) * (size_t)n);
   ln_bwd(R, d, h_in, BT(w, HY_LN1_G), c->mean1, c->rstd1, dln, dh, BT(g, HY_LN1_G), BT(g, HY_LN1_B));
+  g_round = 0;
   free(dact); free(dhm); free(dln); free(datt); free(dqkv);
 }
 
@@ -562,15 +589,6 @@ int oracle_shard_bwd(const hy_dims* m, const float* params, float* grads, int l0
   return 0;
 }
 
-/* round-to-nearest-even to bfloat16, kept in a float */
-static float bf16_rne(float x) {
-  uint32_t u;
-  memcpy(&u, &x, 4);
-  u += 0x7FFFu + ((u >> 16) & 1u);
-  u &= 0xFFFF0000u;
-  memcpy(&x, &u, 4);
-  return x;
-}
 
 void oracle_adam_state(long n, float* p, const float* g, float* m, float* v, float lr, float beta1, float beta2,
                        float eps, float weight_decay, int step, int bf16_state) {

@@ -46,6 +46,9 @@ void oracle_adam_state(long n, float* p, const float* g, float* m, float* v, flo
 double oracle_train_step(const hy_dims* m, float* params, float* mom, float* var, int step, float lr,
                          const int32_t* tokens, const int32_t* targets);
 
+/* "bf16" precision: block GEMM operands rounded to bf16 (see gpt_oracle.c); 0 restores fp32. */
+void oracle_set_bf16(int on);
+
 void oracle_init_params(const hy_dims* m, uint64_t model_key, float* params);
 void oracle_make_tokens(const hy_dims* m, uint64_t seed, int job, int mb, int32_t* tokens, int32_t* targets);
 int oracle_threads(void);

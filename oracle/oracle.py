@@ -35,7 +35,13 @@ def lib():
         _lib.oracle_init_params.argtypes = [P, ctypes.c_uint64, P]
         _lib.oracle_make_tokens.argtypes = [P, ctypes.c_uint64, ctypes.c_int, ctypes.c_int, P, P]
         _lib.oracle_threads.restype = ctypes.c_int
+        _lib.oracle_set_bf16.argtypes = [ctypes.c_int]
     return _lib
+
+
+def set_bf16(on):
+    """Round the blocks' GEMM operands to bf16 (the GPU's "bf16" precision) in later calls."""
+    lib().oracle_set_bf16(int(bool(on)))
 
 
 def _p(a):

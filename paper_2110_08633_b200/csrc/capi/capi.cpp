@@ -185,6 +185,33 @@ int hy_gemm(void* stream, int M, int N, int K, const float* A, long lda, int a_m
                      "hy_gemm");
 }
 
+int hy_gemm_bf16(void* stream, int M, int N, int K, const uint16_t* A, long lda, int a_mn, const uint16_t* B,
+                 long ldb, int b_mn, void* C, long ldc, int c_bf16, const float* bias, const float* R, long ldr,
+                 float beta, int mode, float* Hout, const float* Hin, long ldh) {
+  hy::GemmEpilogue e;
+  e.C = static_cast<float*>(C);
+  e.ldc = ldc;
+  e.c16 = c_bf16 != 0;
+  e.bias = bias;
+  e.R = R;
+  e.ldr = ldr;
+  e.beta = beta;
+  e.mode = mode;
+  e.Hout = Hout;
+  e.ldho = ldh;
+  e.Hin = Hin;
+  e.ldhi = ldh;
+  return cuda_status(hy::gemm_bf16(static_cast<cudaStream_t>(stream), M, N, K,
+                                   reinterpret_cast<const __nv_bfloat16*>(A), lda, a_mn != 0,
+                                   reinterpret_cast<const __nv_bfloat16*>(B), ldb, b_mn != 0, e),
+                     "hy_gemm_bf16");
+}
+
+int hy_to_bf16(void* stream, long n, const float* x, uint16_t* y) {
+  return cuda_status(hy::to_bf16(static_cast<cudaStream_t>(stream), n, x, reinterpret_cast<__nv_bfloat16*>(y)),
+                     "hy_to_bf16");
+}
+
 int hy_layernorm_fwd(void* stream, int rows, int d, const float* x, const float* g, const float* b, float* y,
                      float* mean, float* rstd) {
   return cuda_status(hy::layernorm_fwd(static_cast<cudaStream_t>(stream), rows, d, x, g, b, y, mean, rstd),

@@ -108,8 +108,11 @@ std::unique_ptr<Session> make_session(const std::string& request) {
     };
   }
   const std::string prec = req.value("precision", std::string("tf32"));
-  if (prec != "tf32" && prec != "fp32") throw InvalidArgument("precision must be 'tf32' or 'fp32'");
+  if (prec != "tf32" && prec != "fp32" && prec != "bf16") {
+    throw InvalidArgument("precision must be 'tf32', 'fp32' or 'bf16'");
+  }
   ex.precision_fp32 = prec == "fp32";
+  ex.precision_bf16 = prec == "bf16";
   const std::string state = req.value("opt_state", std::string("fp32"));
   if (state != "fp32" && state != "bf16") throw InvalidArgument("opt_state must be 'fp32' or 'bf16'");
   ex.opt_state_bf16 = state == "bf16";

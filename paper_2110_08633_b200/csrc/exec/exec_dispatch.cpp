@@ -213,7 +213,7 @@ void ExecutorImpl::enqueue_task(Worker& w, int t, int pass) {
   // ---- Compute (comp) ---------------------------------------------------------------
   std::vector<int> host_dirty;  // layers of this backward updated host-side
   hy::Scratch sc;
-  hy::carve_scratch(hj.m, hy::stash_blocks(hj.geom), w.scratch, &sc);
+  hy::carve_scratch(hj.m, hy::stash_blocks(hj.geom), w.scratch, &sc, exec.precision_bf16);
   if (w.stg_alias) {
     for (int i = 0; i < kStaging; ++i) w.stg_tr[i].before_write(w.comp);  // scratch reused as staging
   }

@@ -244,7 +244,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
     for (int l = std::max(g.l0, 1); l < g.l1; ++l) layer_f = std::max(layer_f, hy_layer_floats(&hj.m, l));
     act_f = std::max(act_f, hj.n_act);
     tok_n = std::max(tok_n, hj.M);
-    scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, hy::stash_blocks(hj.geom)));
+    scratch_f = std::max(scratch_f, hy::scratch_floats(hj.m, hy::stash_blocks(hj.geom), exec.precision_bf16));
   }
   const long base_floats = 2 * hy_pad32(slot_f) + hy_pad32(embed_f) + 5 * hy_pad32(act_f) +
                            2 * hy_pad32(2 * tok_n) + hy_pad32(scratch_f) +
@@ -390,7 +390,7 @@ void ExecutorImpl::setup_worker(Worker& w) {
     for (int t : w.tasks) {
       const HostJob& hj = jobs.at(tasks[static_cast<size_t>(t)].t.job);
       hy::Scratch sc;
-      hy::carve_scratch(hj.m, hy::stash_blocks(hj.geom), w.scratch, &sc);
+      hy::carve_scratch(hj.m, hy::stash_blocks(hj.geom), w.scratch, &sc, exec.precision_bf16);
       const long avail = 8L * hj.M * hj.m.d;  // fc + act
       if (avail > best) {
         best = avail;
@@ -557,6 +557,7 @@ void ExecutorImpl::run_pass(int pass, bool timed, ExecResult& res, bool interval
         check_cuda(cudaSetDevice(w.cuda_dev), "set device");
         hy::gemm_set_splitk_workspace(w.splitk, w.splitk_floats);
         hy::gemm_set_precision_fp32(exec.precision_fp32);
+        hy::gemm_set_compute_bf16(exec.precision_bf16);
         g_debug_skip = exec.debug_skip;
         check_cuda(cudaDeviceSynchronize(), "pre-pass sync");
         w.ilog.reset();

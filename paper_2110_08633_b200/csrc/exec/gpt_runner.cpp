@@ -38,6 +38,11 @@ ShardGeom shard_geom(const hy_dims& m, int l0, int l1) {
 
 namespace {
 
+using bf16 = __nv_bfloat16;
+
+// floats of scratch holding one transformer block's parameters as bf16
+long w16_floats(const hy_dims& m) { return hy_pad32((hy_layer_floats(&m, 1) + 1) / 2); }
+
 inline long lo(const hy_dims& m, int layer, int l0) { return hy_layer_offset(&m, layer) - hy_layer_offset(&m, l0); }
 inline const float* bt(const float* w, int d, int t) { return w + hy_block_tensor_offset(d, t); }
 inline float* btw(float* w, int d, int t) { return w + hy_block_tensor_offset(d, t); }
@@ -60,12 +65,161 @@ void gemm(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a
   check_cuda(gemm_tf32(st, M, N, K, A, lda, amn, B, ldb, bmn, e), "gemm");
 }
 
+void gemm16(cudaStream_t st, int M, int N, int K, const bf16* A, long lda, bool amn, const bf16* B, long ldb, bool bmn,
+            void* C, long ldc, bool c16, const float* bias = nullptr, const float* R = nullptr, long ldr = 0,
+            float beta = 0.f, int mode = kEpiStore, float* hout = nullptr, const float* hin = nullptr, long ldh = 0) {
+  GemmEpilogue e;
+  e.C = static_cast<float*>(C);
+  e.ldc = ldc;
+  e.c16 = c16 ? 1 : 0;
+  e.bias = bias;
+  e.R = R;
+  e.ldr = ldr;
+  e.beta = beta;
+  e.mode = mode;
+  e.Hout = hout;
+  e.ldho = ldh;
+  e.Hin = hin;
+  e.ldhi = ldh;
+  check_cuda(gemm_bf16(st, M, N, K, A, lda, amn, B, ldb, bmn, e), "gemm bf16");
+}
+
+// The block's parameters as bf16 into s.w16 (same offsets as the fp32 block).
+const bf16* block_w16(cudaStream_t st, const hy_dims& m, const float* w, Scratch& s) {
+  HY_PROF(st, "w16");
+  check_cuda(to_bf16(st, hy_layer_floats(&m, 1), w, s.w16), "w16");
+  return s.w16;
+}
+inline const bf16* bt16(const bf16* w, int d, int t) { return w + hy_block_tensor_offset(d, t); }
+
+// bf16 views of the block scratch (Scratch::w16 comment).
+struct Views16 {
+  bf16 *ln1, *att, *ln2, *dh, *act, *dqkv;
+  float* datt;
+};
+inline Views16 views16(Scratch& s) {
+  const long n = static_cast<long>(s.M) * s.d;
+  Views16 v;
+  v.ln1 = reinterpret_cast<bf16*>(s.ln1);
+  v.att = v.ln1 + n;
+  v.ln2 = reinterpret_cast<bf16*>(s.ln2);
+  v.dh = v.ln2 + n;
+  v.act = reinterpret_cast<bf16*>(s.act);
+  v.datt = s.act;
+  v.dqkv = reinterpret_cast<bf16*>(s.act + n);
+  return v;
+}
+
+// "bf16" precision, the autocast split: every block GEMM reads bf16 operands (weights, LN
+// outputs, attention output, GELU output, and the gradients feeding dX / dW GEMMs) with fp32
+// accumulation and fp32 epilogues; the residual stream, LayerNorm statistics, attention
+// (TF32 flash kernels on fp32 Q/K/V), softmax-CE, the head and every parameter gradient stay
+// fp32. The CPU oracle's bf16 mode rounds exactly these operands (oracle/gpt_oracle.c).
+void block_forward_bf16(cudaStream_t st, const hy_dims& m, const float* w, const float* h_in, float* h_out,
+                        Scratch& s, bool keep_h) {
+  const int M = s.M, d = m.d;
+  const bf16* w16 = block_w16(st, m, w, s);
+  const Views16 v = views16(s);
+  { HY_PROF(st, "ln1");
+  check_cuda(layernorm_fwd(st, M, d, h_in, bt(w, d, HY_LN1_G), bt(w, d, HY_LN1_B), v.ln1, s.mean1, s.rstd1), "ln1");
+  }
+  { HY_PROF(st, "qkv");
+  gemm16(st, M, 3 * d, d, v.ln1, d, false, bt16(w16, d, HY_WQKV), d, false, s.qkv, 3 * d, false, bt(w, d, HY_BQKV));
+  }
+  { HY_PROF(st, "attn_fwd");
+  check_cuda(attention_fwd_fa(st, m.B, m.T, m.H, s.qkv, s.att, s.lse), "attn_fwd");
+  check_cuda(to_bf16(st, static_cast<long>(M) * d, s.att, v.att), "att16");
+  }
+  { HY_PROF(st, "o_proj");
+  gemm16(st, M, d, d, v.att, d, false, bt16(w16, d, HY_WO), d, false, s.hmid, d, false, bt(w, d, HY_BO), h_in, d);
+  }
+  { HY_PROF(st, "ln2");
+  check_cuda(layernorm_fwd(st, M, d, s.hmid, bt(w, d, HY_LN2_G), bt(w, d, HY_LN2_B), v.ln2, s.mean2, s.rstd2), "ln2");
+  }
+  { HY_PROF(st, "fc");
+  gemm16(st, M, 4 * d, d, v.ln2, d, false, bt16(w16, d, HY_WFC), d, false, v.act, 4 * d, true, bt(w, d, HY_BFC),
+         nullptr, 0, 0.f, kEpiGelu, keep_h ? s.fc : nullptr, nullptr, 4 * d);
+  }
+  if (h_out) {
+    HY_PROF(st, "mlp_proj");
+    gemm16(st, M, d, 4 * d, v.act, 4 * d, false, bt16(w16, d, HY_WPR), 4 * d, false, h_out, d, false, bt(w, d, HY_BPR),
+           s.hmid, d);
+  }
+}
+
+// Backward of block_forward_bf16 (its intermediates and s.w16 must be this block's).
+void block_backward_bf16(cudaStream_t st, const hy_dims& m, const float* w, float* gw, const float* h_in, float* dh,
+                         Scratch& s) {
+  const int M = s.M, d = m.d;
+  const long n = static_cast<long>(M) * d;
+  const bf16* w16 = s.w16;
+  const Views16 v = views16(s);
+  check_cuda(to_bf16(st, n, dh, v.dh), "dh16");
+  { HY_PROF(st, "bwd_dW_proj");
+  gemm16(st, d, 4 * d, M, v.dh, d, true, v.act, 4 * d, true, btw(gw, d, HY_WPR), 4 * d, false, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
+  check_cuda(colsum(st, M, d, dh, d, btw(gw, d, HY_BPR), true, s.ws), "colsum bpr");
+  }
+  bf16* dact = v.act;  // act is dead after dWpr
+  { HY_PROF(st, "bwd_dact");
+  gemm16(st, M, 4 * d, d, v.dh, d, false, bt16(w16, d, HY_WPR), 4 * d, true, dact, 4 * d, true, nullptr, nullptr, 0,
+         0.f, kEpiGeluBwd, nullptr, s.fc, 4 * d);
+  }
+  { HY_PROF(st, "bwd_dW_fc");
+  gemm16(st, 4 * d, d, M, dact, 4 * d, true, v.ln2, d, true, btw(gw, d, HY_WFC), d, false, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
+  check_cuda(colsum(st, M, 4 * d, dact, 4 * d, btw(gw, d, HY_BFC), true, s.ws), "colsum bfc");
+  }
+  float* dln2 = s.fc;  // fc dead after dact
+  { HY_PROF(st, "bwd_dln2");
+  gemm16(st, M, d, 4 * d, dact, 4 * d, false, bt16(w16, d, HY_WFC), d, true, dln2, d, false);
+  }
+  { HY_PROF(st, "bwd_ln");
+  check_cuda(layernorm_bwd(st, M, d, s.hmid, bt(w, d, HY_LN2_G), s.mean2, s.rstd2, dln2, dh, true,
+                           btw(gw, d, HY_LN2_G), btw(gw, d, HY_LN2_B), s.ws),
+             "ln2 bwd");
+  }
+  check_cuda(to_bf16(st, n, dh, v.dh), "dh16");
+  { HY_PROF(st, "bwd_dW_o");
+  gemm16(st, d, d, M, v.dh, d, true, v.att, d, true, btw(gw, d, HY_WO), d, false, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
+  check_cuda(colsum(st, M, d, dh, d, btw(gw, d, HY_BO), true, s.ws), "colsum bo");
+  }
+  { HY_PROF(st, "bwd_datt");
+  gemm16(st, M, d, d, v.dh, d, false, bt16(w16, d, HY_WO), d, true, v.datt, d, false);
+  }
+  float* dqkv = s.fc;
+  { HY_PROF(st, "attn_bwd");
+  check_cuda(attention_bwd_fa(st, m.B, m.T, m.H, s.qkv, s.att, v.datt, s.lse, dqkv, s.attn_ws), "attn bwd");
+  check_cuda(to_bf16(st, 3 * n, dqkv, v.dqkv), "dqkv16");
+  }
+  { HY_PROF(st, "bwd_dW_qkv");
+  gemm16(st, 3 * d, d, M, v.dqkv, 3 * d, true, v.ln1, d, true, btw(gw, d, HY_WQKV), d, false, nullptr, nullptr, 0, 1.f);
+  }
+  { HY_PROF(st, "bwd_bias");
+  check_cuda(colsum(st, M, 3 * d, dqkv, 3 * d, btw(gw, d, HY_BQKV), true, s.ws), "colsum bqkv");
+  }
+  float* dln1 = s.hmid;
+  { HY_PROF(st, "bwd_dln1");
+  gemm16(st, M, d, 3 * d, v.dqkv, 3 * d, false, bt16(w16, d, HY_WQKV), d, true, dln1, d, false);
+  }
+  { HY_PROF(st, "bwd_ln");
+  check_cuda(layernorm_bwd(st, M, d, h_in, bt(w, d, HY_LN1_G), s.mean1, s.rstd1, dln1, dh, true,
+                           btw(gw, d, HY_LN1_G), btw(gw, d, HY_LN1_B), s.ws),
+             "ln1 bwd");
+  }
+}
+
 // keep_h: also store the MLP pre-activation (s.fc), which only the backward's GELU' needs; the
 // forward tasks and the backward's stash recompute skip that M x 4d write. h_out == nullptr:
 // the block's output is not needed (the backward's per-block recompute, or the last block of a
 // shard without the head in the stash pass) — the MLP projection GEMM is skipped.
 void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const float* h_in, float* h_out, Scratch& s,
                    bool keep_h) {
+  if (s.w16) return block_forward_bf16(st, m, w, h_in, h_out, s, keep_h);
   const int M = s.M, d = m.d;
   { HY_PROF(st, "ln1");
   check_cuda(layernorm_fwd(st, M, d, h_in, bt(w, d, HY_LN1_G), bt(w, d, HY_LN1_B), s.ln1, s.mean1, s.rstd1), "ln1");
@@ -102,6 +256,7 @@ void block_forward(cudaStream_t st, const hy_dims& m, const float* w, const floa
 // dh: in dL/dh_out, out dL/dh_in. Requires the intermediates of block_forward(h_in).
 void block_backward(cudaStream_t st, const hy_dims& m, const float* w, float* gw, const float* h_in, float* dh,
                     Scratch& s) {
+  if (s.w16) return block_backward_bf16(st, m, w, gw, h_in, dh, s);
   const int M = s.M, d = m.d;
   // MLP out: h_out = hmid + act Wpr^T + bpr
   { HY_PROF(st, "bwd_dW_proj");
@@ -203,14 +358,16 @@ void head_pass(cudaStream_t st, const hy_dims& m, const float* lnf, const float*
 
 }  // namespace
 
-long scratch_floats(const hy_dims& m, int max_blocks) {
+long scratch_floats(const hy_dims& m, int max_blocks, bool bf16) {
   Scratch s;
-  carve_scratch(m, max_blocks, nullptr, &s);
-  return reinterpret_cast<long>(s.attn_ws) / static_cast<long>(sizeof(float)) +
-         hy_pad32(static_cast<long>(m.B) * m.H * m.T);
+  carve_scratch(m, max_blocks, nullptr, &s, bf16);
+  const long end = bf16 ? reinterpret_cast<long>(s.w16) / static_cast<long>(sizeof(float)) + w16_floats(m)
+                        : reinterpret_cast<long>(s.attn_ws) / static_cast<long>(sizeof(float)) +
+                              hy_pad32(static_cast<long>(m.B) * m.H * m.T);
+  return end;
 }
 
-void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s) {
+void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s, bool bf16) {
   const long M = static_cast<long>(m.B) * m.T, d = m.d;
   float* p = base;
   auto take = [&](long n) {
@@ -257,6 +414,7 @@ void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s) {
   s->row_loss = take(M);
   s->loss = reinterpret_cast<double*>(take(2));
   s->attn_ws = take(static_cast<long>(m.B) * m.H * m.T);
+  s->w16 = bf16 ? reinterpret_cast<__nv_bfloat16*>(take(w16_floats(m))) : nullptr;
 }
 
 void run_forward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const float* slot, const TaskIO& io,
@@ -371,6 +529,8 @@ void run_backward(cudaStream_t st, const hy_dims& m, const ShardGeom& g, const f
     const float* w = slot + lo(m, layer, g.l0);
     if (!(last_block_live && i == nb - 1)) {
       block_forward(st, m, w, stash + i * n, nullptr, s, true);  // intermediates only: no MLP projection
+    } else if (s.w16) {
+      block_w16(st, m, w, s);
     }
     float* gw = sink.acquire(layer);
     block_backward(st, m, w, gw, stash + i * n, dh, s);

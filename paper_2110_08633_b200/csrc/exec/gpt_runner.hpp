@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <vector>
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -39,6 +40,11 @@ struct Scratch {
   float* logits;                 // aliases fc..act, logits_rows x HY_VOCAB_PAD
   int logits_rows = 0;
   float* attn_ws;                // [B*H*T]
+  // "bf16" precision (carved only then): one block's parameters as bf16, same offsets as the
+  // fp32 block (hy_block_tensor_offset), converted before the block's GEMMs use them. Block
+  // GEMM operands are bf16 views inside the fp32 buffers: ln1 = [ln1 | attention out],
+  // ln2 = [ln2 | dh], act = [act] / [dact] / [datt (fp32) | dqkv]; see block_forward_bf16.
+  __nv_bfloat16* w16 = nullptr;
 };
 
 // Stash layout for a job's shards: a backward keeps the input of each of its blocks (plus, for
@@ -78,8 +84,9 @@ inline int ext_stash_slots(const std::vector<ShardGeom>& geom) {
   return ext_stash_offset(geom, static_cast<int>(geom.size()));
 }
 // Bytes of scratch a worker needs for these dims with `max_blocks` blocks per shard.
-long scratch_floats(const hy_dims& m, int max_blocks);
-void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s);
+// bf16: also carve Scratch::w16 (the runner then takes the bf16 block path).
+long scratch_floats(const hy_dims& m, int max_blocks, bool bf16 = false);
+void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s, bool bf16 = false);
 
 struct TaskIO {
   const int32_t* tokens = nullptr;   // [M] device

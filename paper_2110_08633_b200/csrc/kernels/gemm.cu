@@ -2,6 +2,7 @@
 // kernels live in gemm_kernels.cuh, instantiated per epilogue mode in gemm_m{0,1,2}.cu.
 #include <cstdlib>
 #include <cuda.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 
@@ -16,14 +17,20 @@ cudaError_t gemm_dispatch_m1(cudaStream_t st, int M, int N, int K, const float* 
                            long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
 cudaError_t gemm_dispatch_m2(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
                            long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
+cudaError_t gemm_dispatch_b0(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
+                             const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat);
+cudaError_t gemm_dispatch_b1(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
+                             const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat);
+cudaError_t gemm_dispatch_b2(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
+                             const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat);
 
 namespace {
 
 constexpr int BM = 128;  // must match gemm_kernels.cuh
-constexpr int BK = 32;
 
 thread_local float* t_splitk_ws = nullptr;
 thread_local bool t_prec3 = false;
+thread_local bool t_bf16 = false;
 thread_local long t_splitk_floats = 0;
 
 // C = alpha * sum_s part[s] + beta * C   (fixed summation order: deterministic). Rows over
@@ -85,18 +92,25 @@ cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const float* A, long 
   if (e.mode == kEpiGeluBwd) return gemm_dispatch_m2(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
   return gemm_dispatch_m0(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
 }
+cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
+                     const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
+  if (e.mode == kEpiGelu) return gemm_dispatch_b1(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+  if (e.mode == kEpiGeluBwd) return gemm_dispatch_b2(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+  return gemm_dispatch_b0(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+}
 
-}  // namespace
-
-void gemm_set_precision_fp32(bool three_pass) { t_prec3 = three_pass; }
-bool gemm_precision_fp32() { return t_prec3; }
-
-cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
-                      const float* B, long ldb, bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch) {
+// Split-K planning shared by both operand types (BK = K per 128-byte stage row: 32 fp32, 64 bf16).
+template <typename T>
+cudaError_t gemm_run(cudaStream_t stream, int M, int N, int K, const T* A, long lda, bool a_mn, const T* B, long ldb,
+                     bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch) {
+  constexpr int BK = 128 / static_cast<int>(sizeof(T));
+  constexpr long kAlign = 16 / static_cast<long>(sizeof(T));
+  const bool prec3 = sizeof(T) == 4 && t_prec3;
   if (M <= 0 || N <= 0 || K <= 0) return cudaSuccess;
-  if ((lda & 3) || (ldb & 3) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
+  if ((lda % kAlign) || (ldb % kAlign) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
     return cudaErrorInvalidValue;
   }
+  if (epi.c16 && (epi.beta != 0.f || batch || (epi.ldc & 3))) return cudaErrorInvalidValue;
   GemmBatch bat = batch ? *batch : GemmBatch{};
   GemmEpilogue e = epi;
   // Split K when the output has too few tiles to fill the GPU (e.g. the LM-head dz GEMM:
@@ -104,13 +118,13 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   int split = 1;
   const long tiles = static_cast<long>((M + BM - 1) / BM) * ((N + 127) / 128);
   const int kb_all = (K + BK - 1) / BK;
-  const bool plain = !batch && e.mode == kEpiStore && !e.bias && !e.R;
+  const bool plain = !batch && e.mode == kEpiStore && !e.bias && !e.R && !e.c16;
   static const int forced_split = [] {  // diagnostics: HY_GEMM_SPLIT=S forces S-way split-K
     const char* v = std::getenv("HY_GEMM_SPLIT");
     return v ? std::atoi(v) : 0;
   }();
-  if (plain && t_splitk_ws && tiles * 2 <= sm_count_host() && kb_all >= 32) {
-    split = static_cast<int>(std::min<long>(sm_count_host() / tiles, kb_all / 16));
+  if (plain && t_splitk_ws && tiles * 2 <= sm_count_host() && kb_all >= 32 * 32 / BK) {
+    split = static_cast<int>(std::min<long>(sm_count_host() / tiles, kb_all / (16 * 32 / BK)));
     split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
   // Long-K GEMMs whose 256-wide CTA-pair tiles cover under half the pairs (the weight gradients,
@@ -122,9 +136,9 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   }();
   const long tiles256 = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + 255) / 256);
   const long pairs = sm_count_host() / 2;
-  if (split256 && split == 1 && plain && t_splitk_ws && !t_prec3 && M > BM && N > 128 && kb_all >= 64 &&
+  if (split256 && split == 1 && plain && t_splitk_ws && !prec3 && M > BM && N > 128 && kb_all >= 64 * 32 / BK &&
       tiles256 * 2 <= pairs) {
-    split = static_cast<int>(std::min<long>(pairs / tiles256, kb_all / 32));
+    split = static_cast<int>(std::min<long>(pairs / tiles256, kb_all / (32 * 32 / BK)));
     split = static_cast<int>(std::min<long>(split, t_splitk_floats / (static_cast<long>(M) * N)));
   }
   if (forced_split >= 2 && plain && t_splitk_ws) {
@@ -151,6 +165,24 @@ cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, 
   }
   return dispatch(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
 }
+
+}  // namespace
+
+void gemm_set_precision_fp32(bool three_pass) { t_prec3 = three_pass; }
+bool gemm_precision_fp32() { return t_prec3; }
+
+cudaError_t gemm_tf32(cudaStream_t stream, int M, int N, int K, const float* A, long lda, bool a_mn,
+                      const float* B, long ldb, bool b_mn, const GemmEpilogue& epi, const GemmBatch* batch) {
+  return gemm_run<float>(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, epi, batch);
+}
+
+cudaError_t gemm_bf16(cudaStream_t stream, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
+                      const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& epi) {
+  return gemm_run<__nv_bfloat16>(stream, M, N, K, A, lda, a_mn, B, ldb, b_mn, epi, nullptr);
+}
+
+void gemm_set_compute_bf16(bool on) { t_bf16 = on; }
+bool gemm_compute_bf16() { return t_bf16; }
 
 void gemm_set_splitk_workspace(float* ws, long floats) {
   t_splitk_ws = ws;

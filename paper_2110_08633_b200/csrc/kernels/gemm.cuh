@@ -1,6 +1,7 @@
 // tcgen05/TMEM/TMA GEMM (kind::tf32, fp32 accumulate) with fused epilogues.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace hy {
@@ -24,6 +25,7 @@ struct GemmEpilogue {
   long ldhi = 0;
   float beta = 0.f;
   int mode = kEpiStore;
+  int c16 = 0;  // C is bf16 (ldc in bf16 elements; beta must be 0, unbatched): bf16 GEMM operands out
 };
 
 // Batched / causal extensions (used by tensor-core attention). A batch index z in
@@ -57,5 +59,14 @@ void gemm_set_splitk_workspace(float* ws, long floats);
 // accuracy at 3x the MMA work), false = plain TF32 (default).
 void gemm_set_precision_fp32(bool three_pass);
 bool gemm_precision_fp32();
+
+// Same contract with bf16 operands (tcgen05.mma kind::f16, fp32 accumulate; leading dims
+// multiples of 8). The epilogue (bias / residual / GELU / GELU', split-K) runs in fp32 and
+// stores fp32 C, or bf16 C when epi.c16 is set.
+cudaError_t gemm_bf16(cudaStream_t stream, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
+                      const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& epi);
+// Per host thread: the shard runner's "bf16" precision (block GEMMs on bf16 operands).
+void gemm_set_compute_bf16(bool on);
+bool gemm_compute_bf16();
 
 }  // namespace hy

@@ -13,6 +13,7 @@
 // so forward (X W^T), data-grad (dY W) and weight-grad (dY^T X) GEMMs all read their
 // inputs in place with no transposes.
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 #include <cstdio>
@@ -32,6 +33,50 @@ constexpr int BM = 128;
 constexpr int BK = 32;  // one 128-byte swizzle atom of fp32
 constexpr int kStages = 4;
 constexpr int kThreads = 256;
+
+using bf16 = __nv_bfloat16;
+
+// Operand element type: fp32 (kind::tf32, 8-deep MMAs) or bf16 (kind::f16, 16-deep MMAs). A stage
+// row is one 128-byte swizzle atom either way (32 fp32 / 64 bf16 of K), so stage bytes, the
+// K-major descriptors and their 32-byte per-MMA advance are shared; MN-major operands are staged
+// in 128-byte MN chunks (32 fp32 with the 32-byte-atom swizzle, 64 bf16 with the plain 128B one).
+template <typename T>
+struct Elem {
+  static constexpr bool kBf16 = sizeof(T) == 2;
+  static constexpr int BK = 128 / static_cast<int>(sizeof(T));  // K per stage
+  static constexpr int CW = BK;                                 // MN-major chunk width (128 B)
+  static constexpr int kMmaK = kBf16 ? 16 : 8;
+  static constexpr int kMmas = BK / kMmaK;  // 4 MMAs per stage
+};
+
+// UMMA smem descriptor of MMA kk (0..3) of a stage operand at `base`. K-major: 8-row groups of
+// 128 B (SBO 1024), advance 32 B of K. MN-major: LBO = one chunk (BK k-rows x 128 B), SBO = the
+// swizzle atom's k-rows (4 for the fp32 32-byte atom, 8 for bf16), advance kMmaK k-rows.
+template <typename T, bool MN>
+__device__ __forceinline__ uint64_t op_desc(uint32_t base, int kk) {
+  constexpr int BKT = Elem<T>::BK;
+  if constexpr (!MN) {
+    return smem_desc_sw128(base + kk * 32, 16, 1024);
+  } else if constexpr (Elem<T>::kBf16) {
+    return smem_desc_sw128(base + kk * 2048, BKT * 128, 1024);
+  } else {
+    return smem_desc_sw128_b32(base + kk * 1024, BKT * 128, 512);
+  }
+}
+template <typename T>
+__host__ __device__ constexpr uint32_t idesc_of(int M, int N, bool a_mn, bool b_mn) {
+  return Elem<T>::kBf16 ? idesc_bf16(M, N, a_mn, b_mn) : idesc_tf32(M, N, a_mn, b_mn);
+}
+template <typename T>
+__device__ __forceinline__ void mma_one(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (Elem<T>::kBf16) mma_bf16(d, a, b, idesc, acc);
+  else mma_tf32(d, a, b, idesc, acc);
+}
+template <typename T>
+__device__ __forceinline__ void mma_two(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if constexpr (Elem<T>::kBf16) mma_bf16_pair(d, a, b, idesc, acc);
+  else mma_tf32_pair(d, a, b, idesc, acc);
+}
 
 // P3 (3xTF32, "fp32" precision): every stage also holds the low parts A_lo, B_lo
 // (x = hi + lo, hi = tf32_rna(x)); D += A_lo B_hi + A_hi B_lo + A_hi B_hi.
@@ -79,7 +124,7 @@ struct TileInfo {
   bool skip;     // tile not computed (causal upper)
 };
 
-template <int BN>
+template <int BN, int BKT = BK>
 __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n, int M, int N, int K, int nb2,
                                               int causal, int nb1 = 1) {
   TileInfo t;
@@ -90,7 +135,7 @@ __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n
   t.z2 = z - t.z1 * nb2;
   t.m0 = (r % tiles_m) * BM;
   t.n0 = (r / tiles_m) * BN;
-  const int kb_all = (K + BK - 1) / BK;
+  const int kb_all = (K + BKT - 1) / BKT;
   t.kb0 = 0;
   t.nkb = kb_all;
   t.skip = false;
@@ -98,9 +143,9 @@ __device__ __forceinline__ TileInfo tile_info(int tile, int tiles_m, int tiles_n
     t.skip = t.n0 >= t.m0 + BM;
   } else if (causal == kCausalKLower) {
     const int kend = min(K, t.m0 + BM);
-    t.nkb = (kend + BK - 1) / BK;
+    t.nkb = (kend + BKT - 1) / BKT;
   } else if (causal == kCausalKUpper) {
-    t.kb0 = t.m0 / BK;
+    t.kb0 = t.m0 / BKT;
     t.nkb = max(0, kb_all - t.kb0);
   } else if (causal == kSplitK) {
     // z1 indexes the K slice; the operands themselves are not batched (TMA z = 0)
@@ -173,8 +218,17 @@ struct EpiCtx {
   const float* src;
   long lds;
   bool use_beta;
+  bool c16;  // C is bf16 (GemmEpilogue::c16)
   const float* bias;
 };
+
+__device__ __forceinline__ void st_bf16x4(bf16* p, float4 v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = u;
+}
 
 // One 32-column chunk (v: this thread's row, 32 accumulator columns).
 template <int MODE>
@@ -245,7 +299,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
             xe[e] = y;
           }
         }
-        *reinterpret_cast<float4*>(x0.Cb + grow * epi.ldc + col) = xv[i];
+        if (x0.c16) st_bf16x4(reinterpret_cast<bf16*>(epi.C) + grow * epi.ldc + col, xv[i]);
+        else *reinterpret_cast<float4*>(x0.Cb + grow * epi.ldc + col) = xv[i];
       }
     }
   } else {
@@ -267,7 +322,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
           if (epi.R) y += epi.R[grow * epi.ldr + colx];
           if (epi.beta != 0.f) y += epi.beta * x0.Cb[grow * epi.ldc + colx];
         }
-        x0.Cb[grow * epi.ldc + colx] = y;
+        if (x0.c16) reinterpret_cast<bf16*>(epi.C)[grow * epi.ldc + colx] = __float2bfloat16_rn(y);
+        else x0.Cb[grow * epi.ldc + colx] = y;
       }
     }
   }
@@ -297,6 +353,7 @@ __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uin
   x.src = MODE == kEpiGeluBwd ? epi.Hin : (MODE == kEpiStore ? epi.R : nullptr);
   x.lds = MODE == kEpiGeluBwd ? epi.ldhi : epi.ldr;
   x.use_beta = MODE == kEpiStore && epi.beta != 0.f;
+  x.c16 = epi.c16 != 0;
   x.bias = MODE == kEpiGeluBwd ? nullptr : epi.bias;
   const uint32_t tbase = tmem_base + ((q * 32) << 16) + acc * BN;
   uint32_t b0[32], b1[32];
@@ -319,12 +376,15 @@ __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uin
   }
 }
 
-template <int BN, bool A_MN, bool B_MN, bool P3, int MODE>
+template <typename T, int BN, bool A_MN, bool B_MN, bool P3, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                  int N, int K, GemmEpilogue epi, GemmBatch bat) {
   using L = Smem<BN, P3>;
+  using E = Elem<T>;
+  static_assert(!(P3 && E::kBf16), "3xTF32 is an fp32-operand mode");
   constexpr int kStages = L::kStagesN;
+  constexpr int BKT = E::BK, CW = E::CW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_smem = reinterpret_cast<float*>(smem + L::kRing);
@@ -367,7 +427,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+        TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
         if (ti.skip) continue;
         if (bat.causal == kSplitK) ti.z1 = ti.z2 = 0;  // K slices read the same operands
         for (int kb = ti.kb0; kb < ti.kb0 + ti.nkb; ++kb) {
@@ -375,12 +435,12 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           mbar_expect_tx(&full[stage], L::kOpBytes);
-          const int k0 = kb * BK;
+          const int k0 = kb * BKT;
           if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 32; ++j) {
-              if (bat.a_perm) tma_load_4d(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, k0, ti.z2, ti.z1);
+            for (int j = 0; j < BM / CW; ++j) {
+              if (bat.a_perm) tma_load_4d(sa + j * (BKT * 128), &map_a, &full[stage], ti.m0 + CW * j, ti.z2, k0, ti.z1);
+              else tma_load_4d(sa + j * (BKT * 128), &map_a, &full[stage], ti.m0 + CW * j, k0, ti.z2, ti.z1);
             }
           } else {
             if (bat.a_perm) tma_load_4d(sa, &map_a, &full[stage], k0, ti.z2, ti.m0, ti.z1);
@@ -388,9 +448,9 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j) {
-              if (bat.b_perm) tma_load_4d(sb + j * (32 * BK * 4), &map_b, &full[stage], ti.n0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d(sb + j * (32 * BK * 4), &map_b, &full[stage], ti.n0 + 32 * j, k0, ti.z2, ti.z1);
+            for (int j = 0; j < BN / CW; ++j) {
+              if (bat.b_perm) tma_load_4d(sb + j * (BKT * 128), &map_b, &full[stage], ti.n0 + CW * j, ti.z2, k0, ti.z1);
+              else tma_load_4d(sb + j * (BKT * 128), &map_b, &full[stage], ti.n0 + CW * j, k0, ti.z2, ti.z1);
             }
           } else {
             if (bat.b_perm) tma_load_4d(sb, &map_b, &full[stage], k0, ti.z2, ti.n0, ti.z1);
@@ -404,12 +464,12 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_tf32(BM, BN, A_MN, B_MN);
+    constexpr uint32_t idesc = idesc_of<T>(BM, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int local = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+      const TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       const int acc = local & 1;
       const uint32_t acc_phase = (local >> 1) & 1;
@@ -433,7 +493,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
           const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
           const uint32_t sb = sa + L::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
+          for (int kk = 0; kk < E::kMmas; ++kk) {
             if constexpr (P3) {
               const uint32_t la = sa + L::kOpBytes, lb = sb + L::kOpBytes;
               const uint64_t dah = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
@@ -449,14 +509,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
               mma_tf32(d_tmem, dah, dbh, idesc, 1u);
               continue;
             }
-            // K-major: advance 8 fp32 = 32 B inside the swizzled row; SBO = 8 rows * 128 B.
-            // MN-major: advance 8 k-rows = 1024 B; LBO = one 32-element MN column (BK rows * 128 B),
-            // SBO = 4 k-rows (512 B) of the 32-byte-atom swizzle.
-            const uint64_t da = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
-                                     : smem_desc_sw128(sa + kk * 32, 16, 1024);
-            const uint64_t db = B_MN ? smem_desc_sw128_b32(sb + kk * 1024, BK * 128, 512)
-                                     : smem_desc_sw128(sb + kk * 32, 16, 1024);
-            mma_tf32(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+            mma_one<T>(d_tmem, op_desc<T, A_MN>(sa, kk), op_desc<T, B_MN>(sb, kk), idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           mma_commit(&empty[stage]);
           if (kb == ti.nkb - 1) mma_commit(&tfull[acc]);
@@ -474,7 +527,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     int stage = 0;
     uint32_t phase = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+      const TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       for (int kb = 0; kb < ti.nkb; ++kb) {
         mbar_wait(&full[stage], phase);
@@ -506,7 +559,7 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
     const uint32_t q = warp - 4;  // TMEM lane quarter this warp may access
     int local = 0;
     for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-      const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+      const TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       if (ti.skip) continue;
       const int acc = local & 1;
       prefetch_epilogue_rows<BN, MODE>(epi, bat, ti, ti.m0 + static_cast<int>(q * 32 + lane_id()), M, N);
@@ -546,12 +599,15 @@ struct SmemPair {
   static constexpr int kTotal = kRing + kEpi + 1024 + 256;
 };
 
-template <int BN, bool A_MN, bool B_MN, int MODE>
+template <typename T, int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                       int N, int K, GemmEpilogue epi, GemmBatch bat) {
   using L = SmemPair<BN>;
+  using E = Elem<T>;
   constexpr int kStages = L::kStagesN;
+  constexpr int BKT = E::BK, CW = E::CW;
+  static_assert(!B_MN || (BN / 2) % CW == 0, "MN-major B half-tile in whole 128-byte chunks");
   constexpr int BM2 = 2 * BM;
   constexpr int kHalfChunks = (BN / 64) * 2 == BN / 32 ? BN / 64 + ((BN / 64) & 1) : BN / 64;  // even split point
   extern __shared__ uint8_t smem_raw[];
@@ -600,7 +656,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-        TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+        TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
         // tile_info counts 128-row tiles; rescale to this CTA's half of the 256-row pair tile
         ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
         if (bat.causal == kSplitK) ti.z1 = ti.z2 = 0;
@@ -610,12 +666,12 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
           uint8_t* sa = smem + stage * L::kStageBytes;
           uint8_t* sb = sa + L::kABytes;
           if (leader) mbar_expect_tx(&full[stage], 2 * L::kStageBytes);
-          const int k0 = kb * BK;
+          const int k0 = kb * BKT;
           if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 32; ++j) {
-              if (bat.a_perm) tma_load_4d_pair(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d_pair(sa + j * (32 * BK * 4), &map_a, &full[stage], ti.m0 + 32 * j, k0, ti.z2, ti.z1);
+            for (int j = 0; j < BM / CW; ++j) {
+              if (bat.a_perm) tma_load_4d_pair(sa + j * (BKT * 128), &map_a, &full[stage], ti.m0 + CW * j, ti.z2, k0, ti.z1);
+              else tma_load_4d_pair(sa + j * (BKT * 128), &map_a, &full[stage], ti.m0 + CW * j, k0, ti.z2, ti.z1);
             }
           } else {
             if (bat.a_perm) tma_load_4d_pair(sa, &map_a, &full[stage], k0, ti.z2, ti.m0, ti.z1);
@@ -623,9 +679,9 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) {
-              if (bat.b_perm) tma_load_4d_pair(sb + j * (32 * BK * 4), &map_b, &full[stage], nb0 + 32 * j, ti.z2, k0, ti.z1);
-              else tma_load_4d_pair(sb + j * (32 * BK * 4), &map_b, &full[stage], nb0 + 32 * j, k0, ti.z2, ti.z1);
+            for (int j = 0; j < (BN / 2) / CW; ++j) {
+              if (bat.b_perm) tma_load_4d_pair(sb + j * (BKT * 128), &map_b, &full[stage], nb0 + CW * j, ti.z2, k0, ti.z1);
+              else tma_load_4d_pair(sb + j * (BKT * 128), &map_b, &full[stage], nb0 + CW * j, k0, ti.z2, ti.z1);
             }
           } else {
             if (bat.b_perm) tma_load_4d_pair(sb, &map_b, &full[stage], k0, ti.z2, nb0, ti.z1);
@@ -640,12 +696,12 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     }
   } else if (warp == 1) {
     if (leader) {
-      constexpr uint32_t idesc = idesc_tf32(BM2, BN, A_MN, B_MN);
+      constexpr uint32_t idesc = idesc_of<T>(BM2, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
       for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-        const TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+        const TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
         const int acc = local & 1;
         const uint32_t acc_phase = (local >> 1) & 1;
         ++local;
@@ -667,12 +723,8 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
             const uint32_t sa = smem_u32(smem + stage * L::kStageBytes);
             const uint32_t sb = sa + L::kABytes;
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t da = A_MN ? smem_desc_sw128_b32(sa + kk * 1024, BK * 128, 512)
-                                       : smem_desc_sw128(sa + kk * 32, 16, 1024);
-              const uint64_t db = B_MN ? smem_desc_sw128_b32(sb + kk * 1024, BK * 128, 512)
-                                       : smem_desc_sw128(sb + kk * 32, 16, 1024);
-              mma_tf32_pair(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+            for (int kk = 0; kk < E::kMmas; ++kk) {
+              mma_two<T>(d_tmem, op_desc<T, A_MN>(sa, kk), op_desc<T, B_MN>(sb, kk), idesc, (kb | kk) != 0 ? 1u : 0u);
             }
             mma_commit_pair(&empty[stage], 0x3);
             if (kb == ti.nkb - 1) mma_commit_pair(&tfull[acc], 0x3);
@@ -689,7 +741,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     const uint32_t q = warp - 4;
     int local = 0;
     for (int tile = pair; tile < n_tiles; tile += n_pairs) {
-      TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+      TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
       const int acc = local & 1;
       prefetch_epilogue_rows<BN, MODE>(epi, bat, ti, ti.m0 + static_cast<int>(q * 32 + lane_id()), M, N);
@@ -717,7 +769,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     __syncwarp();
     const int cnt = (n_tiles - 1 - pair) / n_pairs + 1;  // tiles of this CTA
     const int tile = pair + (cnt - 1) * n_pairs;
-    TileInfo ti = tile_info<BN>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
+    TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
     ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
     const int acc = (cnt - 1) & 1;
     // not tfull itself: an early parity test on it could pass for an earlier phase
@@ -752,27 +804,30 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 4-D fp32 tensor map over {inner, outer, b2, b1}: row stride ld, batch strides s2, s1
-// (elements). Dimensions are ordered by increasing stride: {inner, outer, b2, b1}, or
-// {inner, b2, outer, b1} when b2's stride is below the row stride (*perm = 1).
-bool make_map(CUtensorMap* map, const float* ptr, long inner, long outer, long ld, int box_inner, int box_outer,
+// 4-D tensor map (fp32 or bf16 elements) over {inner, outer, b2, b1}: row stride ld, batch
+// strides s2, s1 (elements). Dimensions are ordered by increasing stride: {inner, outer, b2, b1},
+// or {inner, b2, outer, b1} when b2's stride is below the row stride (*perm = 1).
+template <typename T>
+bool make_map(CUtensorMap* map, const T* ptr, long inner, long outer, long ld, int box_inner, int box_outer,
               bool mn_major, long nb2 = 1, long s2 = 0, long nb1 = 1, long s1 = 0, int* perm = nullptr) {
   auto fn = encode_fn();
   if (!fn) return false;
+  constexpr long es = sizeof(T);
   const long st2 = s2 > 0 ? s2 : ld * outer;
   const long st1 = s1 > 0 ? s1 : st2 * nb2;
   const bool swap = nb2 > 1 && st2 < ld;
   if (perm) *perm = swap ? 1 : 0;
   cuuint64_t dims[4] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(swap ? nb2 : outer),
                         static_cast<cuuint64_t>(swap ? outer : nb2), static_cast<cuuint64_t>(nb1)};
-  cuuint64_t strides[3] = {static_cast<cuuint64_t>(swap ? st2 : ld) * 4, static_cast<cuuint64_t>(swap ? ld : st2) * 4,
-                           static_cast<cuuint64_t>(st1) * 4};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(swap ? st2 : ld) * es, static_cast<cuuint64_t>(swap ? ld : st2) * es,
+                           static_cast<cuuint64_t>(st1) * es};
   cuuint32_t box[4] = {static_cast<cuuint32_t>(box_inner), swap ? 1u : static_cast<cuuint32_t>(box_outer),
                        swap ? static_cast<cuuint32_t>(box_outer) : 1u, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+  const bool b16 = Elem<T>::kBf16;
+  CUresult r = fn(map, b16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                  const_cast<T*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  (mn_major && !b16) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -788,18 +843,27 @@ int sm_count() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool P3, int MODE>
-cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
+// Operand maps: K-major boxes are {BK, rows} (one 128-byte row of K per tile row), MN-major
+// boxes {CW, BK} (one 128-byte MN chunk per k-row).
+template <typename T>
+bool make_operand_maps(CUtensorMap* ma, CUtensorMap* mb, GemmBatch& b, int M, int N, int K, const T* A, long lda,
+                       bool a_mn, const T* B, long ldb, bool b_mn, int b_rows) {
+  constexpr int BKT = Elem<T>::BK, CW = Elem<T>::CW;
+  const long mb1 = b.causal == kSplitK ? 1 : b.nb1;  // K slices share the (unbatched) operands
+  const bool ok_a = a_mn ? make_map(ma, A, M, K, lda, CW, BKT, true, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm)
+                         : make_map(ma, A, K, M, lda, BKT, BM, false, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm);
+  const bool ok_b = b_mn ? make_map(mb, B, N, K, ldb, CW, BKT, true, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm)
+                         : make_map(mb, B, K, N, ldb, BKT, b_rows, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
+  return ok_a && ok_b;
+}
+
+template <typename T, int BN, bool A_MN, bool B_MN, bool P3, int MODE>
+cudaError_t launch(cudaStream_t stream, int M, int N, int K, const T* A, long lda, const T* B, long ldb,
                    const GemmEpilogue& epi, const GemmBatch& bat) {
   CUtensorMap ma, mb;
   GemmBatch b = bat;
-  const long mb1 = b.causal == kSplitK ? 1 : b.nb1;  // K slices share the (unbatched) operands
-  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm)
-                         : make_map(&ma, A, K, M, lda, BK, BM, false, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm);
-  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm)
-                         : make_map(&mb, B, K, N, ldb, BK, BN, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
-  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-  auto kern = gemm_tf32_kernel<BN, A_MN, B_MN, P3, MODE>;
+  if (!make_operand_maps(&ma, &mb, b, M, N, K, A, lda, A_MN, B, ldb, B_MN, BN)) return cudaErrorInvalidValue;
+  auto kern = gemm_tf32_kernel<T, BN, A_MN, B_MN, P3, MODE>;
   {
     const cudaError_t e = ensure_smem_limit(kern, Smem<BN, P3>::kTotal);
     if (e != cudaSuccess) return e;
@@ -810,18 +874,13 @@ cudaError_t launch(cudaStream_t stream, int M, int N, int K, const float* A, lon
   return launch_pdl(kern, dim3(grid), dim3(kThreads), Smem<BN, P3>::kTotal, stream, ma, mb, M, N, K, epi, b);
 }
 
-template <int BN, bool A_MN, bool B_MN, int MODE>
-cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const float* A, long lda, const float* B, long ldb,
+template <typename T, int BN, bool A_MN, bool B_MN, int MODE>
+cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const T* A, long lda, const T* B, long ldb,
                         const GemmEpilogue& epi, const GemmBatch& bat) {
   CUtensorMap ma, mb;
   GemmBatch b = bat;
-  const long mb1 = b.causal == kSplitK ? 1 : b.nb1;
-  const bool ok_a = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm)
-                         : make_map(&ma, A, K, M, lda, BK, BM, false, b.nb2, b.a_s2, mb1, b.a_s1, &b.a_perm);
-  const bool ok_b = B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm)
-                         : make_map(&mb, B, K, N, ldb, BK, BN / 2, false, b.nb2, b.b_s2, mb1, b.b_s1, &b.b_perm);
-  if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-  auto kern = gemm_tf32_pair_kernel<BN, A_MN, B_MN, MODE>;
+  if (!make_operand_maps(&ma, &mb, b, M, N, K, A, lda, A_MN, B, ldb, B_MN, BN / 2)) return cudaErrorInvalidValue;
+  auto kern = gemm_tf32_pair_kernel<T, BN, A_MN, B_MN, MODE>;
   {
     const cudaError_t e = ensure_smem_limit(kern, SmemPair<BN>::kTotal);
     if (e != cudaSuccess) return e;
@@ -833,22 +892,27 @@ cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const float* A
                     M, N, K, epi, b);
 }
 
-template <int BN, int MODE>
-cudaError_t dispatch_pair(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+template <typename T, int BN, int MODE>
+cudaError_t dispatch_pair(cudaStream_t st, int M, int N, int K, const T* A, long lda, bool a_mn, const T* B,
                           long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
-  if (!a_mn && !b_mn) return launch_pair<BN, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (!a_mn && b_mn) return launch_pair<BN, false, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (a_mn && !b_mn) return launch_pair<BN, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  return launch_pair<BN, true, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (!a_mn && !b_mn) return launch_pair<T, BN, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (a_mn && !b_mn) return launch_pair<T, BN, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if constexpr (Elem<T>::kBf16 && (BN / 2) % Elem<T>::CW != 0) {
+    return cudaErrorInvalidValue;  // pick_bn_pair never picks this (96-wide bf16 MN-major halves)
+  } else {
+    if (!a_mn && b_mn) return launch_pair<T, BN, false, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+    return launch_pair<T, BN, true, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  }
 }
 
 // CTA-pair tile width (256 x BN pair tiles): the widest tile whose wave count is not worse.
-int pick_bn_pair(int M, int N, long batches) {
+// bf16 MN-major B needs whole 64-wide chunks per CTA half: BN 128 or 256.
+int pick_bn_pair(int M, int N, long batches, bool no192 = false) {
   static const int forced = [] {
     const char* e = std::getenv("HY_GEMM_BN");
     return e ? std::atoi(e) : 0;
   }();
-  if (forced == 128 || forced == 192 || forced == 256) return forced;
+  if (forced == 128 || forced == 256 || (forced == 192 && !no192)) return forced;
   static const int kBN[3] = {128, 192, 256};
   static const double kCost[3] = {128 / 0.62, 192 / 0.70, 256 / 0.76};
   const long tm = (M + 2 * BM - 1) / (2 * BM);
@@ -857,6 +921,7 @@ int pick_bn_pair(int M, int N, long batches) {
   double best_t = 1e300;
   for (int i = 0; i < 3; ++i) {
     if (kBN[i] > 128 && N <= 128) break;
+    if (kBN[i] == 192 && no192) continue;
     const long tiles = tm * ((N + kBN[i] - 1) / kBN[i]) * batches;
     const double t = static_cast<double>((tiles + pairs - 1) / pairs) * kCost[i];
     if (t < best_t - 1e-9) {
@@ -875,13 +940,13 @@ bool use_pairs() {
   return on;
 }
 
-template <int BN, int MODE>
-cudaError_t dispatch_bn(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+template <typename T, int BN, int MODE>
+cudaError_t dispatch_bn(cudaStream_t st, int M, int N, int K, const T* A, long lda, bool a_mn, const T* B,
                         long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
-  if (!a_mn && !b_mn) return launch<BN, false, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (!a_mn && b_mn) return launch<BN, false, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (a_mn && !b_mn) return launch<BN, true, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  return launch<BN, true, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (!a_mn && !b_mn) return launch<T, BN, false, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (!a_mn && b_mn) return launch<T, BN, false, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if (a_mn && !b_mn) return launch<T, BN, true, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  return launch<T, BN, true, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
 }
 
 // Output tile width: wider tiles cut the shared-memory traffic per MMA (the TF32 pipe is
@@ -910,30 +975,29 @@ int pick_bn(int M, int N, long batches) {
   return best;
 }
 
-template <int MODE>
-cudaError_t dispatch_mode(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+template <typename T, int MODE>
+cudaError_t dispatch_mode(cudaStream_t st, int M, int N, int K, const T* A, long lda, bool a_mn, const T* B,
                           long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3) {
   if (!prec3 && (bat.causal == kCausalNone || bat.causal == kSplitK) && M > BM && use_pairs()) {
-    const int bn = pick_bn_pair(M, N, static_cast<long>(bat.nb1) * bat.nb2);
-    if (bn == 256) return dispatch_pair<256, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-    if (bn == 192) return dispatch_pair<192, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-    return dispatch_pair<128, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+    const int bn = pick_bn_pair(M, N, static_cast<long>(bat.nb1) * bat.nb2, Elem<T>::kBf16 && b_mn);
+    if (bn == 256) return dispatch_pair<T, 256, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+    if (bn == 192) return dispatch_pair<T, 192, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+    return dispatch_pair<T, 128, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
   }
   if (!prec3 && bat.causal == kCausalNone) {
     const int bn = pick_bn(M, N, static_cast<long>(bat.nb1) * bat.nb2);
-    if (bn == 256) return dispatch_bn<256, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
-    if (bn == 192) return dispatch_bn<192, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+    if (bn == 256) return dispatch_bn<T, 256, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
+    if (bn == 192) return dispatch_bn<T, 192, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
   }
-  if (prec3) {
-    if (!a_mn && !b_mn) return launch<128, false, false, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-    if (!a_mn && b_mn) return launch<128, false, true, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-    if (a_mn && !b_mn) return launch<128, true, false, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-    return launch<128, true, true, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  if constexpr (!Elem<T>::kBf16) {
+    if (prec3) {
+      if (!a_mn && !b_mn) return launch<T, 128, false, false, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+      if (!a_mn && b_mn) return launch<T, 128, false, true, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+      if (a_mn && !b_mn) return launch<T, 128, true, false, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+      return launch<T, 128, true, true, true, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+    }
   }
-  if (!a_mn && !b_mn) return launch<128, false, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (!a_mn && b_mn) return launch<128, false, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  if (a_mn && !b_mn) return launch<128, true, false, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
-  return launch<128, true, true, false, MODE>(st, M, N, K, A, lda, B, ldb, e, bat);
+  return dispatch_bn<T, 128, MODE>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
 }
 
 }  // namespace

@@ -4,6 +4,6 @@
 namespace hy {
 cudaError_t gemm_dispatch_m0(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
                            long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3) {
-  return dispatch_mode<kEpiStore>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, prec3);
+  return dispatch_mode<float, kEpiStore>(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, prec3);
 }
 }  // namespace hy

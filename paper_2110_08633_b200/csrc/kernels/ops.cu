@@ -51,10 +51,27 @@ constexpr int kMaxVecAll = 32;  // d <= 4096
 // Row split over kSplit warps (<= kVec float4 per lane held in registers between the two
 // reductions), the parts' sums meeting in shared memory in a fixed order: more warps per SM
 // than a whole row per warp (8192 x 1600: 24.6 -> 22.5 us, L2-cold).
-template <int kVec, int kSplit>
+// 4 consecutive values as fp32 or as bf16 (the bf16 precision's GEMM operands).
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ void st4(__nv_bfloat16* p, float4 v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = u;
+}
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <int kVec, int kSplit, typename Y = float>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(int rows, int d, const float* __restrict__ x,
                                                      const float* __restrict__ g, const float* __restrict__ b,
-                                                     float* __restrict__ y, float* __restrict__ mean_out,
+                                                     Y* __restrict__ y, float* __restrict__ mean_out,
                                                      float* __restrict__ rstd_out) {
   constexpr int kRows = kWarpsPerBlock / kSplit;
   __shared__ float red[2][kWarpsPerBlock];
@@ -103,7 +120,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(int rows, int d, const floa
 #pragma unroll
   for (int p = 0; p < kSplit; ++p) u += red[1][first + p];
   const float rs = rsqrtf(u / d + 1e-5f);
-  float4* yr = reinterpret_cast<float4*>(y + static_cast<long>(row) * d);
+  Y* yr = y + static_cast<long>(row) * d;
   const float4* g4 = reinterpret_cast<const float4*>(g);
   const float4* b4 = reinterpret_cast<const float4*>(b);
 #pragma unroll
@@ -111,8 +128,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(int rows, int d, const floa
     const int i = part * 32 + lane + 32 * kSplit * k;
     if (i < nv) {
       const float4 gg = g4[i], bb = b4[i];
-      yr[i] = make_float4((buf[k].x - mu) * rs * gg.x + bb.x, (buf[k].y - mu) * rs * gg.y + bb.y,
-                          (buf[k].z - mu) * rs * gg.z + bb.z, (buf[k].w - mu) * rs * gg.w + bb.w);
+      st4(yr + 4 * i, make_float4((buf[k].x - mu) * rs * gg.x + bb.x, (buf[k].y - mu) * rs * gg.y + bb.y,
+                                  (buf[k].z - mu) * rs * gg.z + bb.z, (buf[k].w - mu) * rs * gg.w + bb.w));
     }
   }
   if (part == 0 && lane == 0) {
@@ -490,7 +507,8 @@ __global__ void reduce_parts_kernel(int parts, int N, const float* __restrict__ 
 // 128-column strip x (32 lanes x float4, 8 row groups, fixed-order smem reduction) into
 // part[y]; the last block of a strip to finish (atomic ticket) adds the strip's partials in
 // row-block order and resets the ticket, so the result does not depend on block timing.
-__global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const float* __restrict__ X, long ldx,
+template <typename XT = float>
+__global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const XT* __restrict__ X, long ldx,
                                                            float* __restrict__ part, float* __restrict__ out,
                                                            int accumulate, int rows_per_block,
                                                            unsigned* __restrict__ ticket) {
@@ -505,7 +523,7 @@ __global__ void __launch_bounds__(256) colsum_fused_kernel(int M, int N, const f
   if (c < N) {
 #pragma unroll 8
     for (int r = r0 + ty; r < r1; r += 8) {
-      const float4 v = *reinterpret_cast<const float4*>(X + static_cast<long>(r) * ldx + c);
+      const float4 v = ld4(X + static_cast<long>(r) * ldx + c);
       acc.x += v.x;
       acc.y += v.y;
       acc.z += v.z;
@@ -1088,8 +1106,9 @@ int colsum_blocks(int rows) {
   return rows < target ? (rows > 0 ? rows : 1) : target;
 }
 
-cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b, float* y,
-                          float* mean, float* rstd) {
+template <typename Y>
+cudaError_t layernorm_fwd_t(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b, Y* y,
+                            float* mean, float* rstd) {
   if (d % 4 || d > 4 * 32 * kMaxVecAll) return cudaErrorInvalidValue;
   if (rows <= 0) return cudaSuccess;
   // d <= 1024: a warp per row (8 rows per block) measured faster at C2's 4096 x 768 (10.2 vs
@@ -1097,13 +1116,44 @@ cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const
   const dim3 grid((rows + 1) / 2), block(32 * kWarpsPerBlock);
   count_launch();
   if (d <= 1024) {
-    check_launch(launch_pdl(ln_fwd_kernel<8, 1>, dim3((rows + kWarpsPerBlock - 1) / kWarpsPerBlock), block, 0, s,
+    check_launch(launch_pdl(ln_fwd_kernel<8, 1, Y>, dim3((rows + kWarpsPerBlock - 1) / kWarpsPerBlock), block, 0, s,
                             rows, d, x, g, b, y, mean, rstd));
   } else if (d <= 2048) {
-    check_launch(launch_pdl(ln_fwd_kernel<4, 4>, grid, block, 0, s, rows, d, x, g, b, y, mean, rstd));
+    check_launch(launch_pdl(ln_fwd_kernel<4, 4, Y>, grid, block, 0, s, rows, d, x, g, b, y, mean, rstd));
   } else {
-    check_launch(launch_pdl(ln_fwd_kernel<8, 4>, grid, block, 0, s, rows, d, x, g, b, y, mean, rstd));
+    check_launch(launch_pdl(ln_fwd_kernel<8, 4, Y>, grid, block, 0, s, rows, d, x, g, b, y, mean, rstd));
   }
+  return cudaGetLastError();
+}
+cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b, float* y,
+                          float* mean, float* rstd) {
+  return layernorm_fwd_t(s, rows, d, x, g, b, y, mean, rstd);
+}
+cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b,
+                          __nv_bfloat16* y, float* mean, float* rstd) {
+  return layernorm_fwd_t(s, rows, d, x, g, b, y, mean, rstd);
+}
+
+// fp32 -> bf16 (RNE), 8 elements per thread (n % 8 == 0, 16-byte aligned), grid-stride.
+__global__ void __launch_bounds__(256) cvt_bf16_kernel(long n8, const float4* __restrict__ x, uint4* __restrict__ y) {
+  pdl_wait_and_trigger();
+  for (long i = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; i < n8; i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const float4 a = x[2 * i], b = x[2 * i + 1];
+    __nv_bfloat162 h[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                           __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+    y[i] = *reinterpret_cast<uint4*>(h);
+  }
+}
+cudaError_t to_bf16(cudaStream_t s, long n, const float* x, __nv_bfloat16* y) {
+  if (n % 8 || (reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(y) & 15)) {
+    return cudaErrorInvalidValue;
+  }
+  if (n == 0) return cudaSuccess;
+  const long n8 = n / 8;
+  const int grid = static_cast<int>(std::min<long>((n8 + 255) / 256, 8L * sms()));
+  count_launch();
+  check_launch(launch_pdl(cvt_bf16_kernel, dim3(grid), dim3(256), 0, s, n8, reinterpret_cast<const float4*>(x),
+                          reinterpret_cast<uint4*>(y)));
   return cudaGetLastError();
 }
 
@@ -1183,6 +1233,24 @@ unsigned* colsum_tickets(cudaStream_t s) {
   return p;
 }
 
+cudaError_t colsum(cudaStream_t s, int M, int N, const __nv_bfloat16* X, long ldx, float* out, bool accumulate,
+                   float* ws) {
+  const int strips = (N + 127) / 128;
+  unsigned* tickets = colsum_tickets(s);
+  if (!tickets || N % 4 || ldx % 4 || (reinterpret_cast<uintptr_t>(X) & 7) || (reinterpret_cast<uintptr_t>(out) & 15) ||
+      strips > 4096) {
+    return cudaErrorInvalidValue;
+  }
+  if (M <= 0) return cudaSuccess;
+  int nb = std::max(1, std::min(colsum_blocks(M), (colsum_waves() * sms() + strips - 1) / strips));
+  nb = std::min(nb, std::max(1, M / 32));
+  const int rpb = (M + nb - 1) / nb;
+  nb = (M + rpb - 1) / rpb;
+  count_launch();
+  check_launch(launch_pdl(colsum_fused_kernel<__nv_bfloat16>, dim3(strips, nb), dim3(256), 0, s, M, N, X, ldx, ws, out,
+                          accumulate ? 1 : 0, rpb, tickets));
+  return cudaGetLastError();
+}
 cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float* out, bool accumulate, float* ws) {
   const int strips = (N + 127) / 128;
   unsigned* tickets = colsum_tickets(s);
@@ -1194,7 +1262,7 @@ cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float
     const int rpb = (M + nb - 1) / nb;
     nb = (M + rpb - 1) / rpb;
     count_launch();
-    check_launch(launch_pdl(colsum_fused_kernel, dim3(strips, nb), dim3(256), 0, s, M, N, X, ldx, ws, out, accumulate ? 1 : 0, rpb, tickets));
+    check_launch(launch_pdl(colsum_fused_kernel<float>, dim3(strips, nb), dim3(256), 0, s, M, N, X, ldx, ws, out, accumulate ? 1 : 0, rpb, tickets));
     return cudaGetLastError();
   }
   const int nb = colsum_blocks(M);

@@ -2,6 +2,7 @@
 // column reductions (bias / LN-param grads), fused Adam, flash attention.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -9,6 +10,11 @@ namespace hy {
 
 cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b, float* y,
                           float* mean, float* rstd);
+// bf16 output (the "bf16" precision's GEMM operand); mean / rstd fp32.
+cudaError_t layernorm_fwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* b,
+                          __nv_bfloat16* y, float* mean, float* rstd);
+// y = bf16(x), round to nearest even; n % 8 == 0, 16-byte aligned.
+cudaError_t to_bf16(cudaStream_t s, long n, const float* x, __nv_bfloat16* y);
 // dx (+)= LN backward; dg/db (+)= column sums. ws: >= 2 * d * colsum_blocks(rows) floats.
 cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const float* g, const float* mean,
                           const float* rstd, const float* dy, float* dx, bool accumulate_dx, float* dg, float* db,
@@ -16,6 +22,9 @@ cudaError_t layernorm_bwd(cudaStream_t s, int rows, int d, const float* x, const
 int colsum_blocks(int rows);
 // out[n] (+)= sum_m X[m, n]; ws >= N * colsum_blocks(M) floats.
 cudaError_t colsum(cudaStream_t s, int M, int N, const float* X, long ldx, float* out, bool accumulate, float* ws);
+// Same over a bf16 matrix (N % 4 == 0, ldx % 4 == 0).
+cudaError_t colsum(cudaStream_t s, int M, int N, const __nv_bfloat16* X, long ldx, float* out, bool accumulate,
+                   float* ws);
 
 cudaError_t embed_fwd(cudaStream_t s, int rows, int T, int d, const int32_t* tok, const float* wte, const float* wpe,
                       float* h);

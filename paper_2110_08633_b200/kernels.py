@@ -54,6 +54,30 @@ def gemm(A, B, *, a_mn=False, b_mn=False, M=None, N=None, K=None, C=None, bias=N
     return C
 
 
+def gemm_bf16(A, B, *, a_mn=False, b_mn=False, C=None, c_bf16=False, bias=None, R=None, beta=0.0, mode=0, H=None):
+    """bf16-operand GEMM (tcgen05 kind::f16, fp32 accumulate): C = op(A) op(B)^T (+ epilogue).
+    A, B: torch.bfloat16 CUDA tensors; C fp32, or bf16 when c_bf16."""
+    assert A.dtype == torch.bfloat16 and B.dtype == torch.bfloat16
+    M, K = (A.shape[1], A.shape[0]) if a_mn else (A.shape[0], A.shape[1])
+    N = B.shape[1] if b_mn else B.shape[0]
+    if C is None:
+        C = torch.empty(M, N, device=A.device, dtype=torch.bfloat16 if c_bf16 else torch.float32)
+    ldr = R.stride(0) if R is not None else 0
+    ldh = H.stride(0) if H is not None else 0
+    hout = H if mode == 1 else None
+    hin = H if mode == 2 else None
+    check(lib().hy_gemm_bf16(_s(), M, N, K, _p(A), A.stride(0), int(a_mn), _p(B), B.stride(0), int(b_mn), _p(C),
+                             C.stride(0), int(c_bf16), _p(bias), _p(R), ldr, float(beta), int(mode), _p(hout),
+                             _p(hin), ldh))
+    return C
+
+
+def to_bf16(x):
+    y = torch.empty(x.shape, device=x.device, dtype=torch.bfloat16)
+    check(lib().hy_to_bf16(_s(), x.numel(), _p(x), _p(y)))
+    return y
+
+
 def layernorm_fwd(x, g, b):
     rows, d = x.shape
     y = torch.empty_like(x)
