@@ -97,7 +97,8 @@ int hy_gemm_config(int precision_fp32, float* splitk_ws, long splitk_floats);
 
 /* C[M,N] = beta*C + op(A) op(B)^T (+bias[N]) (+R[M,N]) with tcgen05 kind::tf32.
  * a_mn=0: A is [M][lda] (K contiguous); a_mn=1: A is [K][lda] (M contiguous). Same for B
- * with N. mode 0 store, 1 GELU (Hout = pre-activation), 2 GELU-backward (C = acc*gelu'(Hin)). */
+ * with N. mode 0 store, 1 GELU (C = gelu(acc + bias), Hout = gelu'(acc + bias)), 2 GELU-backward
+ * (C = acc * Hin, Hin = the gelu' mode 1 stored). */
 int hy_gemm(void* stream, int M, int N, int K, const float* A, long lda, int a_mn, const float* B, long ldb,
             int b_mn, float* C, long ldc, const float* bias, const float* R, long ldr, float beta, int mode,
             float* Hout, const float* Hin, long ldh);

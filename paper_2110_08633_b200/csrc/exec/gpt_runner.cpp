@@ -213,7 +213,7 @@ void block_backward_bf16(cudaStream_t st, const hy_dims& m, const float* w, floa
   }
 }
 
-// keep_h: also store the MLP pre-activation (s.fc), which only the backward's GELU' needs; the
+// keep_h: also store gelu' of the MLP pre-activation (s.fc), which only the backward's GELU' needs; the
 // forward tasks and the backward's stash recompute skip that M x 4d write. h_out == nullptr:
 // the block's output is not needed (the backward's per-block recompute, or the last block of a
 // shard without the head in the stash pass) — the MLP projection GEMM is skipped.

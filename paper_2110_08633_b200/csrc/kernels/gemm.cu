@@ -17,6 +17,10 @@ cudaError_t gemm_dispatch_m1(cudaStream_t st, int M, int N, int K, const float* 
                            long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
 cudaError_t gemm_dispatch_m2(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
                            long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
+cudaError_t gemm_dispatch_m3(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
+                           long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat, bool prec3);
+cudaError_t gemm_dispatch_b3(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
+                             const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat);
 cudaError_t gemm_dispatch_b0(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
                              const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat);
 cudaError_t gemm_dispatch_b1(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
@@ -88,12 +92,14 @@ int sm_count_host() {
 // instruction fetch).
 cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const float* A, long lda, bool a_mn, const float* B,
                      long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
+  if (e.mode == kEpiGelu && e.Hout) return gemm_dispatch_m3(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
   if (e.mode == kEpiGelu) return gemm_dispatch_m1(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
   if (e.mode == kEpiGeluBwd) return gemm_dispatch_m2(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
   return gemm_dispatch_m0(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat, t_prec3);
 }
 cudaError_t dispatch(cudaStream_t st, int M, int N, int K, const __nv_bfloat16* A, long lda, bool a_mn,
                      const __nv_bfloat16* B, long ldb, bool b_mn, const GemmEpilogue& e, const GemmBatch& bat) {
+  if (e.mode == kEpiGelu && e.Hout) return gemm_dispatch_b3(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
   if (e.mode == kEpiGelu) return gemm_dispatch_b1(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
   if (e.mode == kEpiGeluBwd) return gemm_dispatch_b2(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);
   return gemm_dispatch_b0(st, M, N, K, A, lda, a_mn, B, ldb, b_mn, e, bat);

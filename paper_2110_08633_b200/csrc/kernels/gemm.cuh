@@ -8,8 +8,10 @@ namespace hy {
 
 enum EpiMode : int {
   kEpiStore = 0,    // C = beta*C + acc (+bias) (+R)
-  kEpiGelu = 1,     // Hout = acc + bias (skipped when Hout is null) ; C = gelu(acc + bias)
-  kEpiGeluBwd = 2,  // C = (acc) * gelu'(Hin)
+  kEpiGelu = 1,     // C = gelu(acc + bias); Hout = gelu'(acc + bias) (skipped when Hout is null)
+  kEpiGeluBwd = 2,  // C = acc * Hin  (Hin = the gelu' the forward stored)
+  kEpiGeluSave = 3,  // internal: kEpiGelu with Hout set (its own instantiation: each kernel carries
+                     // only its epilogue's code, instruction fetch stalled the 2-in-1 form)
 };
 
 struct GemmEpilogue {
@@ -19,9 +21,9 @@ struct GemmEpilogue {
   const float* bias = nullptr;  // [N]
   const float* R = nullptr;     // residual [M, N]
   long ldr = 0;
-  float* Hout = nullptr;  // GELU pre-activation out
+  float* Hout = nullptr;  // gelu' of the pre-activation out (for the backward)
   long ldho = 0;
-  const float* Hin = nullptr;  // GELU pre-activation in (backward)
+  const float* Hin = nullptr;  // gelu' of the pre-activation in (backward)
   long ldhi = 0;
   float beta = 0.f;
   int mode = kEpiStore;

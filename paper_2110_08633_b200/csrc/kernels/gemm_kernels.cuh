@@ -108,9 +108,11 @@ __device__ __forceinline__ float gelu_sig(float x) {
   return __fdividef(1.f, 1.f + __expf(fminf(-2.f * u, 80.f)));
 }
 __device__ __forceinline__ float gelu_tanh(float x) { return x * gelu_sig(x); }
-__device__ __forceinline__ float gelu_tanh_grad(float x) {
+// gelu'(x) from the sigmoid gelu_tanh already computed (the forward epilogue stores it for the
+// backward, whose GELU' epilogue is then one multiply: no second sigmoid, measured 2.2x a plain
+// store at the XL fc shape when it evaluated gelu' itself).
+__device__ __forceinline__ float gelu_grad_s(float x, float sg) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float sg = gelu_sig(x);
   return fmaf(2.f * x * sg * (1.f - sg), k0 * fmaf(3.f * k1, x * x, 1.f), sg);
 }
 
@@ -279,16 +281,21 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
         const float* ae = &av[i].x;
         if constexpr (MODE == kEpiGeluBwd) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e) xe[e] = xe[e] * alpha * gelu_tanh_grad(ae[e]);
+          for (int e = 0; e < 4; ++e) xe[e] = xe[e] * alpha * ae[e];
         } else if constexpr (MODE == kEpiGelu) {
-          float4 h;
-          float* he = &h.x;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) xe[e] = gelu_tanh(xe[e] * alpha + be[e]);
+        } else if constexpr (MODE == kEpiGeluSave) {
+          float4 gd;
+          float* ge = &gd.x;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            he[e] = xe[e] * alpha + be[e];
-            xe[e] = gelu_tanh(he[e]);
+            const float h = xe[e] * alpha + be[e];
+            const float sg = gelu_sig(h);
+            xe[e] = h * sg;
+            ge[e] = gelu_grad_s(h, sg);
           }
-          if (epi.Hout) *reinterpret_cast<float4*>(epi.Hout + grow * epi.ldho + col) = h;
+          *reinterpret_cast<float4*>(epi.Hout + grow * epi.ldho + col) = gd;
         } else {
           const float* pe = &pv[i].x;
 #pragma unroll
@@ -312,11 +319,12 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
         const long grow = x0.row0 + r;
         float y = x0.stile[r * 36 + lane] * alpha;
         if constexpr (MODE == kEpiGeluBwd) {
-          y *= gelu_tanh_grad(epi.Hin[grow * epi.ldhi + colx]);
-        } else if constexpr (MODE == kEpiGelu) {
+          y *= epi.Hin[grow * epi.ldhi + colx];
+        } else if constexpr (MODE == kEpiGelu || MODE == kEpiGeluSave) {
           y += bias_v;
-          if (epi.Hout) epi.Hout[grow * epi.ldho + colx] = y;
-          y = gelu_tanh(y);
+          const float sg = gelu_sig(y);
+          if (MODE == kEpiGeluSave) epi.Hout[grow * epi.ldho + colx] = gelu_grad_s(y, sg);
+          y *= sg;
         } else {
           y += bias_v;
           if (epi.R) y += epi.R[grow * epi.ldr + colx];

@@ -93,21 +93,21 @@ def test_gemm_bf16_epilogues(M):
     # store + bias + residual (fp32 C)
     C = K.gemm_bf16(A, B, bias=bias, R=R)
     assert rel(C, base + bias + R) < 1e-5
-    # GELU forward: bf16 activation out, fp32 pre-activation
+    # GELU forward: bf16 activation out, fp32 gelu'(pre-activation) for the backward
     H = torch.empty(M, N, device=dev)
     G = K.gemm_bf16(A, B, bias=bias, mode=1, H=H, c_bf16=True)
     assert G.dtype == torch.bfloat16
     h = base + bias
-    assert rel(H, h) < 1e-5
+    hd = h.clone().requires_grad_(True)
+    torch.nn.functional.gelu(hd, approximate="tanh").backward(torch.ones_like(h))
+    assert rel(H, hd.grad) < 1e-5
     g_ref = torch.nn.functional.gelu(h, approximate="tanh")
     # bf16 rounding of the output: <= 2^-9 relative per element
     assert rel(G, g_ref) < 4e-3
     assert ((G.float() - g_ref).abs() <= g_ref.abs() * 2.0 ** -8 + 1e-6).float().mean().item() > 0.999
-    # GELU backward: C = acc * gelu'(H) as bf16
+    # GELU backward: C = acc * H (the stored gelu') as bf16
     D = K.gemm_bf16(A, B, mode=2, H=H, c_bf16=True)
-    hd = h.clone().requires_grad_(True)
-    torch.nn.functional.gelu(hd, approximate="tanh").backward(base)
-    assert rel(D, hd.grad) < 4e-3
+    assert rel(D, base * hd.grad) < 4e-3
 
 
 def test_to_bf16_is_rne():

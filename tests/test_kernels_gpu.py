@@ -134,16 +134,18 @@ def test_gemm_epilogues():
     C2 = C0.clone()
     K.gemm(A, B, C=C2, beta=1.0)
     assert rel(C2, C0 + base) < 3e-3
+    # GELU: C = gelu(pre), H = gelu'(pre) (stored for the backward)
     H = torch.empty(M, N, device=dev)
     G = K.gemm(A, B, bias=bias, mode=1, H=H)
-    pre = base + bias
-    assert rel(H, pre) < 3e-3
-    assert rel(G, torch.nn.functional.gelu(pre, approximate="tanh")) < 3e-3
+    pre = (base + bias).clone().requires_grad_(True)
+    gl = torch.nn.functional.gelu(pre, approximate="tanh")
+    gl.backward(torch.ones_like(gl))
+    assert rel(G, gl.detach()) < 3e-3
+    assert rel(H, pre.grad) < 3e-3
+    # GELU backward: C = acc * Hin
     Hin = torch.randn(M, N, device=dev)
     D = K.gemm(A, B, mode=2, H=Hin)
-    x = Hin.clone().requires_grad_(True)
-    torch.nn.functional.gelu(x, approximate="tanh").backward(torch.ones_like(x))
-    assert rel(D, base * x.grad) < 3e-3
+    assert rel(D, base * Hin) < 3e-3
 
 
 def test_gemm_vocab_head_shapes():
