@@ -347,11 +347,10 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
 template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uint32_t q, uint32_t tmem_base,
                                                 float* epi_smem, const GemmEpilogue& epi, const GemmBatch& bat,
-                                                int M, int N, int c_begin = 0, int c_end = BN / 32) {
-  static_assert((BN / 32) % 2 == 0, "chunk pairs");
+                                                int M, int N, int c_begin = 0, int c_end = BN / 32, int slot = -1) {
   EpiCtx x;
   x.lane = lane_id();
-  x.stile = epi_smem + q * (32 * 36);
+  x.stile = epi_smem + (slot < 0 ? static_cast<int>(q) : slot) * (32 * 36);
   x.st_base = smem_u32(x.stile);
   x.row0 = ti.m0 + static_cast<int>(q * 32);
   x.nrows = min(32, M - x.row0);
@@ -368,10 +367,12 @@ __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uin
   if (ti.nkb > 0) {
     tmem_ld_x32_issue(tbase + c_begin * 32, b0);
 #pragma unroll 1
-    for (int c = c_begin; c < c_end; c += 2) {  // c_end - c_begin even
+    for (int c = c_begin; c < c_end; c += 2) {
       tmem_ld_wait();
-      tmem_ld_x32_issue(tbase + (c + 1) * 32, b1);
+      const bool two = c + 1 < c_end;
+      if (two) tmem_ld_x32_issue(tbase + (c + 1) * 32, b1);
       epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
+      if (!two) break;
       tmem_ld_wait();
       if (c + 2 < c_end) tmem_ld_x32_issue(tbase + (c + 2) * 32, b0);
       epilogue_chunk<MODE>(x, b1, ti.n0 + (c + 1) * 32, epi, N);
@@ -596,19 +597,25 @@ gemm_tf32_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constan
 // L2 (vs BN x 128 B of B alone before): the shared-memory / L2 operand traffic per MMA
 // flop drops by a third at BN = 256, the bound that held the 1-CTA kernel near 0.6 of the
 // library GEMM on the workload's short-K shapes.
+// 12 warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4-11 epilogue — two warps
+// per TMEM lane quarter, each taking half of the tile's 32-column chunks. The short-K block GEMMs
+// (K = 768 at d768: ~2.5 us of bf16 MMA per 256-row tile) were bound by a 4-warp epilogue.
+constexpr int kPairEpiWarps = 8;
+constexpr int kPairThreads = 128 + 32 * kPairEpiWarps;
 template <int BN>
 struct SmemPair {
   static constexpr int kABytes = BM * BK * 4;
   static constexpr int kBBytes = (BN / 2) * BK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStagesN = (200 * 1024) / kStageBytes > 8 ? 8 : (200 * 1024) / kStageBytes;
+  static constexpr int kEpi = kPairEpiWarps * 32 * 36 * 4;
+  static constexpr int kBudget = 232448 - kEpi - 1024 - 256;  // 227 KB of dynamic smem per CTA
+  static constexpr int kStagesN = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
   static constexpr int kRing = kStagesN * kStageBytes;
-  static constexpr int kEpi = 4 * 32 * 36 * 4;
   static constexpr int kTotal = kRing + kEpi + 1024 + 256;
 };
 
 template <typename T, int BN, bool A_MN, bool B_MN, int MODE>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
                       int N, int K, GemmEpilogue epi, GemmBatch bat) {
   using L = SmemPair<BN>;
@@ -617,7 +624,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
   constexpr int BKT = E::BK, CW = E::CW;
   static_assert(!B_MN || (BN / 2) % CW == 0, "MN-major B half-tile in whole 128-byte chunks");
   constexpr int BM2 = 2 * BM;
-  constexpr int kHalfChunks = (BN / 64) * 2 == BN / 32 ? BN / 64 + ((BN / 64) & 1) : BN / 64;  // even split point
+  constexpr int kHalfChunks = (BN / 32 + 1) / 2;  // epilogue warp 4+q: chunks [0, kHalf); warp 8+q: the rest
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   float* epi_smem = reinterpret_cast<float*>(smem + L::kRing);
@@ -625,8 +632,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
-  uint64_t* lastbar = tempty + 2;  // the CTA's last accumulator is ready (epilogue warps -> warps 0-3)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lastbar + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id();
   const uint32_t rank = cluster_ctarank();
@@ -646,9 +652,8 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty[a], 2 * kPairEpiWarps);  // epilogue warps x 2 CTAs
     }
-    mbar_init(lastbar, 4);
     fence_barrier_init();
   }
   constexpr uint32_t kTmemCols = 2 * BN <= 256 ? 256 : 512;
@@ -746,24 +751,19 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       }
     }
   } else if (warp >= 4) {
-    const uint32_t q = warp - 4;
+    const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+    const int half = (static_cast<int>(warp) - 4) >> 2;
+    const int c0 = half ? kHalfChunks : 0, c1 = half ? BN / 32 : kHalfChunks;
     int local = 0;
     for (int tile = pair; tile < n_tiles; tile += n_pairs) {
       TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
       ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
       const int acc = local & 1;
-      prefetch_epilogue_rows<BN, MODE>(epi, bat, ti, ti.m0 + static_cast<int>(q * 32 + lane_id()), M, N);
+      if (half == 0) prefetch_epilogue_rows<BN, MODE>(epi, bat, ti, ti.m0 + static_cast<int>(q * 32 + lane_id()), M, N);
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       ++local;
       tc_fence_after();
-      // the CTA's last tile: warps 0-3 (done with loading / issuing) take the second half of
-      // its columns, so the one epilogue nothing overlaps runs on twice the warps
-      const bool last = tile + n_pairs >= n_tiles;
-      if (last) {  // (tfull phases are tracked here; warps 0-3 only learn of the last one)
-        __syncwarp();
-        if (lane_id() == 0) mbar_arrive(lastbar);
-      }
-      epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N, 0, last ? kHalfChunks : BN / 32);
+      epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N, c0, c1, static_cast<int>(warp) - 4);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) {
@@ -771,21 +771,6 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
         else mbar_arrive_cluster(&tempty[acc], 0);
       }
     }
-  }
-
-  if (warp < 4 && pair < n_tiles) {
-    __syncwarp();
-    const int cnt = (n_tiles - 1 - pair) / n_pairs + 1;  // tiles of this CTA
-    const int tile = pair + (cnt - 1) * n_pairs;
-    TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
-    ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
-    const int acc = (cnt - 1) & 1;
-    // not tfull itself: an early parity test on it could pass for an earlier phase
-    mbar_wait(lastbar, 0);
-    tc_fence_after();
-    // the pipeline ring is idle now (every TMA landed, every MMA read it): per-warp transposes
-    epilogue_tile_m<BN, MODE>(ti, acc, warp, tmem_base, reinterpret_cast<float*>(smem), epi, bat, M, N, kHalfChunks,
-                              BN / 32);
   }
 
   tc_fence_before();
@@ -896,7 +881,7 @@ cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const T* A, lo
   const long tiles = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
   const long pairs = std::min<long>(tiles, sm_count() / 2);
   count_launch();
-  return launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(kThreads), SmemPair<BN>::kTotal, stream, ma, mb,
+  return launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(kPairThreads), SmemPair<BN>::kTotal, stream, ma, mb,
                     M, N, K, epi, b);
 }
 
