@@ -45,6 +45,7 @@ struct GemmBatch {
   // set by the launcher: TMA dimension order {inner, b2, outer, b1} when b2's stride is
   // smaller than the row stride (e.g. heads interleaved inside a row)
   int a_perm = 0, b_perm = 0;
+  int c_tma = 0;  // set by the launcher: the CTA-pair epilogue stores C (and Hout) with TMA
 };
 
 // C[M,N] = op(A)[M,K] * op(B)[N,K]^T.

@@ -338,16 +338,79 @@ __device__ __forceinline__ void epilogue_chunk(const EpiCtx& x0, const uint32_t 
   __syncwarp();
 }
 
+// TMA-store epilogue of one 32-column chunk (CTA-pair kernel; modes with no per-element global
+// operand: store with optional bias and beta = 0, GELU, GELU + gelu'): thread = row finishes its
+// 32 values in registers (the bias chunk is one broadcast load per 4 columns), writes them to the
+// warp's staging tile in the store map's swizzled layout (128B swizzle for 32 fp32, 64B for 32
+// bf16: conflict-free 16-byte stores) and one lane issues the bulk tensor store — no shared-memory
+// transpose back, no per-lane address math, ragged edges clipped by the TMA unit.
+struct TmaEpi {
+  const CUtensorMap* map_c;
+  uint8_t* stage;     // this warp's staging tile (1024-aligned, 4 KB)
+  const float* sbias;  // this warp's bias columns in shared memory (nullptr: no bias), from col_base
+  int col_base;
+  int slice;          // split-K slice (the map's third coordinate)
+};
+template <int MODE>
+__device__ __forceinline__ void epilogue_chunk_tma(const TmaEpi& t, const uint32_t (&v)[32], int col0, int row0,
+                                                   const GemmEpilogue& epi, int N) {
+  if (col0 >= N) return;  // warp-uniform
+  const uint32_t lane = lane_id();
+  const float alpha = epi.alpha;
+  float y[32];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (t.sbias) b = lds128(smem_u32(t.sbias + (col0 - t.col_base) + 4 * k));  // broadcast
+    y[4 * k] = __uint_as_float(v[4 * k]) * alpha + b.x;
+    y[4 * k + 1] = __uint_as_float(v[4 * k + 1]) * alpha + b.y;
+    y[4 * k + 2] = __uint_as_float(v[4 * k + 2]) * alpha + b.z;
+    y[4 * k + 3] = __uint_as_float(v[4 * k + 3]) * alpha + b.w;
+  }
+  if constexpr (MODE == kEpiGelu) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) y[i] = gelu_tanh(y[i]);
+  }
+  if (lane == 0) bulk_wait_read0();  // the previous chunk's store has read the staging tile
+  __syncwarp();
+  if (epi.c16) {  // 32 bf16 = 64 B per row, 64B swizzle
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      __nv_bfloat162 h2[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(y[8 * j + 2 * e], y[8 * j + 2 * e + 1]);
+      const uint4 u = *reinterpret_cast<const uint4*>(h2);
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                       smem_u32(t.stage + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4))),
+                   "r"(u.x), "r"(u.y), "r"(u.z), "r"(u.w)
+                   : "memory");
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      sts128(smem_u32(t.stage + lane * 128 + ((j ^ (lane & 7)) << 4)),
+             make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]));
+    }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(t.map_c, t.stage, col0, row0, t.slice);
+    bulk_commit();
+  }
+}
+
 // Epilogue of one accumulator tile, run by epilogue warp q (TMEM lane quarter q), specialised
 // per mode at compile time (no per-element mode branches): TMEM -> registers (thread = row,
 // the next 32-column chunk's tcgen05.ld in flight while this one is processed) -> smem
 // transpose -> each lane takes 4 consecutive columns of a row (8 lanes per 32-column row, 4
 // rows per instruction), so bias / residual / GELU operands and the stores move as coalesced
-// 128-bit accesses.
+// 128-bit accesses. With `tma` (CTA-pair kernel, bat.c_tma): epilogue_chunk_tma instead.
 template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uint32_t q, uint32_t tmem_base,
                                                 float* epi_smem, const GemmEpilogue& epi, const GemmBatch& bat,
-                                                int M, int N, int c_begin = 0, int c_end = BN / 32, int slot = -1) {
+                                                int M, int N, int c_begin = 0, int c_end = BN / 32, int slot = -1,
+                                                const TmaEpi* tma = nullptr) {
   EpiCtx x;
   x.lane = lane_id();
   x.stile = epi_smem + (slot < 0 ? static_cast<int>(q) : slot) * (32 * 36);
@@ -371,17 +434,35 @@ __device__ __forceinline__ void epilogue_tile_m(const TileInfo& ti, int acc, uin
       tmem_ld_wait();
       const bool two = c + 1 < c_end;
       if (two) tmem_ld_x32_issue(tbase + (c + 1) * 32, b1);
-      epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
+      if constexpr (MODE == kEpiStore || MODE == kEpiGelu) {
+        if (tma) epilogue_chunk_tma<MODE>(*tma, b0, ti.n0 + c * 32, x.row0, epi, N);
+        else epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
+      } else {
+        epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
+      }
       if (!two) break;
       tmem_ld_wait();
       if (c + 2 < c_end) tmem_ld_x32_issue(tbase + (c + 2) * 32, b0);
-      epilogue_chunk<MODE>(x, b1, ti.n0 + (c + 1) * 32, epi, N);
+      if constexpr (MODE == kEpiStore || MODE == kEpiGelu) {
+        if (tma) epilogue_chunk_tma<MODE>(*tma, b1, ti.n0 + (c + 1) * 32, x.row0, epi, N);
+        else epilogue_chunk<MODE>(x, b1, ti.n0 + (c + 1) * 32, epi, N);
+      } else {
+        epilogue_chunk<MODE>(x, b1, ti.n0 + (c + 1) * 32, epi, N);
+      }
     }
   } else {
 #pragma unroll
     for (int i = 0; i < 32; ++i) b0[i] = 0u;
 #pragma unroll 1
-    for (int c = c_begin; c < c_end; ++c) epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
+    for (int c = c_begin; c < c_end; ++c) {
+      if constexpr (MODE == kEpiStore || MODE == kEpiGelu) {
+        if (tma) {
+          epilogue_chunk_tma<MODE>(*tma, b0, ti.n0 + c * 32, x.row0, epi, N);
+          continue;
+        }
+      }
+      epilogue_chunk<MODE>(x, b0, ti.n0 + c * 32, epi, N);
+    }
   }
 }
 
@@ -607,7 +688,10 @@ struct SmemPair {
   static constexpr int kABytes = BM * BK * 4;
   static constexpr int kBBytes = (BN / 2) * BK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kEpi = kPairEpiWarps * 32 * 36 * 4;
+  // per epilogue warp (1024-aligned): the 32 x 36 transpose tile, or the TMA staging tile (4 KB
+  // at +0) and the warp's bias columns (<= 128 floats at +4096)
+  static constexpr int kEpiWarp = 5120;
+  static constexpr int kEpi = kPairEpiWarps * kEpiWarp;
   static constexpr int kBudget = 232448 - kEpi - 1024 - 256;  // 227 KB of dynamic smem per CTA
   static constexpr int kStagesN = kBudget / kStageBytes > 8 ? 8 : kBudget / kStageBytes;
   static constexpr int kRing = kStagesN * kStageBytes;
@@ -616,7 +700,8 @@ struct SmemPair {
 
 template <typename T, int BN, bool A_MN, bool B_MN, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
-gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int M,
+gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                      const __grid_constant__ CUtensorMap map_c, int M,
                       int N, int K, GemmEpilogue epi, GemmBatch bat) {
   using L = SmemPair<BN>;
   using E = Elem<T>;
@@ -627,7 +712,6 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
   constexpr int kHalfChunks = (BN / 32 + 1) / 2;  // epilogue warp 4+q: chunks [0, kHalf); warp 8+q: the rest
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  float* epi_smem = reinterpret_cast<float*>(smem + L::kRing);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kRing + L::kEpi);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
@@ -646,6 +730,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
   if (warp == 0 && elect_one()) {
     tma_prefetch_desc(&map_a);
     tma_prefetch_desc(&map_b);
+    if (bat.c_tma) tma_prefetch_desc(&map_c);
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -754,6 +839,9 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
     const int half = (static_cast<int>(warp) - 4) >> 2;
     const int c0 = half ? kHalfChunks : 0, c1 = half ? BN / 32 : kHalfChunks;
+    uint8_t* wsm = smem + L::kRing + (static_cast<int>(warp) - 4) * L::kEpiWarp;
+    TmaEpi te{&map_c, wsm, nullptr, 0, 0};
+    float* sbias = reinterpret_cast<float*>(wsm + 4096);
     int local = 0;
     for (int tile = pair; tile < n_tiles; tile += n_pairs) {
       TileInfo ti = tile_info<BN, BKT>(tile, tiles_m, tiles_n, M, N, K, bat.nb2, bat.causal, bat.nb1);
@@ -763,7 +851,19 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       mbar_wait(&tfull[acc], (local >> 1) & 1);
       ++local;
       tc_fence_after();
-      epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, epi_smem, epi, bat, M, N, c0, c1, static_cast<int>(warp) - 4);
+      te.slice = bat.causal == kSplitK ? ti.z1 : 0;
+      if (bat.c_tma && epi.bias) {  // this warp's bias columns -> shared memory (read as broadcasts)
+        te.col_base = ti.n0 + c0 * 32;
+        __syncwarp();  // the previous tile's chunks have read the old values
+        for (int i = static_cast<int>(lane_id()); i < (c1 - c0) * 32; i += 32) {
+          const int col = te.col_base + i;
+          sbias[i] = col < N ? epi.bias[col] : 0.f;
+        }
+        __syncwarp();
+        te.sbias = sbias;
+      }
+      epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, reinterpret_cast<float*>(wsm), epi, bat, M, N, c0, c1, 0,
+                                bat.c_tma ? &te : nullptr);
       tc_fence_before();
       __syncwarp();
       if (lane_id() == 0) {
@@ -771,6 +871,7 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
         else mbar_arrive_cluster(&tempty[acc], 0);
       }
     }
+    if (bat.c_tma && lane_id() == 0) bulk_wait0();  // this warp's stores complete before exit
   }
 
   tc_fence_before();
@@ -867,21 +968,58 @@ cudaError_t launch(cudaStream_t stream, int M, int N, int K, const T* A, long ld
   return launch_pdl(kern, dim3(grid), dim3(kThreads), Smem<BN, P3>::kTotal, stream, ma, mb, M, N, K, epi, b);
 }
 
+// Store map of C [slices][rows][ld] for the TMA epilogue: box 32 columns x 32 rows x 1 slice,
+// 128B swizzle for fp32 (128-byte box rows), 64B for bf16; split-K partials are the slices (each
+// clips at its own last row).
+bool make_store_map(CUtensorMap* map, void* ptr, long cols, long rows, long ld, long slices, bool c16) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const long es = c16 ? 2 : 4;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(slices)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld * es), static_cast<cuuint64_t>(ld * rows * es)};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(map, c16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, c16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool tma_store_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HY_GEMM_TMA_STORE");  // experiments: 0 = per-lane global stores
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename T, int BN, bool A_MN, bool B_MN, int MODE>
 cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const T* A, long lda, const T* B, long ldb,
                         const GemmEpilogue& epi, const GemmBatch& bat) {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc;
   GemmBatch b = bat;
   if (!make_operand_maps(&ma, &mb, b, M, N, K, A, lda, A_MN, B, ldb, B_MN, BN / 2)) return cudaErrorInvalidValue;
+  // TMA-store epilogue: store (bias allowed, no residual, beta = 0) and GELU without the gelu'
+  // store, unbatched (split-K partials are the map's slices), 16-byte aligned rows. The other
+  // epilogues read per-element global operands (R, C, gelu') and keep the transposed path.
+  const long es = epi.c16 ? 2 : 4;
+  const bool split = b.causal == kSplitK;
+  bool tma = tma_store_enabled() && (MODE == kEpiStore || MODE == kEpiGelu) && !epi.R && epi.beta == 0.f &&
+             b.nb2 == 1 && (b.causal == kCausalNone || split) && (b.nb1 == 1 || split) && M >= 32 && N >= 32 &&
+             (reinterpret_cast<uintptr_t>(epi.C) & 15) == 0 && (epi.ldc * es) % 16 == 0 &&
+             (!split || b.c_s1 == static_cast<long>(M) * epi.ldc);
+  if (tma) tma = make_store_map(&mc, epi.C, N, M, epi.ldc, split ? b.nb1 : 1, epi.c16 != 0);
+  b.c_tma = tma ? 1 : 0;
+  if (!tma) mc = ma;  // unused
+  using L = SmemPair<BN>;
   auto kern = gemm_tf32_pair_kernel<T, BN, A_MN, B_MN, MODE>;
   {
-    const cudaError_t e = ensure_smem_limit(kern, SmemPair<BN>::kTotal);
+    const cudaError_t e = ensure_smem_limit(kern, L::kTotal);
     if (e != cudaSuccess) return e;
   }
   const long tiles = static_cast<long>((M + 2 * BM - 1) / (2 * BM)) * ((N + BN - 1) / BN) * bat.nb1 * bat.nb2;
   const long pairs = std::min<long>(tiles, sm_count() / 2);
   count_launch();
-  return launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(kPairThreads), SmemPair<BN>::kTotal, stream, ma, mb,
+  return launch_pdl(kern, dim3(static_cast<unsigned>(2 * pairs)), dim3(kPairThreads), L::kTotal, stream, ma, mb, mc,
                     M, N, K, epi, b);
 }
 
