@@ -998,9 +998,10 @@ cudaError_t launch_pair(cudaStream_t stream, int M, int N, int K, const T* A, lo
   CUtensorMap ma, mb, mc;
   GemmBatch b = bat;
   if (!make_operand_maps(&ma, &mb, b, M, N, K, A, lda, A_MN, B, ldb, B_MN, BN / 2)) return cudaErrorInvalidValue;
-  // TMA-store epilogue: store (bias allowed, no residual, beta = 0) and GELU without the gelu'
-  // store, unbatched (split-K partials are the map's slices), 16-byte aligned rows. The other
-  // epilogues read per-element global operands (R, C, gelu') and keep the transposed path.
+  // TMA-store epilogue: store (bias allowed; no residual, beta = 0) and GELU without the gelu'
+  // store, unbatched (split-K partials are the map's slices), 16-byte aligned rows. The residual,
+  // beta != 0, GELU' and the gelu' store keep the transposed path (a thread-per-row residual read
+  // measured slower: C2 o_proj bf16 18.7 -> 24.4 us, profiles/r02_epilogue/residual_tma.json).
   const long es = epi.c16 ? 2 : 4;
   const bool split = b.causal == kSplitK;
   bool tma = tma_store_enabled() && (MODE == kEpiStore || MODE == kEpiGelu) && !epi.R && epi.beta == 0.f &&

@@ -46,6 +46,18 @@ def main():
         }
         r["mma_only_us_at_1.4PF"] = round(2.0 * M * N * Kd / 1.4e15 * 1e6, 1)
         out[name] = r
+    # bias + residual (the attention / MLP output projections), TF32 and bf16 operands
+    for name, (M, N, Kd) in {"c2 o_proj": (4096, 768, 768), "c2 mlp_proj": (4096, 768, 3072),
+                             "xl mlp_proj": (16384, 1600, 6400)}.items():
+        A = torch.randn(M, Kd, device=dev)
+        B = torch.randn(N, Kd, device=dev) * 0.05
+        bias = torch.randn(N, device=dev)
+        R = torch.randn(M, N, device=dev)
+        C = torch.empty(M, N, device=dev)
+        A16, B16 = A.to(torch.bfloat16), B.to(torch.bfloat16)
+        out[name] = {"tf32_bias_res": timeit(lambda: K.gemm(A, B, C=C, bias=bias, R=R)),
+                     "bf16_bias_res": timeit(lambda: K.gemm_bf16(A16, B16, C=C, bias=bias, R=R)),
+                     "bf16_plain": timeit(lambda: K.gemm_bf16(A16, B16, C=C))}
     print(json.dumps(out))
 
 
