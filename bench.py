@@ -260,6 +260,29 @@ def live_gemm_roofline(torch, cfg, peak):
                      "frac_of_nominal_tf32": round(ach / 1100.0, 4),
                      "traffic": traffic.get((e["name"], tuple(e["shape"]))),
                      "algorithmic_bytes": e["algorithmic_bytes"], "launch_us": round(e["seconds"] * 1e6, 2)})
+    # the bf16 precision's GEMM (tcgen05 kind::f16) against the driver-measured bf16 peak
+    # (MEASURED_PEAKS.json, burst: a kernel timed alone): the C2 fc shape and GPT-2 XL's fc shape
+    # (C3's block GEMMs), plain fp32 store
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            bf16_peak = float(json.load(f)["bf16_tflops"])
+    except (OSError, ValueError, KeyError):
+        bf16_peak = None
+    if bf16_peak:
+        for name, (Mb, Nb, Kb) in (("bf16_fc_c2", (M, 4 * d, d)), ("bf16_fc_xl", (16384, 6400, 1600))):
+            A = torch.randn(Mb, Kb, device=dev).to(torch.bfloat16)
+            B = torch.randn(Nb, Kb, device=dev).to(torch.bfloat16)
+            C = torch.empty(Mb, Nb, device=dev)
+            t = _time_launches(torch, lambda: K.gemm_bf16(A, B, C=C))
+            ach = 2.0 * Mb * Nb * Kb / t / 1e12
+            recs.append({"bound": "tensor", "kernel": f"gemm_tf32_pair_kernel<bf16> [{Mb}x{Nb}x{Kb}] (tcgen05 kind::f16, "
+                         "cta_group::2, TMA-store epilogue)", "achieved": round(ach, 1), "peak": round(bf16_peak, 1),
+                         "unit": "TFLOP/s", "frac": round(ach / bf16_peak, 4),
+                         "peak_source": "MEASURED_PEAKS.json bf16_tflops (driver-measured cuBLAS bf16 8192^3, burst)",
+                         "traffic": traffic.get((name, (Mb, Nb, Kb))),
+                         "algorithmic_bytes": int(2 * (Mb * Kb + Nb * Kb) + 4 * Mb * Nb),
+                         "launch_us": round(t * 1e6, 2)})
+            del A, B, C
     top = dict(recs[0])
     top["others"] = recs[1:]
     return top
