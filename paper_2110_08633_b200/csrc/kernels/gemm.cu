@@ -116,7 +116,10 @@ cudaError_t gemm_run(cudaStream_t stream, int M, int N, int K, const T* A, long 
   if ((lda % kAlign) || (ldb % kAlign) || (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(B) & 15)) {
     return cudaErrorInvalidValue;
   }
-  if (epi.c16 && (epi.beta != 0.f || batch || (epi.ldc & 3))) return cudaErrorInvalidValue;
+  // bf16 C: stored 4 values (8 bytes) per lane, so 8-byte aligned rows
+  if (epi.c16 && (epi.beta != 0.f || batch || (epi.ldc & 3) || (reinterpret_cast<uintptr_t>(epi.C) & 7))) {
+    return cudaErrorInvalidValue;
+  }
   GemmBatch bat = batch ? *batch : GemmBatch{};
   GemmEpilogue e = epi;
   // Split K when the output has too few tiles to fill the GPU (e.g. the LM-head dz GEMM:
