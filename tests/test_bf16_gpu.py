@@ -150,3 +150,39 @@ def test_executor_bf16_toy_vs_oracle(tmp_path):
         d32 = np.linalg.norm(params32[j] - params[j]) / np.linalg.norm(params[j])
         assert d16 < 4e-3, d16
         assert d16 < d32, (d16, d32)
+
+
+@pytest.mark.parametrize("M,N,Kd", [(333, 200, 96), (4100, 3080, 768), (1000, 520, 256)])
+def test_gemm_ragged_epilogues_both_precisions(M, N, Kd):
+    """Ragged M / N through the CTA-pair kernel's epilogues (the TMA-store path clips the tile
+    edges; bias columns past N are never read): store + bias, GELU (+ gelu') with fp32 and bf16
+    outputs, GELU', for TF32 and bf16 operands."""
+    torch.manual_seed(M + N)
+    A = torch.randn(M, Kd, device=dev)
+    B = torch.randn(N, Kd, device=dev) * 0.05
+    bias = torch.randn(N, device=dev)
+    for prec in ("tf32", "bf16"):
+        if prec == "bf16":
+            A_, B_ = bf(A), bf(B)
+            base = A_.float() @ B_.float().T
+            run = lambda **kw: K.gemm_bf16(A_, B_, **kw)  # noqa: E731
+            tol = 1e-5
+        else:
+            base = A @ B.T
+            run = lambda **kw: K.gemm(A, B, **kw)  # noqa: E731
+            tol = 3e-3
+        C = run(bias=bias)
+        assert rel(C, base + bias) < tol, (prec, "bias")
+        pre = (base + bias).clone().requires_grad_(True)
+        gl = torch.nn.functional.gelu(pre, approximate="tanh")
+        gl.backward(torch.ones_like(gl))
+        G = run(bias=bias, mode=1)
+        assert rel(G, gl.detach()) < max(tol, 1e-5) * 3, (prec, "gelu")
+        H = torch.empty(M, N, device=dev)
+        G2 = run(bias=bias, mode=1, H=H)
+        assert rel(G2, gl.detach()) < max(tol, 1e-5) * 3 and rel(H, pre.grad) < max(tol, 1e-5) * 3, (prec, "gelu+h")
+        if prec == "bf16":
+            G16 = run(bias=bias, mode=1, c_bf16=True)
+            assert rel(G16, gl.detach()) < 4e-3
+        D = run(mode=2, H=H)
+        assert rel(D, base * H) < max(tol, 1e-5) * 3, (prec, "gelu'")
