@@ -848,12 +848,9 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
       ti.m0 = ti.m0 * 2 + static_cast<int>(rank) * BM;
       const int acc = local & 1;
       if (half == 0) prefetch_epilogue_rows<BN, MODE>(epi, bat, ti, ti.m0 + static_cast<int>(q * 32 + lane_id()), M, N);
-      mbar_wait(&tfull[acc], (local >> 1) & 1);
-      ++local;
-      tc_fence_after();
       te.slice = bat.causal == kSplitK ? ti.z1 : 0;
-      if (bat.c_tma && epi.bias) {  // this warp's bias columns -> shared memory (read as broadcasts)
-        te.col_base = ti.n0 + c0 * 32;
+      if (bat.c_tma && epi.bias) {  // this warp's bias columns -> shared memory (read as broadcasts),
+        te.col_base = ti.n0 + c0 * 32;  // loaded while the accumulator is still being computed
         __syncwarp();  // the previous tile's chunks have read the old values
         for (int i = static_cast<int>(lane_id()); i < (c1 - c0) * 32; i += 32) {
           const int col = te.col_base + i;
@@ -862,6 +859,9 @@ gemm_tf32_pair_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
         __syncwarp();
         te.sbias = sbias;
       }
+      mbar_wait(&tfull[acc], (local >> 1) & 1);
+      ++local;
+      tc_fence_after();
       epilogue_tile_m<BN, MODE>(ti, acc, q, tmem_base, reinterpret_cast<float*>(wsm), epi, bat, M, N, c0, c1, 0,
                                 bat.c_tma ? &te : nullptr);
       tc_fence_before();
