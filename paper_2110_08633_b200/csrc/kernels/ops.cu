@@ -1395,8 +1395,14 @@ cudaError_t embed_rows_to_host(cudaStream_t s, long max_rows, const int* count, 
                                const float* cp, const void* cm, const void* cv, float* hp, void* hm, void* hv,
                                bool bf16) {
   count_launch();
-  // few CTAs: host-link bound, and small enough not to crowd the compute kernels
-  const int grid = static_cast<int>(std::min<long>(32, (max_rows * d + 255) / 256));
+  // few CTAs: host-link bound, and small enough not to crowd the compute kernels (every SM a CTA
+  // of this kernel sits on cannot host a CTA of the persistent GEMMs until it finishes)
+  static const int max_ctas = [] {
+    const char* e = std::getenv("HY_ROWS_TO_HOST_CTAS");  // diagnostics
+    const int v = e ? std::atoi(e) : 0;
+    return v > 0 ? v : 32;
+  }();
+  const int grid = static_cast<int>(std::min<long>(max_ctas, (max_rows * d + 255) / 256));
   if (bf16) {
     rows_to_host_kernel<2><<<grid, 256, 0, s>>>(count, rows, d, cp, cm, cv, hp, hm, hv);
   } else {
