@@ -389,20 +389,27 @@ void carve_scratch(const hy_dims& m, int max_blocks, float* base, Scratch* s, bo
   s->ln2 = take(M * d);
   s->mean2 = take(M);
   s->rstd2 = take(M);
-  // fc and act are adjacent: the head's logits chunk aliases both.
+  // fc, act and tmp_h are adjacent: the head's logits chunk aliases them. tmp_h is free during
+  // the head's chunk loop (a block output held there is read by ln_f before it; the backward's
+  // dh is written after it). Chunks are balanced and rounded up to 256 rows (a CTA-pair tile row)
+  // when that still fits: C2's 4096 tokens go in 8 chunks of 512 rows instead of 8 x 500 + 96.
   s->fc = take(4 * M * d);
   s->act = take(4 * M * d);
-  // Head logits chunk: aliases fc+act when at least 16 rows fit there, else its own region.
-  const long alias_rows = std::min<long>(M, 8 * M * d / HY_VOCAB_PAD);
-  const bool alias_logits = alias_rows >= std::min<long>(M, 16);
+  s->tmp_h = take(M * d);
+  const long span = (s->tmp_h + M * d) - s->fc;
+  const long cap = std::min<long>(M, span / HY_VOCAB_PAD);
+  const bool alias_logits = cap >= std::min<long>(M, 16);
   if (alias_logits) {
+    const long chunks = (M + cap - 1) / cap;
+    long rows = (M + chunks - 1) / chunks;
+    const long r256 = (rows + 255) / 256 * 256;
+    if (r256 <= cap) rows = r256;
     s->logits = s->fc;
-    s->logits_rows = static_cast<int>(alias_rows);
+    s->logits_rows = static_cast<int>(rows);
   } else {
     s->logits_rows = static_cast<int>(std::min<long>(M, 16));
     s->logits = take(static_cast<long>(s->logits_rows) * HY_VOCAB_PAD);
   }
-  s->tmp_h = take(M * d);
   s->ws = take(512L * 4 * d);  // >= colsum_blocks(M) * max(4d, 2d)
   // the head's ln_f output and its gradient alias the QKV buffer (3 M d): the head pass runs
   // when no block intermediates are live (before the blocks' recompute in a backward, after
